@@ -1,0 +1,214 @@
+/*
+ * cacheopt.h -- C ABI of the B200-native CacheOPT hot path.
+ *
+ * The reference (`/root/reference/pkg/src/kvcsim`, pure Python) has no FFI:
+ * its "operator" boundary is the engine object (engine.py:222-672) that owns
+ * the request table and the KV pool and calls `plan_batch` once per step
+ * (engine.py:616, scheduler.py:939).  This header is the boundary a
+ * maintainer would bind instead (ctypes stub in INTEGRATION.md): one opaque
+ * engine instance per (device, stream), plain pointers and sizes only, no
+ * torch types, no C++ exceptions across the ABI.  Every entry point names the
+ * reference interface it replaces.
+ *
+ * Status codes: CO_OK (0), CO_EINVAL (unsupported / invalid input, see
+ * co_last_error), CO_ECUDA (a CUDA error), CO_EDEVICE (the device engine
+ * raised the equivalent of a reference exception, e.g. the no-progress guard
+ * engine.py:653-656).
+ */
+#ifndef CACHEOPT_H
+#define CACHEOPT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CO_OK 0
+#define CO_EINVAL 1
+#define CO_ECUDA 2
+#define CO_EDEVICE 3
+
+/* lifecycle codes (core.py:26-30); PENDING = not yet arrived */
+#define CO_PENDING 0
+#define CO_WAITING 1
+#define CO_RUNNING 2
+#define CO_PREEMPTED 3
+#define CO_COMPLETED 4
+
+#define CO_SWAP 0
+#define CO_RECOMPUTE 1
+
+/* event kinds (engine.py:338-340 and its call sites) */
+#define CO_EV_ARRIVE 0   /* engine.py:353 */
+#define CO_EV_ADMIT 1    /* engine.py:520 */
+#define CO_EV_ITER 2     /* engine.py:630-633 */
+#define CO_EV_PREEMPT 3  /* engine.py:383-384 */
+#define CO_EV_READMIT 4  /* engine.py:401-402 */
+#define CO_EV_COMPLETE 5 /* engine.py:412 */
+
+#define CO_CAUSE_PLAN 0
+#define CO_CAUSE_SQUEEZE 1
+#define CO_CAUSE_COLLISION 2
+
+#define CO_MAX_SLO_EDGES 8
+
+/* Scalars of EngineConfig (engine.py:66-79), SchedulerConfig
+ * (scheduler.py:34-48), BucketConfig (preemption.py:19-28) and the
+ * per-run constants the reference derives from floats at engine init.
+ * The host evaluates every float expression with Python's own IEEE double
+ * semantics and passes the results; the device only does integer work plus
+ * the two double expressions it evaluates with round-to-nearest intrinsics
+ * (iteration latency, costmodel.py:51-55). */
+typedef struct co_config {
+    int64_t capacity_tokens;        /* engine.py:67 */
+    int32_t reserved_blocks;        /* engine.py:68 */
+    int32_t allow_stacking;         /* engine.py:69; must be 0 (EINVAL otherwise) */
+    int32_t block_size;             /* small_block_b, engine.py:236 */
+    int32_t buffer_b;               /* scheduler.py:41 */
+    int32_t token_budget;           /* scheduler.py:39 */
+    int32_t preallocate_m;          /* scheduler.py:40 */
+    int32_t decode_runway_iters;    /* scheduler.py:44 */
+    int32_t victim_rule_fcfs;       /* scheduler.py:42: 0 = "slo", 1 = "fcfs" */
+    int64_t epsilon_us;             /* scheduler.py:38 */
+    int32_t n_slo_edges;            /* preemption.py:21-26 */
+    int32_t token_step;             /* preemption.py:27 */
+    int64_t slo_edges_us[CO_MAX_SLO_EDGES];
+    double iter_base_ms;            /* costmodel.py:21 */
+    double iter_per_token_ms;       /* costmodel.py:22 */
+    int64_t horizon_factor;         /* engine.py:76 */
+    int32_t validate_every;         /* engine.py:77 */
+    int32_t record_events;          /* engine.py:78 */
+    int32_t padding;                /* estimation.py:139-142 for the run's confidence */
+    int32_t _pad0;
+    int64_t s_star;                 /* scheduler.py:381-393 sweet spot */
+    int64_t t_i_init_us;            /* engine.py:268-270 */
+} co_config;
+
+/* One trace, any order (the library sorts by (arrival_us, id) like
+ * engine.py:241).  err_draw/flip_draw are the predictor noise draws of
+ * estimation.py:76-99 in (arrival, id) order, i.e. aligned with the SORTED
+ * order; the host produces them from numpy's default_rng([seed, 3]) stream
+ * exactly as engine.py:267/348 consumes it. */
+typedef struct co_trace {
+    int64_t n;
+    const int64_t* req_id;
+    const int64_t* arrival_us;
+    const int32_t* prompt_len;
+    const int32_t* true_output_len;
+    const int64_t* slo_ttft_us;
+    const int64_t* slo_tbt_us;
+    const int32_t* err_draw;        /* sorted order */
+    const uint8_t* flip_draw;       /* sorted order */
+} co_trace;
+
+/* Host-evaluated integer lookup tables over sequence length S in [0, s_max]
+ * (index 0 unused): the float cost models of costmodel.py:58-69 /
+ * preemption.py:94-116 rounded exactly as the reference rounds them. */
+typedef struct co_luts {
+    int64_t s_max;
+    const int64_t* swap_half_us;    /* to_us(swap_latency(S)/2)      engine.py:372,392 */
+    const int64_t* recompute_us;    /* to_us(recompute_latency(S))   engine.py:395-397 */
+    const int64_t* survive_swap_us; /* int(L_s(S)*1000+0.5)          scheduler.py:368-374 */
+    const int64_t* survive_rec_us;  /* int(L_r(S)*1000+0.5)          scheduler.py:368-374 */
+} co_luts;
+
+/* Engine-level scalars (engine.py:243-270 state), read back after a step. */
+typedef struct co_scalars {
+    int64_t now_us;
+    int64_t horizon_us;
+    int64_t first_arrival_us;
+    int64_t t_i_max_us;
+    int64_t footprint_tokens;       /* kvc.py:101 */
+    int64_t granted_tokens;         /* kvc.py:105 */
+    int64_t used_tokens;            /* kvc.py:109 */
+    int64_t generated_total;
+    int64_t iterations;
+    int64_t steps;
+    int64_t record_seq;
+    int64_t n_events;               /* undrained events on the device */
+    int64_t n_samples;
+    int32_t reserved_blocks_current;/* kvc.py:79 */
+    int32_t n_live;
+    int32_t n_pending;
+    int32_t done;
+    int32_t stalled;
+    int32_t last_step_result;       /* return value of engine.py:606 step() */
+    int32_t error;
+    int32_t _pad0;
+} co_scalars;
+
+/* Fixed-size event record; host turns it into the reference dict. */
+typedef struct co_event {
+    int32_t kind;
+    int32_t idx;        /* request index (sorted order); ITER: member count */
+    int64_t t;
+    int64_t a;          /* ITER: end; PREEMPT: kv; READMIT: ready_at */
+    int64_t b;          /* ITER: tokens; PREEMPT: strategy */
+    int64_t c;          /* ITER: offset into the member stream; PREEMPT: cause */
+} co_event;
+
+/* Per-request state readback (sorted order), field by field. */
+typedef enum co_field {
+    CO_F_STATE = 0, CO_F_GENERATED, CO_F_USED, CO_F_KV_NEED, CO_F_PREFILL_DONE,
+    CO_F_PREEMPTION_COUNT, CO_F_PREEMPTION_TIME, CO_F_FIRST_TOKEN, CO_F_LAST_TOKEN,
+    CO_F_MAX_TBT, CO_F_READY_AT, CO_F_PREEMPT_STARTED, CO_F_SWAP_OUT_DONE,
+    CO_F_LAST_STRATEGY, CO_F_FIRST_START, CO_F_COMPLETION, CO_F_ALLOCATED_KVC,
+    CO_F_PREDICTED, CO_F_ESTIMATED, CO_F_HOLDS, CO_F_GRANTED, CO_F_HOST,
+    CO_F_EMBED_OFFSET, CO_F_RESERVED_DRAWN, CO_F_RECORD_SEQ, CO_F_CLAIM_WAITER,
+    CO_F_SORTED_ORDER, CO_F_COUNT
+} co_field;
+
+typedef struct co_engine co_engine;
+
+/* engine.py:225-271 Engine.__init__ (plus the host-derived constants).
+ * device < 0 keeps the current device. */
+int co_create(const co_config* cfg, const co_trace* trace, const co_luts* luts,
+              int device, co_engine** out);
+/* releases every device/pinned buffer of the instance */
+int co_destroy(co_engine* eng);
+
+/* engine.py:606-641 Engine.step(): one scheduling round on the device.
+ * *result receives step()'s boolean. */
+int co_step(co_engine* eng, int32_t* result);
+
+/* engine.py:643-661 Engine.run() loop including the no-progress guard,
+ * executed as CUDA-graph launches of `steps_per_launch` device steps.
+ * max_steps <= 0 means until done.  *steps_done = step() calls made. */
+int co_run(co_engine* eng, int64_t max_steps, int32_t steps_per_launch, int64_t* steps_done);
+
+/* engine.py:360-384 Engine._preempt(rid, strategy, now, cause) on the device
+ * (white-box hook used by the reference's own engine tests). */
+int co_preempt(co_engine* eng, int64_t idx, int32_t strategy, int64_t now_us, int32_t cause);
+
+/* Blocking readbacks into caller-owned host buffers. */
+int co_get_scalars(co_engine* eng, co_scalars* out);
+int co_read_field(co_engine* eng, int32_t field, int64_t* out /* n values */);
+/* Drains up to max_events events (and their iter member streams) into the
+ * caller's buffers; returns counts.  members: (idx, tokens) int32 pairs. */
+int co_drain_events(co_engine* eng, co_event* events, int64_t max_events,
+                    int32_t* members, int64_t max_members,
+                    int64_t* n_events, int64_t* n_members);
+int co_pending_events(co_engine* eng, int64_t* n_events, int64_t* n_members);
+/* per-iteration (footprint, used) samples (engine.py:636), drained */
+int co_drain_samples(co_engine* eng, int64_t* out /* 2 per sample */, int64_t max, int64_t* n);
+/* token timestamps: offsets[n+1] and the Σ true_output_len slab; callers
+ * use generated[i] to know how many entries of request i are valid. */
+int co_read_token_times(co_engine* eng, int64_t* offsets, int64_t* times);
+/* kvc.py:336-375 BlockPool.check_invariants on the device; CO_EDEVICE on
+ * a violation with the reason in co_last_error(). */
+int co_check_invariants(co_engine* eng);
+
+/* Device time of the last co_run/co_step launch sequence (CUDA events on
+ * the engine stream), milliseconds. */
+int co_last_device_ms(co_engine* eng, double* ms);
+/* Number of kernels one device step launches (for gpu_launches accounting). */
+int co_kernels_per_step(co_engine* eng, int32_t* n);
+
+const char* co_last_error(void);
+const char* co_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CACHEOPT_H */

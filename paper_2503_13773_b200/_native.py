@@ -1,0 +1,127 @@
+"""ctypes binding of include/cacheopt.h (the in-tree libcacheopt.so).
+
+There is no CPU fallback: if the shared library is missing or cannot be
+loaded, importing the engine raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libcacheopt.so"
+
+CO_OK, CO_EINVAL, CO_ECUDA, CO_EDEVICE = 0, 1, 2, 3
+MAX_SLO_EDGES = 8
+
+EV_ARRIVE, EV_ADMIT, EV_ITER, EV_PREEMPT, EV_READMIT, EV_COMPLETE = range(6)
+CAUSES = ("plan", "squeeze", "collision")
+
+FIELDS = ("STATE GENERATED USED KV_NEED PREFILL_DONE PREEMPTION_COUNT PREEMPTION_TIME "
+          "FIRST_TOKEN LAST_TOKEN MAX_TBT READY_AT PREEMPT_STARTED SWAP_OUT_DONE LAST_STRATEGY "
+          "FIRST_START COMPLETION ALLOCATED_KVC PREDICTED ESTIMATED HOLDS GRANTED HOST "
+          "EMBED_OFFSET RESERVED_DRAWN RECORD_SEQ CLAIM_WAITER SORTED_ORDER").split()
+FIELD = {name: k for k, name in enumerate(FIELDS)}
+
+I64P = C.POINTER(C.c_int64)
+I32P = C.POINTER(C.c_int32)
+U8P = C.POINTER(C.c_uint8)
+
+
+class CoConfig(C.Structure):
+    _fields_ = [
+        ("capacity_tokens", C.c_int64), ("reserved_blocks", C.c_int32), ("allow_stacking", C.c_int32),
+        ("block_size", C.c_int32), ("buffer_b", C.c_int32), ("token_budget", C.c_int32),
+        ("preallocate_m", C.c_int32), ("decode_runway_iters", C.c_int32), ("victim_rule_fcfs", C.c_int32),
+        ("epsilon_us", C.c_int64), ("n_slo_edges", C.c_int32), ("token_step", C.c_int32),
+        ("slo_edges_us", C.c_int64 * MAX_SLO_EDGES), ("iter_base_ms", C.c_double),
+        ("iter_per_token_ms", C.c_double), ("horizon_factor", C.c_int64), ("validate_every", C.c_int32),
+        ("record_events", C.c_int32), ("padding", C.c_int32), ("_pad0", C.c_int32), ("s_star", C.c_int64),
+        ("t_i_init_us", C.c_int64),
+    ]
+
+
+class CoTrace(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64), ("req_id", I64P), ("arrival_us", I64P), ("prompt_len", I32P),
+        ("true_output_len", I32P), ("slo_ttft_us", I64P), ("slo_tbt_us", I64P), ("err_draw", I32P),
+        ("flip_draw", U8P),
+    ]
+
+
+class CoLuts(C.Structure):
+    _fields_ = [("s_max", C.c_int64), ("swap_half_us", I64P), ("recompute_us", I64P),
+                ("survive_swap_us", I64P), ("survive_rec_us", I64P)]
+
+
+class CoScalars(C.Structure):
+    _fields_ = [
+        ("now_us", C.c_int64), ("horizon_us", C.c_int64), ("first_arrival_us", C.c_int64),
+        ("t_i_max_us", C.c_int64), ("footprint_tokens", C.c_int64), ("granted_tokens", C.c_int64),
+        ("used_tokens", C.c_int64), ("generated_total", C.c_int64), ("iterations", C.c_int64),
+        ("steps", C.c_int64), ("record_seq", C.c_int64), ("n_events", C.c_int64), ("n_samples", C.c_int64),
+        ("reserved_blocks_current", C.c_int32), ("n_live", C.c_int32), ("n_pending", C.c_int32),
+        ("done", C.c_int32), ("stalled", C.c_int32), ("last_step_result", C.c_int32), ("error", C.c_int32),
+        ("_pad0", C.c_int32),
+    ]
+
+
+class CoEvent(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("idx", C.c_int32), ("t", C.c_int64), ("a", C.c_int64),
+                ("b", C.c_int64), ("c", C.c_int64)]
+
+
+EXPORTS = (
+    "co_create", "co_destroy", "co_step", "co_run", "co_preempt", "co_get_scalars", "co_read_field",
+    "co_drain_events", "co_pending_events", "co_drain_samples", "co_read_token_times",
+    "co_check_invariants", "co_last_device_ms", "co_kernels_per_step", "co_last_error", "co_version",
+)
+
+_lib = None
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def load() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = os.environ.get("CACHEOPT_LIB", str(LIB_PATH))
+    if not os.path.exists(path):
+        raise NativeError(f"libcacheopt.so not built at {path}: run __graft_entry__.build()")
+    lib = C.CDLL(path)
+    V = C.c_void_p
+    sig = {
+        "co_create": (C.c_int, [C.POINTER(CoConfig), C.POINTER(CoTrace), C.POINTER(CoLuts), C.c_int,
+                                C.POINTER(V)]),
+        "co_destroy": (C.c_int, [V]),
+        "co_step": (C.c_int, [V, I32P]),
+        "co_run": (C.c_int, [V, C.c_int64, C.c_int32, I64P]),
+        "co_preempt": (C.c_int, [V, C.c_int64, C.c_int32, C.c_int64, C.c_int32]),
+        "co_get_scalars": (C.c_int, [V, C.POINTER(CoScalars)]),
+        "co_read_field": (C.c_int, [V, C.c_int32, I64P]),
+        "co_drain_events": (C.c_int, [V, C.POINTER(CoEvent), C.c_int64, I32P, C.c_int64, I64P, I64P]),
+        "co_pending_events": (C.c_int, [V, I64P, I64P]),
+        "co_drain_samples": (C.c_int, [V, I64P, C.c_int64, I64P]),
+        "co_read_token_times": (C.c_int, [V, I64P, I64P]),
+        "co_check_invariants": (C.c_int, [V]),
+        "co_last_device_ms": (C.c_int, [V, C.POINTER(C.c_double)]),
+        "co_kernels_per_step": (C.c_int, [V, I32P]),
+        "co_last_error": (C.c_char_p, []),
+        "co_version": (C.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != CO_OK:
+        msg = _lib.co_last_error().decode() if _lib is not None else ""
+        kind = {CO_EINVAL: ValueError, CO_EDEVICE: RuntimeError}.get(rc, NativeError)
+        raise kind(f"{what}: {msg}")

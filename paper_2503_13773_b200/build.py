@@ -1,0 +1,43 @@
+"""Builds libcacheopt.so in-tree for sm_100a with nvcc (no JIT cache)."""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+SRC = PKG / "csrc" / "cacheopt.cu"
+OUT = PKG / "_lib" / "libcacheopt.so"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and Path(cand).exists():
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def sources():
+    return sorted((PKG / "csrc").glob("*.cu*")) + [PKG.parent / "include" / "cacheopt.h"]
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if OUT.exists() and not force:
+        newest = max(p.stat().st_mtime for p in sources())
+        if OUT.stat().st_mtime >= newest:
+            return OUT
+    OUT.parent.mkdir(parents=True, exist_ok=True)
+    tmp = OUT.with_suffix(".so.tmp")
+    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+           "-I", str(PKG.parent / "include"), "-o", str(tmp), str(SRC)]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.run(cmd, check=True)
+    tmp.replace(OUT)
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(force=True, verbose=True))

@@ -1,0 +1,268 @@
+// k_apply: plan application and the rest of one engine step (rows a11/a12):
+// engine.py:437-536 (_apply_plan), 619-625 (idle jump to the next event),
+// 627-633 (iteration charge + event), 553-571 (_emit), 404-433
+// (_complete/_fulfill_claim), 573-591 (_resolve_collisions), 636-640.
+// Pool mutations happen in plan order on thread 0; token emission is a
+// block-parallel pass over the (distinct) surviving members, and
+// completions, whose claim hand-offs are order dependent, are then replayed
+// in member order.
+#pragma once
+#include "block_ops.cuh"
+#include "pool_ops.cuh"
+
+namespace co {
+
+struct ApplySh {
+    BlkShared b;
+    int64_t batch, end;
+    int32_t n_surv, n_acted, idle;
+};
+
+__global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
+    __shared__ ApplySh S;
+    Ctl& c = *d.ctl;
+    if (!c.active) return;
+    const int tid = threadIdx.x;
+    const int64_t now = c.now;
+    const int32_t sid = c.sid;
+    const PlanHdr& P = *d.plan;
+    const int32_t n_nw = c.cnt_nw, n_nwp = c.cnt_nwp, n_run = c.cnt_run;
+    const int32_t* RUN = reinterpret_cast<const int32_t*>(d.vals_out) + n_nw + n_nwp;
+
+    if (tid == 0) {
+        for (int32_t k = 0; k < P.n_pre; k++) do_preempt(d, d.pre_idx[k], d.pre_strat[k], now, CO_CAUSE_PLAN);
+        int32_t n_acted = 0;
+        for (int32_t a = 0; a < P.n_act; a++) {
+            const int32_t i = d.act_idx[a];
+            if (d.st_failed[i] == sid || !live_state(d.state[i])) continue;
+            const int32_t kind = d.act_kind[a];
+            const int64_t tok = d.act_tok[a];
+            bool ok;
+            if (kind == A_ALLOCATE) ok = pool_allocate(d, i, tok);
+            else if (kind == A_GROW) ok = pool_grow(d, i, tok);
+            else if (kind == A_RESERVE) ok = pool_draw_reserved(d, i, d.act_nb[a]);
+            else ok = pool_embed(d, i, tok, d.act_host[a], d.act_start[a]);
+            if (ok) {
+                if (d.st_acted[i] != sid) { d.st_acted[i] = sid; d.l_acted[n_acted++] = i; }
+                d.alloc_kvc[i] = d.granted[i];
+                continue;
+            }
+            // a guest out of room is promoted when the pool covers it,
+            // squeezed out otherwise (engine.py:474-494)
+            if (kind == A_GROW && d.holds[i] && d.host[i] >= 0 && d.state[i] == ST_RUNNING) {
+                if (pool_promote(d, i)) {
+                    if (pool_grow(d, i, tok)) {
+                        if (d.st_acted[i] != sid) { d.st_acted[i] = sid; d.l_acted[n_acted++] = i; }
+                        d.alloc_kvc[i] = d.granted[i];
+                        continue;
+                    }
+                    d.st_failed[i] = sid;
+                    continue;
+                }
+                do_preempt(d, i, strategy_of(d, i), now, CO_CAUSE_SQUEEZE);
+            }
+            d.st_failed[i] = sid;
+        }
+        for (int32_t k = 0; k < n_acted; k++) {
+            int32_t i = d.l_acted[k];
+            if (d.state[i] == ST_PREEMPTED) do_readmit(d, i);
+        }
+        // member filter (engine.py:500-531)
+        int32_t ns = 0;
+        int64_t batch = 0;
+        for (int32_t m = 0; m < P.n_mem; m++) {
+            const int32_t i = d.mem_idx[m];
+            const int32_t tok = d.mem_tok[m];
+            if (d.st_failed[i] == sid || d.st_seen[i] == sid) continue;
+            d.st_seen[i] = sid;
+            int8_t s = d.state[i];
+            if (!live_state(s)) continue;
+            if (s == ST_WAITING) {
+                if (!d.holds[i] || d.granted[i] < d.prefill[i] + tok) continue;
+                d.state[i] = ST_RUNNING;
+                if (d.first_start[i] < 0) {
+                    d.first_start[i] = now;
+                    emit_event(d, CO_EV_ADMIT, i, now);
+                }
+            } else if (s != ST_RUNNING) {
+                continue;
+            }
+            if (d.ready_at[i] > now) continue;
+            if (d.prefill[i] >= d.kv_need[i]) {
+                if (eff_of(d, i) < d.used[i] + 1) continue;
+            } else if (d.granted[i] < d.prefill[i] + tok) {
+                continue;
+            }
+            d.l_surv_idx[ns] = i;
+            d.l_surv_tok[ns] = tok;
+            ns++;
+            batch += tok;
+        }
+        // claims (engine.py:533-535): setdefault(provider, waiter)
+        for (int32_t k = 0; k < P.n_cl; k++) {
+            int32_t w = d.cl_w[k], p = d.cl_p[k];
+            if (live_state(d.state[w]) && live_state(d.state[p]) && !claim_valid(d, p)) {
+                d.claim_w[p] = w;
+                d.claim_ep[p] = d.epoch[w];
+            }
+        }
+        S.n_surv = ns;
+        S.batch = batch;
+        S.idle = (ns == 0 && P.n_act == 0 && P.n_pre == 0) ? 1 : 0;
+    }
+    __syncthreads();
+
+    if (S.idle) {
+        // engine.py:619-625 / 593-602: jump to the next arrival or resume
+        // barrier; nothing changed state in this step, so the classify-time
+        // running set is current
+        uint64_t best = ~0ull;
+        for (int32_t k = tid; k < n_run; k += NT) {
+            int32_t i = RUN[k];
+            if (d.state[i] == ST_RUNNING && d.ready_at[i] > now) {
+                uint64_t v = (uint64_t)d.ready_at[i];
+                best = v < best ? v : best;
+            }
+        }
+        best = blk_min(best, S.b);
+        if (tid == 0) {
+            if (c.next_pending < d.n) {
+                uint64_t a = (uint64_t)d.arr[c.next_pending];
+                best = a < best ? a : best;
+            }
+            if (best == ~0ull) {
+                c.stalled = 1; c.done = 1; c.last_result = 0;
+            } else {
+                c.now = (int64_t)best;
+                c.last_result = 1;
+            }
+        }
+        return;
+    }
+
+    // ---- iteration charge and event (engine.py:627-633) -------------------
+    const int32_t ns = S.n_surv;
+    int64_t mem0 = 0;
+    if (tid == 0) {
+        int64_t il = to_us_d(iter_ms(d, S.batch));
+        S.end = now + il;
+        c.t_i = il;
+        if (d.record_events) {
+            mem0 = c.mem_count;
+            emit_event(d, CO_EV_ITER, ns, now, S.end, S.batch, mem0);
+            c.mem_count += ns;
+        }
+        d.plan->batch_tokens = S.batch;  // keep the applied batch for readers
+        S.n_acted = (int32_t)mem0;       // stash member-stream offset
+    }
+    __syncthreads();
+    const int64_t end = S.end;
+    if (d.record_events) {
+        const int64_t off = S.n_acted;
+        for (int32_t k = tid; k < ns; k += NT) {
+            d.members[2 * (off + k)] = d.l_surv_idx[k];
+            d.members[2 * (off + k) + 1] = d.l_surv_tok[k];
+        }
+    }
+
+    // ---- emission (engine.py:553-571), members are distinct ---------------
+    int64_t dused = 0, dgen = 0;
+    for (int32_t k = tid; k < ns; k += NT) {
+        const int32_t i = d.l_surv_idx[k];
+        const int32_t tok = d.l_surv_tok[k];
+        bool token = false;
+        int32_t nu;
+        if (d.prefill[i] < d.kv_need[i]) {
+            d.prefill[i] += tok;
+            nu = d.prefill[i];
+            token = d.prefill[i] >= d.kv_need[i] && d.gen[i] == 0;
+        } else {
+            nu = d.used[i] + 1;
+            token = true;
+        }
+        if (nu < 0 || nu > d.granted[i]) { c.error = 2; c.err_info[0] = i; c.err_info[1] = nu; }
+        dused += (int64_t)nu - d.used[i];
+        d.used[i] = nu;
+        if (token) {
+            int32_t g = d.gen[i] + 1;
+            d.gen[i] = g;
+            dgen += 1;
+            if (d.first_tok[i] < 0) {
+                d.first_tok[i] = end;
+            } else {
+                int64_t gap = end - d.last_tok[i];
+                if (gap > d.max_tbt[i]) d.max_tbt[i] = gap;
+            }
+            d.last_tok[i] = end;
+            d.tok_times[d.tok_off[i] + g - 1] = end;
+        }
+    }
+    dused = blk_sum(dused, S.b);
+    dgen = blk_sum(dgen, S.b);
+    const int32_t n_done = blk_compact(d.l_surv_idx, ns, d.l_done, [&](int32_t i) { return d.gen[i] >= d.tout[i]; }, S.b);
+    if (tid == 0) {
+        c.used_sum += dused;
+        c.gen_total += dgen;
+        for (int32_t k = 0; k < n_done; k++) do_complete(d, d.l_done[k], end);
+    }
+    __syncthreads();
+
+    // ---- collisions (engine.py:573-591), hosts in record-creation order ----
+    const int32_t n_coll = blk_compact(RUN, n_run, d.l_coll, [&](int32_t h) {
+        if (d.state[h] != ST_RUNNING || !d.holds[h] || d.host[h] >= 0) return false;
+        int32_t g = d.guest[h];
+        return g >= 0 && d.used[h] >= d.off[g];
+    }, S.b);
+    blk_sort(d.l_coll, n_coll, [&](int32_t h, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
+        k0 = (uint64_t)d.rec_seq[h]; k1 = 0; k2 = 0;
+    }, d, S.b);
+    if (tid == 0) {
+        for (int32_t k = 0; k < n_coll; k++) {
+            int32_t h = d.l_coll[k];
+            if (d.state[h] != ST_RUNNING || !d.holds[h]) continue;
+            int32_t g = d.guest[h];
+            if (g < 0 || d.used[h] < d.off[g]) continue;
+            if (pool_promote(d, g)) continue;
+            if (d.state[g] == ST_RUNNING) do_preempt(d, g, strategy_of(d, g), end, CO_CAUSE_COLLISION);
+        }
+        // engine.py:636-640
+        int64_t sp = c.sample_count++;
+        d.samples[2 * sp] = c.fp_sum;
+        d.samples[2 * sp + 1] = c.used_sum;
+        c.iters += 1;
+        c.check_due = (d.validate_every && c.iters % d.validate_every == 0) ? 1 : 0;
+        c.now = end;
+        c.last_result = 1;
+    }
+}
+
+// kvc.py:336-375 check_invariants over every record (debug / validate_every)
+__global__ void __launch_bounds__(NT, 1) k_check(Dev d, int32_t force) {
+    __shared__ BlkShared sb;
+    Ctl& c = *d.ctl;
+    if (!force && !(c.active && c.check_due)) return;
+    int64_t fp = 0, bad = 0;
+    for (int32_t i = threadIdx.x; i < d.n; i += NT) {
+        if (!d.holds[i]) continue;
+        if (d.host[i] < 0) fp += fp_tokens(d.granted[i], d.bs);
+        if (d.used[i] > d.granted[i]) bad |= 1;
+        int32_t h = d.host[i];
+        if (h >= 0) {
+            if (d.guest[i] >= 0) bad |= 2;
+            if (!d.holds[h] || d.guest[h] != i) bad |= 4;
+            else if (d.off[i] < 0 || (int64_t)d.off[i] + d.granted[i] > d.granted[h]) bad |= 8;
+        }
+        int32_t g = d.guest[i];
+        if (g >= 0 && d.off[g] < d.used[i]) bad |= 16;
+    }
+    fp = blk_sum(fp, sb);
+    bad = blk_sum(bad ? 1 : 0, sb);
+    if (threadIdx.x == 0) {
+        if (fp != c.fp_sum) bad += 1;
+        if (free_tokens(d) < 0) bad += 1;
+        if (c.rsv_cur < 0 || c.rsv_cur > d.rsv_target) bad += 1;
+        if (bad) { c.error = 4; c.done = 1; }
+    }
+}
+
+}  // namespace co

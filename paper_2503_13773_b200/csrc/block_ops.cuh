@@ -1,0 +1,166 @@
+// Single-CTA (1024-thread) cooperative primitives used by the planner and
+// apply kernels: reductions, exclusive scans, order-preserving compaction and
+// a rank sort for the small totally-ordered sets the reference sorts with
+// Python's sorted() (every key there ends in req_id, so keys are unique).
+#pragma once
+#include <cstdint>
+#include "engine_state.cuh"
+
+namespace co {
+
+struct BlkShared {
+    int64_t red[32];
+    uint64_t ured[32];
+    int32_t scan[32];
+    // rank-sort tile
+    static constexpr int TILE = 1024;
+    uint64_t t0[TILE], t1[TILE], t2[TILE];
+};
+
+__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+
+// all threads must call; every thread receives the block total
+__device__ int64_t blk_sum(int64_t v, BlkShared& s) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    v = warp_sum64(v);
+    if (lane == 0) s.red[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        int64_t x = s.red[lane];
+        x = warp_sum64(x);
+        if (lane == 0) s.red[0] = x;
+    }
+    __syncthreads();
+    int64_t r = s.red[0];
+    __syncthreads();
+    return r;
+}
+
+__device__ uint64_t blk_min(uint64_t v, BlkShared& s) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    v = warp_min_u64(v);
+    if (lane == 0) s.ured[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        uint64_t x = s.ured[lane];
+        x = warp_min_u64(x);
+        if (lane == 0) s.ured[0] = x;
+    }
+    __syncthreads();
+    uint64_t r = s.ured[0];
+    __syncthreads();
+    return r;
+}
+
+// exclusive prefix of a 0/1 (or small int) value across the block
+__device__ int32_t blk_excl_scan(int32_t v, int32_t* total, BlkShared& s) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s.scan[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int32_t y = s.scan[lane];
+        int32_t z = y;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int32_t q = __shfl_up_sync(0xffffffffu, z, o);
+            if (lane >= o) z += q;
+        }
+        s.scan[lane] = z - y;  // exclusive warp offsets
+        if (lane == 31) s.red[0] = z;
+    }
+    __syncthreads();
+    int32_t r = s.scan[w] + x - v;
+    *total = (int32_t)s.red[0];
+    __syncthreads();
+    return r;
+}
+
+// Order-preserving compaction of src[0..m) (or of 0..m when src == nullptr)
+// by predicate pred(item) into dst, returning the count (all threads).
+template <class Pred>
+__device__ int32_t blk_compact(const int32_t* src, int32_t m, int32_t* dst, Pred pred, BlkShared& s) {
+    int32_t base = 0;
+    for (int32_t c = 0; c < m; c += NT) {
+        int32_t k = c + (int32_t)threadIdx.x;
+        int32_t item = 0;
+        int32_t f = 0;
+        if (k < m) {
+            item = src ? src[k] : k;
+            f = pred(item) ? 1 : 0;
+        }
+        int32_t tot;
+        int32_t p = blk_excl_scan(f, &tot, s);
+        if (f) dst[base + p] = item;
+        base += tot;
+    }
+    __syncthreads();
+    return base;
+}
+
+// Sort items[0..m) by the unique 192-bit key kf(item, k0, k1, k2),
+// lexicographic ascending, in place (rank sort, O(m^2 / NT)).
+template <class KeyFn>
+__device__ void blk_sort(int32_t* items, int32_t m, KeyFn kf, const Dev& d, BlkShared& s) {
+    if (m <= 1) return;
+    for (int32_t k = threadIdx.x; k < m; k += NT) {
+        uint64_t a, b, c;
+        kf(items[k], a, b, c);
+        d.sk0[k] = a; d.sk1[k] = b; d.sk2[k] = c;
+        d.sk_item[k] = items[k];
+    }
+    __syncthreads();
+    constexpr int Q = 4;
+    for (int32_t base = 0; base < m; base += Q * NT) {
+        int32_t rank[Q];
+        uint64_t m0[Q], m1[Q], m2[Q];
+#pragma unroll
+        for (int q = 0; q < Q; q++) {
+            int32_t k = base + q * NT + threadIdx.x;
+            rank[q] = 0;
+            if (k < m) { m0[q] = d.sk0[k]; m1[q] = d.sk1[k]; m2[q] = d.sk2[k]; }
+            else { m0[q] = m1[q] = m2[q] = 0; }
+        }
+        for (int32_t t = 0; t < m; t += BlkShared::TILE) {
+            int32_t tn = m - t < BlkShared::TILE ? m - t : BlkShared::TILE;
+            for (int32_t j = threadIdx.x; j < tn; j += NT) {
+                s.t0[j] = d.sk0[t + j]; s.t1[j] = d.sk1[t + j]; s.t2[j] = d.sk2[t + j];
+            }
+            __syncthreads();
+            for (int32_t j = 0; j < tn; j++) {
+                uint64_t a = s.t0[j], b = s.t1[j], c = s.t2[j];
+#pragma unroll
+                for (int q = 0; q < Q; q++) {
+                    bool lt = a < m0[q] || (a == m0[q] && (b < m1[q] || (b == m1[q] && c < m2[q])));
+                    rank[q] += lt ? 1 : 0;
+                }
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int q = 0; q < Q; q++) {
+            int32_t k = base + q * NT + threadIdx.x;
+            if (k < m) items[rank[q]] = d.sk_item[k];
+        }
+    }
+    __syncthreads();
+}
+
+}  // namespace co

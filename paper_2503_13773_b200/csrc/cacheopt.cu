@@ -1,0 +1,588 @@
+// libcacheopt: the B200-native CacheOPT engine behind the C ABI of
+// include/cacheopt.h.  One translation unit so every device helper inlines.
+//
+// Per engine step the stream runs:
+//   k_begin (1 thread)  -> k_admit (grid) -> k_classify (grid)
+//   -> cub::DeviceRadixSort (one 64-bit composite key per request)
+//   -> k_plan (1 CTA x 1024) -> k_apply (1 CTA x 1024) -> k_check (1 CTA, gated)
+// co_run captures `steps_per_launch` steps into one CUDA graph and relaunches
+// it; every kernel early-exits once the device control block says the run is
+// done or paused (an append buffer needs draining), so no host round trip is
+// needed inside a launch.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "engine_state.cuh"
+#include "block_ops.cuh"
+#include "pool_ops.cuh"
+#include "grid_kernels.cuh"
+#include "planner.cuh"
+#include "apply.cuh"
+
+using namespace co;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(x)                                                                              \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(CO_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));         \
+    } while (0)
+
+__global__ void k_preempt_one(Dev d, int32_t i, int32_t strat, int64_t now, int32_t cause) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) do_preempt(d, i, strat, now, cause);
+}
+__global__ void k_reset_drained(Dev d, int64_t ev, int64_t mem, int64_t smp) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        d.ctl->ev_count -= ev;
+        d.ctl->mem_count -= mem;
+        d.ctl->sample_count -= smp;
+        d.ctl->paused = 0;
+    }
+}
+
+struct co_engine {
+    Dev d{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::vector<void*> allocs;
+    void* cub_tmp = nullptr;
+    size_t cub_bytes = 0;
+    Ctl* h_ctl = nullptr;  // pinned mirror
+    cudaGraphExec_t graph = nullptr;
+    int32_t graph_k = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    double last_ms = 0.0;
+    int grid = 1;
+    int64_t n = 0;
+    int64_t tok_total = 0;
+    std::vector<int64_t> perm;         // sorted position -> caller position
+    std::vector<int64_t> tok_off_host;
+    std::vector<co_event> st_events;   // host staging of drained device events
+    std::vector<int32_t> st_members;
+    std::vector<int64_t> st_samples;
+
+    template <class T>
+    int alloc(T** p, size_t count) {
+        void* q = nullptr;
+        size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+        cudaError_t e = cudaMalloc(&q, bytes);
+        if (e != cudaSuccess) return fail(CO_ECUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        allocs.push_back(q);
+        *p = static_cast<T*>(q);
+        return CO_OK;
+    }
+};
+
+#define AL(ptr, cnt)                                  \
+    do {                                              \
+        int r_ = E->alloc(&(ptr), (size_t)(cnt));     \
+        if (r_) { co_destroy(E); return r_; }         \
+    } while (0)
+
+template <class T>
+static int upload(co_engine* E, T* dst, const std::vector<T>& src) {
+    if (src.empty()) return CO_OK;
+    CK(cudaMemcpyAsync(dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, E->stream));
+    return CO_OK;
+}
+
+static int launch_step(co_engine* E, int32_t guard) {
+    Dev& d = E->d;
+    cudaStream_t s = E->stream;
+    k_begin<<<1, 32, 0, s>>>(d, guard);
+    k_admit<<<E->grid, 256, 0, s>>>(d);
+    k_classify<<<E->grid, 256, 0, s>>>(d);
+    size_t bytes = E->cub_bytes;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(E->cub_tmp, bytes, d.keys_in, d.keys_out, d.vals_in,
+                                                    d.vals_out, (int)E->n, 0, 64, s);
+    if (e != cudaSuccess) return fail(CO_ECUDA, std::string("radix sort: ") + cudaGetErrorString(e));
+    k_plan<<<1, NT, 0, s>>>(d);
+    k_apply<<<1, NT, 0, s>>>(d);
+    k_check<<<1, NT, 0, s>>>(d, 0);
+    return CO_OK;
+}
+
+static int sync_ctl(co_engine* E) {
+    CK(cudaMemcpyAsync(E->h_ctl, E->d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, E->stream));
+    CK(cudaStreamSynchronize(E->stream));
+    return CO_OK;
+}
+
+// move device append buffers into host staging and reset the device fill
+static int drain_device(co_engine* E) {
+    int r = sync_ctl(E);
+    if (r) return r;
+    const Ctl& c = *E->h_ctl;
+    int64_t ne = c.ev_count, nm = c.mem_count, ns = c.sample_count;
+    if (ne > 0) {
+        size_t base = E->st_events.size();
+        int64_t mbase = (int64_t)E->st_members.size() / 2;
+        E->st_events.resize(base + ne);
+        CK(cudaMemcpyAsync(E->st_events.data() + base, E->d.events, ne * sizeof(co_event), cudaMemcpyDeviceToHost,
+                           E->stream));
+        if (nm > 0) {
+            size_t mb = E->st_members.size();
+            E->st_members.resize(mb + 2 * nm);
+            CK(cudaMemcpyAsync(E->st_members.data() + mb, E->d.members, 2 * nm * sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, E->stream));
+        }
+        CK(cudaStreamSynchronize(E->stream));
+        for (size_t k = base; k < E->st_events.size(); k++)
+            if (E->st_events[k].kind == CO_EV_ITER) E->st_events[k].c += mbase;
+    }
+    if (ns > 0) {
+        size_t sb = E->st_samples.size();
+        E->st_samples.resize(sb + 2 * ns);
+        CK(cudaMemcpyAsync(E->st_samples.data() + sb, E->d.samples, 2 * ns * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                           E->stream));
+    }
+    k_reset_drained<<<1, 1, 0, E->stream>>>(E->d, ne, nm, ns);
+    CK(cudaGetLastError());
+    return sync_ctl(E);
+}
+
+template <class T>
+static int read_arr(co_engine* E, const T* src, int64_t* out) {
+    std::vector<T> h(E->n);
+    if (E->n) {
+        CK(cudaMemcpyAsync(h.data(), src, E->n * sizeof(T), cudaMemcpyDeviceToHost, E->stream));
+        CK(cudaStreamSynchronize(E->stream));
+    }
+    for (int64_t k = 0; k < E->n; k++) out[k] = (int64_t)h[k];
+    return CO_OK;
+}
+
+extern "C" {
+
+const char* co_last_error(void) { return g_err.c_str(); }
+const char* co_version(void) { return "cacheopt-b200 0.1 (sm_100a)"; }
+
+int co_destroy(co_engine* E) {
+    if (!E) return CO_OK;
+    if (E->graph) cudaGraphExecDestroy(E->graph);
+    for (void* p : E->allocs) cudaFree(p);
+    if (E->cub_tmp) cudaFree(E->cub_tmp);
+    if (E->h_ctl) cudaFreeHost(E->h_ctl);
+    if (E->ev0) cudaEventDestroy(E->ev0);
+    if (E->ev1) cudaEventDestroy(E->ev1);
+    if (E->stream) cudaStreamDestroy(E->stream);
+    delete E;
+    return CO_OK;
+}
+
+int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int device, co_engine** out) {
+    if (!cfg || !tr || !lu || !out) return fail(CO_EINVAL, "null argument");
+    *out = nullptr;
+    if (cfg->allow_stacking) return fail(CO_EINVAL, "allow_stacking=True is not supported by the device pool");
+    if (cfg->block_size < 1 || cfg->buffer_b < 0 || cfg->token_budget < 1 || cfg->preallocate_m < 0 ||
+        cfg->decode_runway_iters < 0 || cfg->epsilon_us < 0 || cfg->token_step < 1 || cfg->capacity_tokens < 1 ||
+        cfg->reserved_blocks < 0 || cfg->n_slo_edges < 0 || cfg->n_slo_edges > CO_MAX_SLO_EDGES)
+        return fail(CO_EINVAL, "invalid configuration scalar");
+    if ((int64_t)cfg->reserved_blocks * cfg->block_size > cfg->capacity_tokens)
+        return fail(CO_EINVAL, "reserve exceeds capacity");
+    if (cfg->capacity_tokens > (1ll << 30)) return fail(CO_EINVAL, "capacity_tokens too large for int32 records");
+    const int64_t n = tr->n;
+    if (n < 0 || n > (1ll << 30)) return fail(CO_EINVAL, "bad trace size");
+    if (lu->s_max < 1) return fail(CO_EINVAL, "LUTs must cover S >= 1");
+    // sorted order (engine.py:241) and uniqueness (engine.py:226-228)
+    std::vector<int64_t> perm(n);
+    std::iota(perm.begin(), perm.end(), 0);
+    std::sort(perm.begin(), perm.end(), [&](int64_t a, int64_t b) {
+        if (tr->arrival_us[a] != tr->arrival_us[b]) return tr->arrival_us[a] < tr->arrival_us[b];
+        return tr->req_id[a] < tr->req_id[b];
+    });
+    for (int64_t k = 1; k < n; k++)
+        if (tr->req_id[perm[k]] == tr->req_id[perm[k - 1]]) return fail(CO_EINVAL, "request ids must be unique");
+    std::vector<int64_t> by_id(n);
+    std::iota(by_id.begin(), by_id.end(), 0);
+    std::sort(by_id.begin(), by_id.end(),
+              [&](int64_t a, int64_t b) { return tr->req_id[perm[a]] < tr->req_id[perm[b]]; });
+    std::vector<int32_t> idrank(n), rank_to_idx(n);
+    for (int64_t r = 0; r < n; r++) { idrank[by_id[r]] = (int32_t)r; rank_to_idx[r] = (int32_t)by_id[r]; }
+    if (std::adjacent_find(by_id.begin(), by_id.end(), [&](int64_t a, int64_t b) {
+            return tr->req_id[perm[a]] == tr->req_id[perm[b]];
+        }) != by_id.end())
+        return fail(CO_EINVAL, "request ids must be unique");
+
+    std::vector<int64_t> rid(n), arr(n), sttft(n), stbt(n), tok_off(n + 1, 0);
+    std::vector<int32_t> prompt(n), tout(n), err(n);
+    std::vector<uint8_t> flip(n);
+    int64_t maxD = 0, max_tbt_slo = 0, tot_tokens = 0, max_s = 1;
+    for (int64_t k = 0; k < n; k++) {
+        int64_t p = perm[k];
+        rid[k] = tr->req_id[p]; arr[k] = tr->arrival_us[p]; prompt[k] = tr->prompt_len[p];
+        tout[k] = tr->true_output_len[p]; sttft[k] = tr->slo_ttft_us[p]; stbt[k] = tr->slo_tbt_us[p];
+        err[k] = tr->err_draw[k]; flip[k] = tr->flip_draw[k];
+        if (arr[k] < 0 || prompt[k] < 1 || tout[k] < 1 || sttft[k] <= 0 || stbt[k] <= 0)
+            return fail(CO_EINVAL, "invalid request (core.py:59-69 rules)");
+        tok_off[k + 1] = tok_off[k] + tout[k];
+        maxD = std::max(maxD, arr[k] + sttft[k]);
+        max_tbt_slo = std::max(max_tbt_slo, stbt[k]);
+        tot_tokens += (int64_t)prompt[k] + tout[k] + 1;
+        max_s = std::max<int64_t>(max_s, (int64_t)prompt[k] + tout[k]);
+    }
+    if (lu->s_max < max_s) return fail(CO_EINVAL, "LUTs do not cover max(prompt_len + true_output_len)");
+    int64_t first = n ? arr[0] : 0, horizon = 0;
+    if (n) {
+        int64_t span = arr[n - 1] - first;
+        horizon = arr[n - 1] + cfg->horizon_factor * std::max<int64_t>(span, 1000000);
+    }
+    // composite classify key: [class:2][flag:1][time:61-idbits][idrank:idbits]
+    int idbits = 1;
+    while ((1ll << idbits) < n) idbits++;
+    const int timebits = 61 - idbits;
+    double max_iter_ms = cfg->iter_base_ms + cfg->iter_per_token_ms * (double)tot_tokens;
+    double bound = std::max((double)maxD, (double)horizon + max_iter_ms * 1000.0 + 2.0 + (double)max_tbt_slo);
+    if (bound >= std::ldexp(1.0, timebits)) return fail(CO_EINVAL, "trace time range exceeds the sort-key budget");
+
+    co_engine* E = new co_engine();
+    E->n = n;
+    E->perm = perm;
+    E->tok_off_host = tok_off;
+    E->tok_total = tok_off[n];
+    if (device >= 0) {
+        cudaError_t e = cudaSetDevice(device);
+        if (e != cudaSuccess) { delete E; return fail(CO_ECUDA, cudaGetErrorString(e)); }
+    }
+    cudaGetDevice(&E->device);
+    if (cudaStreamCreateWithFlags(&E->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete E;
+        return fail(CO_ECUDA, "stream create failed");
+    }
+    cudaEventCreate(&E->ev0);
+    cudaEventCreate(&E->ev1);
+    if (cudaMallocHost(&E->h_ctl, sizeof(Ctl)) != cudaSuccess) { co_destroy(E); return fail(CO_ECUDA, "pinned alloc"); }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, E->device);
+    E->grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8));
+
+    Dev& d = E->d;
+    d.n = (int32_t)n; d.bs = cfg->block_size; d.B = cfg->block_size; d.buffer_b = cfg->buffer_b;
+    d.token_budget = cfg->token_budget; d.prealloc_m = cfg->preallocate_m; d.runway_iters = cfg->decode_runway_iters;
+    d.fcfs = cfg->victim_rule_fcfs; d.record_events = cfg->record_events; d.validate_every = cfg->validate_every;
+    d.pad = cfg->padding; d.idbits = idbits; d.n_edges = cfg->n_slo_edges; d.token_step = cfg->token_step;
+    d.rsv_target = cfg->reserved_blocks; d.eps = cfg->epsilon_us; d.capacity = cfg->capacity_tokens;
+    d.s_star = cfg->s_star; d.s_max = lu->s_max;
+    for (int k = 0; k < CO_MAX_SLO_EDGES; k++) d.edges[k] = k < cfg->n_slo_edges ? cfg->slo_edges_us[k] : 0;
+    d.base_ms = cfg->iter_base_ms; d.per_token_ms = cfg->iter_per_token_ms;
+    d.ev_cap = std::max<int64_t>(1 << 16, 8 * n + 4096);
+    d.mem_cap = std::max<int64_t>(1 << 16, 4 * n + 4096);
+    d.sample_cap = 1 << 16;
+    const int64_t n2 = 2 * n + 64, n3 = 3 * n + 64;
+
+    int64_t *p_rid, *p_arr, *p_sttft, *p_stbt, *p_tok_off;
+    int32_t *p_prompt, *p_tout, *p_idrank, *p_err;
+    uint8_t* p_flip;
+    int64_t *l0, *l1, *l2, *l3;
+    AL(p_rid, n); AL(p_arr, n); AL(p_sttft, n); AL(p_stbt, n); AL(p_tok_off, n + 1);
+    AL(p_prompt, n); AL(p_tout, n); AL(p_idrank, n); AL(p_err, n); AL(p_flip, n);
+    const int64_t L = lu->s_max + 1;
+    AL(l0, L); AL(l1, L); AL(l2, L); AL(l3, L);
+    d.rid = p_rid; d.arr = p_arr; d.slo_ttft = p_sttft; d.slo_tbt = p_stbt; d.tok_off = p_tok_off;
+    d.prompt = p_prompt; d.tout = p_tout; d.idrank = p_idrank; d.err = p_err; d.flip = p_flip;
+    d.lut_swap_half = l0; d.lut_rec = l1; d.lut_surv_swap = l2; d.lut_surv_rec = l3;
+    AL(d.state, n); AL(d.last_strat, n);
+    AL(d.gen, n); AL(d.used, n); AL(d.kv_need, n); AL(d.prefill, n); AL(d.pcount, n); AL(d.pred, n); AL(d.est, n);
+    AL(d.alloc_kvc, n);
+    AL(d.first_tok, n); AL(d.last_tok, n); AL(d.max_tbt, n); AL(d.ready_at, n); AL(d.pstart, n);
+    AL(d.swap_done, n); AL(d.first_start, n); AL(d.completion, n); AL(d.ptime, n);
+    AL(d.tok_times, E->tok_total);
+    AL(d.holds, n); AL(d.granted, n); AL(d.host, n); AL(d.off, n); AL(d.rsv, n); AL(d.guest, n); AL(d.rec_seq, n);
+    AL(d.claim_w, n); AL(d.claim_ep, n); AL(d.epoch, n);
+    AL(d.st_nr, n); AL(d.st_crit, n); AL(d.st_removed, n); AL(d.st_embedded, n); AL(d.st_resumed, n);
+    AL(d.st_stalled, n); AL(d.st_parts, n); AL(d.st_claimed, n); AL(d.st_failed, n); AL(d.st_seen, n);
+    AL(d.st_acted, n); AL(d.st_deferred, n);
+    AL(d.keys_in, n); AL(d.keys_out, n); AL(d.vals_in, n); AL(d.vals_out, n);
+    AL(d.plan, 1);
+    AL(d.mem_idx, n3); AL(d.mem_tok, n3);
+    AL(d.act_kind, n3); AL(d.act_idx, n3); AL(d.act_tok, n3); AL(d.act_nb, n3); AL(d.act_host, n3); AL(d.act_start, n3);
+    AL(d.pre_idx, n); AL(d.pre_strat, n); AL(d.cl_w, n2); AL(d.cl_p, n2); AL(d.def_idx, n2);
+    AL(d.l_nr, n); AL(d.l_nrp, n); AL(d.l_pend, n); AL(d.l_tri, n); AL(d.l_tri_taken, n); AL(d.l_vict, n);
+    AL(d.l_defer, n); AL(d.l_pro, n); AL(d.l_ful, n); AL(d.l_part, n3); AL(d.l_part_need, n3);
+    AL(d.l_part_grant, n3); AL(d.l_mready, n2); AL(d.l_gm_idx, n); AL(d.l_gm_tok, n); AL(d.l_acted, n3);
+    AL(d.l_surv_idx, n3); AL(d.l_surv_tok, n3); AL(d.l_done, n3); AL(d.l_coll, n); AL(d.l_grp, 2 * n3);
+    AL(d.l_tri_key, n); AL(d.am_rhi, n3); AL(d.am_rlo, n3); AL(d.rank_to_idx, n);
+    AL(d.sk0, n3); AL(d.sk1, n3); AL(d.sk2, n3); AL(d.sk_item, n3);
+    AL(d.events, d.ev_cap); AL(d.members, 2 * d.mem_cap); AL(d.samples, 2 * d.sample_cap);
+    AL(d.ctl, 1);
+
+    int r = 0;
+    std::vector<int64_t> lut_v(L);
+    auto up_lut = [&](int64_t* dst, const int64_t* src) {
+        CK(cudaMemcpyAsync(dst, src, L * sizeof(int64_t), cudaMemcpyHostToDevice, E->stream));
+        return CO_OK;
+    };
+    if ((r = upload(E, p_rid, rid)) || (r = upload(E, p_arr, arr)) || (r = upload(E, p_sttft, sttft)) ||
+        (r = upload(E, p_stbt, stbt)) || (r = upload(E, p_tok_off, tok_off)) || (r = upload(E, p_prompt, prompt)) ||
+        (r = upload(E, p_tout, tout)) || (r = upload(E, p_idrank, idrank)) || (r = upload(E, p_err, err)) ||
+        (r = upload(E, p_flip, flip)) || (r = upload(E, d.rank_to_idx, rank_to_idx)) ||
+        (r = upload(E, d.kv_need, prompt)) || (r = up_lut(l0, lu->swap_half_us)) || (r = up_lut(l1, lu->recompute_us)) ||
+        (r = up_lut(l2, lu->survive_swap_us)) || (r = up_lut(l3, lu->survive_rec_us))) {
+        co_destroy(E);
+        return r;
+    }
+    auto memset_all = [&](void* p, int v, size_t bytes) { return cudaMemsetAsync(p, v, bytes, E->stream); };
+    const size_t n8 = n * 8, n4 = n * 4;
+    memset_all(d.state, 0, n); memset_all(d.last_strat, 0xff, n);
+    for (int32_t* p : {d.gen, d.used, d.prefill, d.pcount, d.pred, d.est, d.alloc_kvc, d.granted, d.off, d.rsv,
+                       d.claim_ep, d.epoch})
+        memset_all(p, 0, n4);
+    for (int32_t* p : {d.host, d.guest, d.claim_w}) memset_all(p, 0xff, n4);
+    for (int32_t* p : {d.st_nr, d.st_crit, d.st_removed, d.st_embedded, d.st_resumed, d.st_stalled, d.st_parts,
+                       d.st_claimed, d.st_failed, d.st_seen, d.st_acted, d.st_deferred})
+        memset_all(p, 0, n4);
+    for (int64_t* p : {d.max_tbt, d.ready_at, d.pstart, d.swap_done, d.ptime, d.rec_seq}) memset_all(p, 0, n8);
+    for (int64_t* p : {d.first_tok, d.last_tok, d.first_start, d.completion}) memset_all(p, 0xff, n8);
+    memset_all(d.holds, 0, n);
+    memset_all(d.plan, 0, sizeof(PlanHdr));
+    Ctl c0;
+    std::memset(&c0, 0, sizeof(c0));
+    c0.now = first; c0.horizon = horizon; c0.first_arrival = first; c0.t_i = cfg->t_i_init_us;
+    c0.rsv_cur = cfg->reserved_blocks;
+    *E->h_ctl = c0;
+    if (cudaMemcpyAsync(d.ctl, E->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, E->stream) != cudaSuccess) {
+        co_destroy(E);
+        return fail(CO_ECUDA, "ctl upload");
+    }
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, d.keys_in, d.keys_out, d.vals_in, d.vals_out, (int)n, 0, 64,
+                                    E->stream);
+    E->cub_bytes = std::max<size_t>(bytes, 256);
+    if (cudaMalloc(&E->cub_tmp, E->cub_bytes) != cudaSuccess) { co_destroy(E); return fail(CO_ECUDA, "cub temp"); }
+    cudaError_t e = cudaStreamSynchronize(E->stream);
+    if (e != cudaSuccess) { co_destroy(E); return fail(CO_ECUDA, cudaGetErrorString(e)); }
+    *out = E;
+    return CO_OK;
+}
+
+static int check_device_error(co_engine* E) {
+    int32_t err = E->h_ctl->error;
+    if (!err) return CO_OK;
+    char buf[256];
+    const char* what = err == 3 ? "no progress after 1000000 rounds (engine.py:653-656)"
+                     : err == 4 ? "pool invariant violated (kvc.py:336-375)"
+                     : err == 2 ? "set_used outside [0, granted] (kvc.py:326-332)"
+                                : "device engine error";
+    snprintf(buf, sizeof(buf), "%s [code %d, info %d %d]", what, err, E->h_ctl->err_info[0], E->h_ctl->err_info[1]);
+    return fail(CO_EDEVICE, buf);
+}
+
+int co_step(co_engine* E, int32_t* result) {
+    if (!E || !result) return fail(CO_EINVAL, "null argument");
+    for (int attempt = 0; attempt < 3; attempt++) {
+        CK(cudaEventRecord(E->ev0, E->stream));
+        int r = launch_step(E, 0);
+        if (r) return r;
+        CK(cudaEventRecord(E->ev1, E->stream));
+        CK(cudaGetLastError());
+        if ((r = sync_ctl(E))) return r;
+        float ms = 0;
+        cudaEventElapsedTime(&ms, E->ev0, E->ev1);
+        E->last_ms = ms;
+        if ((r = check_device_error(E))) return r;
+        if (E->h_ctl->paused) {
+            if ((r = drain_device(E))) return r;
+            continue;
+        }
+        *result = E->h_ctl->done ? 0 : E->h_ctl->last_result;
+        return CO_OK;
+    }
+    return fail(CO_EDEVICE, "step could not make buffer headroom");
+}
+
+int co_run(co_engine* E, int64_t max_steps, int32_t K, int64_t* steps_done) {
+    if (!E) return fail(CO_EINVAL, "null argument");
+    if (K < 1) K = 1;
+    int r = sync_ctl(E);
+    if (r) return r;
+    const int64_t steps0 = E->h_ctl->steps;
+    if (E->graph && E->graph_k != K) { cudaGraphExecDestroy(E->graph); E->graph = nullptr; }
+    if (!E->graph) {
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(E->stream, cudaStreamCaptureModeThreadLocal));
+        for (int k = 0; k < K; k++) {
+            if ((r = launch_step(E, 1))) { cudaStreamEndCapture(E->stream, &g); return r; }
+        }
+        CK(cudaStreamEndCapture(E->stream, &g));
+        CK(cudaGraphInstantiate(&E->graph, g, 0));
+        cudaGraphDestroy(g);
+        E->graph_k = K;
+    }
+    double total_ms = 0;
+    while (true) {
+        int64_t done_steps = E->h_ctl->steps - steps0;
+        if (max_steps > 0 && done_steps >= max_steps) break;
+        bool single = max_steps > 0 && max_steps - done_steps < K;
+        CK(cudaEventRecord(E->ev0, E->stream));
+        if (single) {
+            if ((r = launch_step(E, 1))) return r;
+        } else {
+            CK(cudaGraphLaunch(E->graph, E->stream));
+        }
+        CK(cudaEventRecord(E->ev1, E->stream));
+        if ((r = sync_ctl(E))) return r;
+        float ms = 0;
+        cudaEventElapsedTime(&ms, E->ev0, E->ev1);
+        total_ms += ms;
+        if ((r = check_device_error(E))) return r;
+        if (E->h_ctl->paused) {
+            if ((r = drain_device(E))) return r;
+            continue;
+        }
+        if (E->h_ctl->done) break;
+    }
+    E->last_ms = total_ms;
+    if (steps_done) *steps_done = E->h_ctl->steps - steps0;
+    return CO_OK;
+}
+
+int co_preempt(co_engine* E, int64_t idx, int32_t strategy, int64_t now_us, int32_t cause) {
+    if (!E || idx < 0 || idx >= E->n) return fail(CO_EINVAL, "bad request index");
+    k_preempt_one<<<1, 1, 0, E->stream>>>(E->d, (int32_t)idx, strategy, now_us, cause);
+    CK(cudaGetLastError());
+    return sync_ctl(E);
+}
+
+int co_get_scalars(co_engine* E, co_scalars* o) {
+    if (!E || !o) return fail(CO_EINVAL, "null argument");
+    int r = sync_ctl(E);
+    if (r) return r;
+    const Ctl& c = *E->h_ctl;
+    std::memset(o, 0, sizeof(*o));
+    o->now_us = c.now; o->horizon_us = c.horizon; o->first_arrival_us = c.first_arrival; o->t_i_max_us = c.t_i;
+    o->footprint_tokens = c.fp_sum; o->granted_tokens = c.granted_sum; o->used_tokens = c.used_sum;
+    o->generated_total = c.gen_total; o->iterations = c.iters; o->steps = c.steps; o->record_seq = c.seq;
+    o->n_events = c.ev_count + (int64_t)E->st_events.size(); o->n_samples = c.sample_count + E->st_samples.size() / 2;
+    o->reserved_blocks_current = c.rsv_cur; o->n_live = c.n_live; o->n_pending = (int32_t)(E->n - c.next_pending);
+    o->done = c.done; o->stalled = c.stalled; o->last_step_result = c.done ? 0 : c.last_result; o->error = c.error;
+    return CO_OK;
+}
+
+int co_read_field(co_engine* E, int32_t f, int64_t* out) {
+    if (!E || !out) return fail(CO_EINVAL, "null argument");
+    Dev& d = E->d;
+    switch (f) {
+        case CO_F_STATE: return read_arr(E, d.state, out);
+        case CO_F_GENERATED: return read_arr(E, d.gen, out);
+        case CO_F_USED: return read_arr(E, d.used, out);
+        case CO_F_KV_NEED: return read_arr(E, d.kv_need, out);
+        case CO_F_PREFILL_DONE: return read_arr(E, d.prefill, out);
+        case CO_F_PREEMPTION_COUNT: return read_arr(E, d.pcount, out);
+        case CO_F_PREEMPTION_TIME: return read_arr(E, d.ptime, out);
+        case CO_F_FIRST_TOKEN: return read_arr(E, d.first_tok, out);
+        case CO_F_LAST_TOKEN: return read_arr(E, d.last_tok, out);
+        case CO_F_MAX_TBT: return read_arr(E, d.max_tbt, out);
+        case CO_F_READY_AT: return read_arr(E, d.ready_at, out);
+        case CO_F_PREEMPT_STARTED: return read_arr(E, d.pstart, out);
+        case CO_F_SWAP_OUT_DONE: return read_arr(E, d.swap_done, out);
+        case CO_F_LAST_STRATEGY: return read_arr(E, d.last_strat, out);
+        case CO_F_FIRST_START: return read_arr(E, d.first_start, out);
+        case CO_F_COMPLETION: return read_arr(E, d.completion, out);
+        case CO_F_ALLOCATED_KVC: return read_arr(E, d.alloc_kvc, out);
+        case CO_F_PREDICTED: return read_arr(E, d.pred, out);
+        case CO_F_ESTIMATED: return read_arr(E, d.est, out);
+        case CO_F_HOLDS: return read_arr(E, d.holds, out);
+        case CO_F_GRANTED: return read_arr(E, d.granted, out);
+        case CO_F_HOST: return read_arr(E, d.host, out);
+        case CO_F_EMBED_OFFSET: return read_arr(E, d.off, out);
+        case CO_F_RESERVED_DRAWN: return read_arr(E, d.rsv, out);
+        case CO_F_RECORD_SEQ: return read_arr(E, d.rec_seq, out);
+        case CO_F_CLAIM_WAITER: {
+            std::vector<int64_t> w(E->n), ep(E->n), epo(E->n);
+            int r;
+            if ((r = read_arr(E, d.claim_w, w.data())) || (r = read_arr(E, d.claim_ep, ep.data())) ||
+                (r = read_arr(E, d.epoch, epo.data())))
+                return r;
+            for (int64_t k = 0; k < E->n; k++) out[k] = (w[k] >= 0 && ep[k] == epo[w[k]]) ? w[k] : -1;
+            return CO_OK;
+        }
+        case CO_F_SORTED_ORDER:
+            for (int64_t k = 0; k < E->n; k++) out[k] = E->perm[k];
+            return CO_OK;
+        default: return fail(CO_EINVAL, "unknown field");
+    }
+}
+
+int co_pending_events(co_engine* E, int64_t* ne, int64_t* nm) {
+    if (!E) return fail(CO_EINVAL, "null argument");
+    int r = sync_ctl(E);
+    if (r) return r;
+    if (ne) *ne = (int64_t)E->st_events.size() + E->h_ctl->ev_count;
+    if (nm) *nm = (int64_t)E->st_members.size() / 2 + E->h_ctl->mem_count;
+    return CO_OK;
+}
+
+int co_drain_events(co_engine* E, co_event* events, int64_t max_events, int32_t* members, int64_t max_members,
+                    int64_t* n_events, int64_t* n_members) {
+    if (!E) return fail(CO_EINVAL, "null argument");
+    int r = drain_device(E);
+    if (r) return r;
+    int64_t ne = (int64_t)E->st_events.size(), nm = (int64_t)E->st_members.size() / 2;
+    if (ne > max_events || nm > max_members) return fail(CO_EINVAL, "drain buffers too small");
+    if (ne) std::memcpy(events, E->st_events.data(), ne * sizeof(co_event));
+    if (nm) std::memcpy(members, E->st_members.data(), 2 * nm * sizeof(int32_t));
+    E->st_events.clear();
+    E->st_members.clear();
+    if (n_events) *n_events = ne;
+    if (n_members) *n_members = nm;
+    return CO_OK;
+}
+
+int co_drain_samples(co_engine* E, int64_t* out, int64_t max, int64_t* n) {
+    if (!E) return fail(CO_EINVAL, "null argument");
+    int r = drain_device(E);
+    if (r) return r;
+    int64_t ns = (int64_t)E->st_samples.size() / 2;
+    if (ns > max) return fail(CO_EINVAL, "sample buffer too small");
+    if (ns) std::memcpy(out, E->st_samples.data(), 2 * ns * sizeof(int64_t));
+    E->st_samples.clear();
+    if (n) *n = ns;
+    return CO_OK;
+}
+
+int co_read_token_times(co_engine* E, int64_t* offsets, int64_t* times) {
+    if (!E) return fail(CO_EINVAL, "null argument");
+    if (offsets) std::memcpy(offsets, E->tok_off_host.data(), (E->n + 1) * sizeof(int64_t));
+    if (times && E->tok_total) {
+        CK(cudaMemcpyAsync(times, E->d.tok_times, E->tok_total * sizeof(int64_t), cudaMemcpyDeviceToHost, E->stream));
+        CK(cudaStreamSynchronize(E->stream));
+    }
+    return CO_OK;
+}
+
+int co_check_invariants(co_engine* E) {
+    if (!E) return fail(CO_EINVAL, "null argument");
+    k_check<<<1, NT, 0, E->stream>>>(E->d, 1);
+    CK(cudaGetLastError());
+    int r = sync_ctl(E);
+    if (r) return r;
+    return check_device_error(E);
+}
+
+int co_last_device_ms(co_engine* E, double* ms) {
+    if (!E || !ms) return fail(CO_EINVAL, "null argument");
+    *ms = E->last_ms;
+    return CO_OK;
+}
+
+int co_kernels_per_step(co_engine* E, int32_t* n) {
+    if (!E || !n) return fail(CO_EINVAL, "null argument");
+    *n = 7;  // begin, admit, classify, sort (counted as one stage), plan, apply, check
+    return CO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,162 @@
+// Device-resident CacheOPT engine state: a structure-of-arrays request table
+// in HBM indexed by arrival rank (engine.py:241 orders requests by
+// (arrival_us, id); that rank is also the reference's _live iteration order,
+// engine.py:242/352), the KV pool records of kvc.py:44-52 as parallel arrays,
+// and a small control block of engine scalars (engine.py:243-270).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/cacheopt.h"
+
+namespace co {
+
+constexpr int NT = 1024;           // threads of the single-CTA planner / apply kernels
+constexpr int ST_PENDING = CO_PENDING, ST_WAITING = CO_WAITING, ST_RUNNING = CO_RUNNING,
+              ST_PREEMPTED = CO_PREEMPTED, ST_COMPLETED = CO_COMPLETED;
+
+enum ActKind : int32_t { A_ALLOCATE = 0, A_GROW = 1, A_RESERVE = 2, A_EMBED = 3 };
+
+// Engine scalars shared by every kernel of a step (device memory).
+struct Ctl {
+    int64_t now, horizon, first_arrival, t_i;
+    int64_t fp_sum, granted_sum, used_sum;          // kvc.py:83-84, used_tokens kvc.py:109
+    int64_t gen_total, iters, steps, seq;
+    int64_t ev_count, mem_count, sample_count;      // undrained append-buffer fill
+    int64_t mark[5];                                 // engine.py:647-650 progress mark
+    int64_t streak;
+    int32_t has_mark, guard;                         // guard: run() semantics active
+    int32_t rsv_cur, n_live, next_pending, adm_lo, adm_hi;
+    int32_t done, stalled, error, paused;
+    int32_t active;                                   // this step proceeds past begin
+    int32_t last_result;                              // step() return value
+    int32_t cnt_nw, cnt_nwp, cnt_run;                 // classify counts
+    int32_t sid;                                      // stamp id of the current step
+    int32_t check_due;
+    int32_t err_info[4];
+};
+
+// The plan of one step (scheduler.py:295-323 BatchPlan) as device lists.
+struct PlanHdr {
+    int32_t n_mem, n_act, n_pre, n_cl, n_def, overflow, sated, k_sel;
+    int64_t batch_tokens;
+};
+
+struct Dev {
+    // configuration (co_config + derived)
+    int32_t n, bs, B, buffer_b, token_budget, prealloc_m, runway_iters, fcfs;
+    int32_t record_events, validate_every, pad, idbits, n_edges, token_step, rsv_target;
+    int64_t eps, capacity, s_star, s_max, ev_cap, mem_cap, sample_cap;
+    int64_t edges[CO_MAX_SLO_EDGES];
+    double base_ms, per_token_ms;
+    // trace (sorted order)
+    const int64_t *rid, *arr, *slo_ttft, *slo_tbt;
+    const int32_t *prompt, *tout, *idrank, *err;
+    const uint8_t* flip;
+    // LUTs
+    const int64_t *lut_swap_half, *lut_rec, *lut_surv_swap, *lut_surv_rec;
+    // runtime (core.py:72-94)
+    int8_t *state, *last_strat;
+    int32_t *gen, *used, *kv_need, *prefill, *pcount, *pred, *est, *alloc_kvc;
+    int64_t *first_tok, *last_tok, *max_tbt, *ready_at, *pstart, *swap_done, *first_start,
+        *completion, *ptime;
+    const int64_t* tok_off;
+    int64_t* tok_times;
+    // pool records (kvc.py:44-52); no stacking: at most one guest per host
+    uint8_t* holds;
+    int32_t *granted, *host, *off, *rsv, *guest;
+    int64_t* rec_seq;
+    // claims provider -> waiter (engine.py:246) with lazy invalidation epochs
+    int32_t *claim_w, *claim_ep, *epoch;
+    // per-step membership stamps (compared with Ctl::sid, never cleared)
+    int32_t *st_nr, *st_crit, *st_removed, *st_embedded, *st_resumed, *st_stalled, *st_parts,
+        *st_claimed, *st_failed, *st_seen, *st_acted, *st_deferred;
+    // classify + sort
+    uint64_t *keys_in, *keys_out;
+    uint32_t *vals_in, *vals_out;
+    // plan buffers
+    PlanHdr* plan;
+    int32_t *mem_idx, *mem_tok, *act_kind, *act_idx, *act_tok, *act_nb, *act_host, *act_start;
+    int32_t *pre_idx, *pre_strat, *cl_w, *cl_p, *def_idx;
+    // planner / apply scratch (n-sized unless noted)
+    int32_t *l_nr, *l_nrp, *l_pend, *l_tri, *l_tri_taken, *l_vict, *l_defer, *l_pro, *l_ful,
+        *l_part, *l_part_need, *l_part_grant, *l_mready, *l_gm_idx, *l_gm_tok, *l_acted,
+        *l_surv_idx, *l_surv_tok, *l_done, *l_coll, *l_grp;
+    int64_t* l_tri_key;
+    uint64_t *am_rhi, *am_rlo;   // amortize remainders (128-bit), by participant position
+    int32_t* rank_to_idx;        // inverse of idrank
+    uint64_t *sk0, *sk1, *sk2;   // generic sort keys
+    int32_t* sk_item;
+    // outputs
+    co_event* events;
+    int32_t* members;   // (idx, tok) pairs
+    int64_t* samples;   // (footprint, used) pairs
+    Ctl* ctl;
+};
+
+// ---------------------------------------------------------------------------
+// per-request view quantities (engine.py:284-317, scheduler.py:99-118);
+// valid while the pool is not mutated (planning phase) or at the instant read
+
+__device__ __forceinline__ int64_t fp_tokens(int64_t t, int bs) { return ((t + bs - 1) / bs) * bs; }
+
+__device__ __forceinline__ int64_t rt_of(const Dev& d, int i, int64_t now) {
+    return d.first_tok[i] < 0 ? d.slo_ttft[i] - (now - d.arr[i]) : d.slo_tbt[i] - (now - d.last_tok[i]);
+}
+__device__ __forceinline__ int32_t eff_of(const Dev& d, int i) {
+    if (!d.holds[i]) return 0;
+    int32_t g = d.granted[i];
+    int32_t gu = d.guest[i];
+    if (gu >= 0) { int32_t o = d.off[gu]; return o < g ? o : g; }
+    return g;
+}
+__device__ __forceinline__ bool guest_of(const Dev& d, int i) { return d.holds[i] && d.host[i] >= 0; }
+__device__ __forceinline__ int32_t est_rem(const Dev& d, int i) {
+    int32_t r = d.est[i] - d.gen[i];
+    return r > 0 ? r : 0;
+}
+__device__ __forceinline__ int32_t target_of(const Dev& d, int i) {
+    int32_t a = d.used[i] > d.kv_need[i] ? d.used[i] : d.kv_need[i];
+    return a + est_rem(d, i);
+}
+__device__ __forceinline__ bool returned_of(const Dev& d, int i) {
+    return d.state[i] == ST_RUNNING && eff_of(d, i) < d.used[i] + 1;
+}
+__device__ __forceinline__ bool ready_of(const Dev& d, int i, int64_t now) {
+    return d.state[i] != ST_RUNNING || now >= d.ready_at[i];
+}
+// _FreeTracker.alloc_cost (scheduler.py:350-354)
+__device__ __forceinline__ int64_t cost_of(const Dev& d, int i, int64_t grant) {
+    if (guest_of(d, i)) return 0;
+    int64_t h = d.holds[i] ? d.granted[i] : 0;
+    return fp_tokens(h + grant, d.bs) - fp_tokens(h, d.bs);
+}
+__device__ __forceinline__ int64_t free_tokens(const Dev& d) {
+    const Ctl& c = *d.ctl;
+    return d.capacity - (int64_t)c.rsv_cur * d.bs - c.fp_sum;
+}
+// BlockPool.net_release_gain (kvc.py:142-152)
+__device__ __forceinline__ int64_t gain_of(const Dev& d, int i) {
+    if (d.host[i] >= 0) return 0;
+    int64_t freed = fp_tokens(d.granted[i], d.bs);
+    int32_t g = d.guest[i];
+    if (g >= 0) freed -= fp_tokens(d.granted[g], d.bs);
+    int64_t room = (int64_t)d.rsv_target - d.ctl->rsv_cur;
+    int64_t refill = d.rsv[i] < room ? d.rsv[i] : room;
+    return freed - refill * d.bs;
+}
+// preemption.py:198-200 via engine.py:355-358
+__device__ __forceinline__ int32_t strategy_of(const Dev& d, int i) {
+    int64_t s = d.used[i] > 1 ? d.used[i] : 1;
+    return s > d.s_star ? CO_SWAP : CO_RECOMPUTE;
+}
+__device__ __forceinline__ int64_t lut(const int64_t* t, int64_t s, int64_t smax) {
+    return t[s < smax ? s : smax];
+}
+// costmodel.py:51-55 iteration_latency in IEEE double, no contraction
+__device__ __forceinline__ double iter_ms(const Dev& d, int64_t tokens) {
+    return __dadd_rn(d.base_ms, __dmul_rn(d.per_token_ms, (double)tokens));
+}
+// core.py:21-23 to_us
+__device__ __forceinline__ int64_t to_us_d(double ms) { return (int64_t)floor(__dadd_rn(__dmul_rn(ms, 1000.0), 0.5)); }
+
+}  // namespace co

@@ -1,0 +1,641 @@
+// k_plan: the CacheOPT planner (scheduler.py:408-753, rows a4-a10) on one
+// 1024-thread CTA.  The reference's greedy loops are order dependent and
+// operate on a running free counter, so they run in reference order on
+// thread 0 over staged lists, while every N-wide pass (set construction,
+// demand sums, decode membership, the token-budget prefix, the case-2 extras
+// walk, the pair-release provider search, the amortized split's ranking) is
+// a block-cooperative scan / reduction / compaction / rank sort.
+#pragma once
+#include "block_ops.cuh"
+#include "pool_ops.cuh"
+
+namespace co {
+
+struct PlanSh {
+    BlkShared b;
+    int64_t free, shortfall, runway, batch_now, gm_tokens;
+    int64_t f_total, a_total, f_supply, a_supply, tbt_floor, lim, resid;
+    int32_t rsvb, n_mem, n_act, n_pre, n_cl, n_def, n_gm, n_pend, n_mready, n_part;
+    int32_t k_sel, search, cur, pos, stop, sated, overflow, g_nlive, g_left;
+};
+
+__device__ __forceinline__ void push_act(const Dev& d, PlanSh& S, int32_t kind, int32_t i, int64_t tok,
+                                         int32_t nb = 0, int32_t h = -1, int64_t start = 0) {
+    int32_t p = S.n_act++;
+    d.act_kind[p] = kind; d.act_idx[p] = i; d.act_tok[p] = (int32_t)tok;
+    d.act_nb[p] = nb; d.act_host[p] = h; d.act_start[p] = (int32_t)start;
+}
+__device__ __forceinline__ void push_mem(const Dev& d, PlanSh& S, int32_t i, int64_t tok) {
+    int32_t p = S.n_mem++;
+    d.mem_idx[p] = i; d.mem_tok[p] = (int32_t)tok;
+    S.batch_now += tok;
+}
+
+// scheduler.py:432-449 try_embed + kvc.py:169-200 find_embedding_host.
+// Without stacking a host is feasible iff (a_j - u_j) >= b + need + out, so
+// with the hosts sorted by (a_j - u_j, id) the argmin is the first free entry
+// at or after a lower bound.
+__device__ bool try_embed(const Dev& d, PlanSh& S, int32_t i, int32_t n_tri, int32_t sid) {
+    if (eff_of(d, i) > 0 || d.pcount[i] > 0) return false;
+    int32_t er = est_rem(d, i);
+    int32_t pg = d.pred[i] - d.gen[i];
+    int32_t out = er > pg ? er : pg;
+    if (out < 1) out = 1;
+    int64_t need = (int64_t)d.kv_need[i] + out;
+    int64_t thr = (int64_t)d.buffer_b + need + out;
+    int32_t lo = 0, hi = n_tri;
+    while (lo < hi) {
+        int32_t mid = (lo + hi) >> 1;
+        if (d.l_tri_key[mid] < thr) lo = mid + 1; else hi = mid;
+    }
+    while (lo < n_tri && (d.l_tri_taken[lo] || d.st_removed[d.l_tri[lo]] == sid)) lo++;
+    if (lo >= n_tri) return false;
+    int32_t h = d.l_tri[lo];
+    push_act(d, S, A_EMBED, i, need, 0, h, (int64_t)d.granted[h] - need);
+    d.st_embedded[i] = sid;
+    d.l_tri_taken[lo] = 1;  // one guest per host per plan (scheduler.py:446-448)
+    return true;
+}
+
+__device__ __forceinline__ int64_t nw_need(const Dev& d, int32_t i) {  // scheduler.py:166-167
+    int64_t v = (int64_t)d.kv_need[i] + d.B - eff_of(d, i);
+    return v > 0 ? v : 0;
+}
+
+__device__ __forceinline__ void amort_weight(const Dev& d, int32_t i, int64_t now, uint64_t& w) {
+    int64_t rt = rt_of(d, i, now);   // scheduler.py:645: max(1, rt_us), max(1, kv_need)
+    if (rt < 1) rt = 1;
+    int64_t pr = d.kv_need[i] < 1 ? 1 : d.kv_need[i];
+    w = (uint64_t)rt * (uint64_t)pr;
+}
+
+// allocate_remaining (scheduler.py:211-243) + block flooring
+// (scheduler.py:642-660) over participant positions grp[0..m).  Exact
+// integer restatement of the Fraction arithmetic: every share has the common
+// denominator W, so floor(share_i) = q_i and the fractional order is the
+// order of r_i = supply*w_i mod W (unsigned 128-bit).
+__device__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64_t supply, int64_t now,
+                         int64_t* total_out) {
+    const int tid = threadIdx.x;
+    int64_t tot = 0, live_tot = 0, nlive = 0;
+    for (int32_t k = tid; k < m; k += NT) {
+        int32_t p = grp[k];
+        int64_t need = d.l_part_need[p];
+        tot += need;
+        if (need > 0) { live_tot += need; nlive += 1; }
+        d.l_part_grant[p] = 0;
+    }
+    tot = blk_sum(tot, S.b);
+    live_tot = blk_sum(live_tot, S.b);
+    nlive = blk_sum(nlive, S.b);
+    *total_out = tot;
+    if (nlive == 0) return;
+    if (live_tot <= supply) {
+        for (int32_t k = tid; k < m; k += NT) {
+            int32_t p = grp[k];
+            int64_t need = d.l_part_need[p];
+            if (need > 0) d.l_part_grant[p] = (int32_t)need;
+        }
+        __syncthreads();
+        return;
+    }
+    if (tid == 0) {
+        int32_t w = 0;
+        for (int32_t k = 0; k < m; k++)
+            if (d.l_part_need[grp[k]] > 0) grp[w++] = grp[k];
+        S.g_nlive = w;
+        unsigned __int128 W = 0;
+        for (int32_t k = 0; k < w; k++) {
+            uint64_t wi;
+            amort_weight(d, d.l_part[grp[k]], now, wi);
+            W += (unsigned __int128)wi;
+        }
+        int64_t sq = 0;
+        for (int32_t k = 0; k < w; k++) {
+            int32_t p = grp[k];
+            uint64_t wi;
+            amort_weight(d, d.l_part[p], now, wi);
+            unsigned __int128 x = (unsigned __int128)(uint64_t)supply * (unsigned __int128)wi;
+            unsigned __int128 q = x / W, r = x % W;
+            d.l_part_grant[p] = (int32_t)(uint64_t)q;
+            sq += (int64_t)(uint64_t)q;
+            d.am_rhi[p] = (uint64_t)(r >> 64);
+            d.am_rlo[p] = (uint64_t)r;
+        }
+        S.g_left = (int32_t)(supply - sq);
+    }
+    __syncthreads();
+    const int32_t w = S.g_nlive;
+    const int32_t left = S.g_left;
+    // largest remainder first, ties by req_id (scheduler.py:240-242)
+    blk_sort(grp, w, [&](int32_t p, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
+        k0 = ~d.am_rhi[p];
+        k1 = ~d.am_rlo[p];
+        k2 = (uint64_t)d.idrank[d.l_part[p]];
+    }, d, S.b);
+    for (int32_t k = tid; k < left && k < w; k += NT) d.l_part_grant[grp[k]] += 1;
+    __syncthreads();
+    if (tot > supply) {
+        const int bs = d.bs;
+        int64_t fsum = 0;
+        for (int32_t k = tid; k < w; k += NT) {
+            int64_t g = d.l_part_grant[grp[k]];
+            fsum += (g / bs) * bs;
+        }
+        fsum = blk_sum(fsum, S.b);
+        const int64_t left_blocks = (supply - fsum) / bs;
+        blk_sort(grp, w, [&](int32_t p, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
+            int64_t g = d.l_part_grant[p];
+            k0 = 0x7fffffffull - (uint64_t)(g - (g / bs) * bs);
+            k1 = (uint64_t)d.idrank[d.l_part[p]];
+            k2 = 0;
+        }, d, S.b);
+        for (int32_t k = tid; k < w; k += NT) {
+            int32_t p = grp[k];
+            int64_t g = d.l_part_grant[p];
+            g = (g / bs) * bs;
+            if (k < left_blocks) g += bs;
+            d.l_part_grant[p] = (int32_t)g;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
+    __shared__ PlanSh S;
+    const Ctl& c = *d.ctl;
+    if (!c.active) return;
+    const int tid = threadIdx.x;
+    const int64_t now = c.now, ti = c.t_i, eps = d.eps;
+    const int32_t sid = c.sid;
+    const int32_t n_nw = c.cnt_nw, n_nwp = c.cnt_nwp, n_run = c.cnt_run;
+    const int32_t* NW = reinterpret_cast<const int32_t*>(d.vals_out);
+    const int32_t* NWP = NW + n_nw;
+    const int32_t* RUN = NWP + n_nwp;
+    const int B = d.B, bs = d.bs;
+    if (tid == 0) {
+        S.free = free_tokens(d);
+        S.rsvb = c.rsv_cur;
+        S.n_mem = S.n_act = S.n_pre = S.n_cl = S.n_def = S.n_gm = S.n_pend = S.n_mready = S.n_part = 0;
+        S.batch_now = 0; S.gm_tokens = 0; S.overflow = 0; S.sated = 0;
+    }
+    __syncthreads();
+
+    // ---- returned running (scheduler.py:142-150, 161-162) ------------------
+    auto crit_rt = [&](int64_t r) { return r >= -eps && r - ti < eps; };
+    const int32_t n_nr = blk_compact(RUN, n_run, d.l_nr, [&](int32_t i) {
+        return ready_of(d, i, now) && returned_of(d, i) && crit_rt(rt_of(d, i, now));
+    }, S.b);
+    const int32_t n_nrp = blk_compact(RUN, n_run, d.l_nrp, [&](int32_t i) {
+        return ready_of(d, i, now) && returned_of(d, i) && !crit_rt(rt_of(d, i, now));
+    }, S.b);
+    blk_sort(d.l_nr, n_nr, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
+        k0 = (uint64_t)(rt_of(d, i, now) + (1ll << 62)); k1 = (uint64_t)d.idrank[i]; k2 = 0;
+    }, d, S.b);
+    blk_sort(d.l_nrp, n_nrp, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
+        int64_t r = rt_of(d, i, now);
+        k0 = r < 0 ? 1 : 0; k1 = r < 0 ? (uint64_t)d.arr[i] : (uint64_t)r; k2 = (uint64_t)d.idrank[i];
+    }, d, S.b);
+    for (int32_t k = tid; k < n_nr; k += NT) d.st_nr[d.l_nr[k]] = sid;
+
+    // ---- embedding hosts (scheduler.py:425-430) sorted by (a_j - u_j, id) --
+    const int32_t n_tri = blk_compact(RUN, n_run, d.l_tri, [&](int32_t i) {
+        return !guest_of(d, i) && d.holds[i] && d.prefill[i] >= d.kv_need[i];
+    }, S.b);
+    blk_sort(d.l_tri, n_tri, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
+        k0 = (uint64_t)((int64_t)d.granted[i] - d.used[i] + (1ll << 40)); k1 = (uint64_t)d.idrank[i]; k2 = 0;
+    }, d, S.b);
+    for (int32_t k = tid; k < n_tri; k += NT) {
+        int32_t h = d.l_tri[k];
+        d.l_tri_key[k] = (int64_t)d.granted[h] - d.used[h];
+        d.l_tri_taken[k] = d.guest[h] >= 0 ? 1 : 0;  // already hosting: skipped without stacking
+    }
+    __syncthreads();
+
+    // ---- critical waiting: embed first (scheduler.py:451-457) -------------
+    if (tid == 0) {
+        for (int32_t k = 0; k < n_nw; k++) {
+            int32_t i = NW[k];
+            if (try_embed(d, S, i, n_tri, sid)) {
+                int32_t ch = d.kv_need[i] - d.prefill[i];
+                d.l_gm_idx[S.n_gm] = i; d.l_gm_tok[S.n_gm] = ch; S.n_gm++;
+                S.gm_tokens += ch;
+            } else {
+                d.l_pend[S.n_pend++] = i;
+            }
+        }
+    }
+    __syncthreads();
+    const int32_t n_pend0 = S.n_pend;
+
+    // ---- exact-consumption demand and reserve (scheduler.py:459-472) ------
+    int64_t dem = 0;
+    for (int32_t k = tid; k < n_pend0; k += NT) { int32_t i = d.l_pend[k]; dem += cost_of(d, i, nw_need(d, i)); }
+    for (int32_t k = tid; k < n_nr; k += NT) { int32_t i = d.l_nr[k]; if (!guest_of(d, i)) dem += cost_of(d, i, B); }
+    dem = blk_sum(dem, S.b);
+    if (tid == 0) {
+        int64_t sf = dem - S.free;
+        if (sf < 0) sf = 0;
+        if (sf > 0) { int64_t r = (int64_t)S.rsvb * bs; sf -= sf < r ? sf : r; }
+        S.shortfall = sf;
+    }
+    __syncthreads();
+
+    // ---- victims and deferral (scheduler.py:474-507) ----------------------
+    if (S.shortfall > 0) {
+        for (int32_t k = tid; k < n_pend0; k += NT) d.st_crit[d.l_pend[k]] = sid;
+        for (int32_t k = tid; k < n_nr; k += NT) d.st_crit[d.l_nr[k]] = sid;
+        __syncthreads();
+        const bool fcfs = d.fcfs;
+        const int32_t n_v = blk_compact(RUN, n_run, d.l_vict, [&](int32_t i) {
+            return !guest_of(d, i) && d.st_crit[i] != sid && d.holds[i] && gain_of(d, i) > 0 &&
+                   (fcfs || d.prefill[i] >= d.kv_need[i]);
+        }, S.b);
+        blk_sort(d.l_vict, n_v, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
+            if (fcfs) {  // scheduler.py:397-398: (-arrival, id)
+                k0 = (uint64_t)((1ll << 62) - d.arr[i]); k1 = (uint64_t)d.idrank[i]; k2 = 0;
+            } else {     // preemption.py:54-64: (-slo bucket, -remaining bucket, occupancy, id)
+                uint64_t sb = 0;
+                for (int e = 0; e < d.n_edges; e++) sb += d.slo_tbt[i] >= d.edges[e] ? 1 : 0;
+                uint64_t rb = (uint64_t)(est_rem(d, i) / d.token_step);
+                k0 = ((15ull - sb) << 32) | (0x7fffffffull - rb);
+                k1 = (uint64_t)(uint32_t)d.used[i];
+                k2 = (uint64_t)d.idrank[i];
+            }
+        }, d, S.b);
+        if (tid == 0) {
+            const int64_t queued = (int64_t)n_nw + n_nwp;  // every waiting view is ready
+            for (int32_t k = 0; k < n_v && S.shortfall > 0; k++) {
+                int32_t i = d.l_vict[k];
+                int32_t strat = strategy_of(d, i);
+                if (!fcfs) {  // _survives_eviction (scheduler.py:362-375)
+                    int64_t s = d.used[i] > 1 ? d.used[i] : 1;
+                    int64_t charge = lut(strat == CO_SWAP ? d.lut_surv_swap : d.lut_surv_rec, s, d.s_max) +
+                                     ti * (1 + queued);
+                    if (!(rt_of(d, i, now) > charge)) continue;
+                }
+                int64_t g = gain_of(d, i);
+                d.pre_idx[S.n_pre] = i; d.pre_strat[S.n_pre] = strat; S.n_pre++;
+                d.st_removed[i] = sid;
+                S.free += g;
+                S.shortfall -= g;
+            }
+        }
+        __syncthreads();
+        if (S.shortfall > 0) {
+            for (int32_t k = tid; k < n_pend0; k += NT) d.l_defer[k] = d.l_pend[k];
+            __syncthreads();
+            blk_sort(d.l_defer, n_pend0, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
+                k0 = (uint64_t)((1ll << 62) - rt_of(d, i, now)); k1 = (uint64_t)d.idrank[i]; k2 = 0;
+            }, d, S.b);
+            if (tid == 0) {
+                for (int32_t k = 0; k < n_pend0 && S.shortfall > 0; k++) {
+                    int32_t i = d.l_defer[k];
+                    S.shortfall -= cost_of(d, i, nw_need(d, i));
+                    d.st_deferred[i] = sid;
+                    d.def_idx[S.n_def++] = i;
+                }
+            }
+            __syncthreads();
+        }
+    }
+
+    // ---- continuation, resumption, critical admission (scheduler.py:515-574)
+    if (tid == 0) {
+        const int32_t nb_B = (B + bs - 1) / bs;
+        for (int32_t k = 0; k < n_nr; k++) {
+            int32_t i = d.l_nr[k];
+            if (d.st_removed[i] == sid) continue;
+            int64_t cst = cost_of(d, i, B);
+            if (guest_of(d, i)) {
+                push_act(d, S, A_GROW, i, B);
+            } else if (cst <= S.free) {
+                push_act(d, S, A_GROW, i, B);
+                S.free -= cst;
+            } else if (S.rsvb >= nb_B) {
+                push_act(d, S, A_RESERVE, i, 0, nb_B);
+                S.rsvb -= nb_B;
+            } else {
+                d.st_stalled[i] = sid;
+            }
+        }
+        for (int32_t k = 0; k < n_nrp; k++) {
+            int32_t i = d.l_nrp[k];
+            if (d.st_removed[i] == sid) continue;
+            if (guest_of(d, i)) {
+                push_act(d, S, A_GROW, i, B);
+                d.st_resumed[i] = sid;
+                continue;
+            }
+            int64_t cst = cost_of(d, i, B);
+            if (cst <= S.free) {
+                push_act(d, S, A_GROW, i, B);
+                S.free -= cst;
+                d.st_resumed[i] = sid;
+            }
+        }
+        for (int32_t k = 0; k < n_pend0; k++) {
+            int32_t i = d.l_pend[k];
+            if (d.st_deferred[i] == sid) continue;
+            int64_t need = nw_need(d, i);
+            int64_t cst = cost_of(d, i, need);
+            if (cst <= S.free) {
+                push_act(d, S, d.holds[i] ? A_GROW : A_ALLOCATE, i, need);
+                S.free -= cst;
+            } else if (!guest_of(d, i)) {
+                int32_t nb = (int32_t)((need + bs - 1) / bs);
+                if (nb <= S.rsvb) {
+                    push_act(d, S, A_RESERVE, i, 0, nb);
+                    S.rsvb -= nb;
+                } else {
+                    d.def_idx[S.n_def++] = i;
+                    continue;
+                }
+            } else {
+                d.def_idx[S.n_def++] = i;
+                continue;
+            }
+            int32_t ch = d.kv_need[i] - d.prefill[i];
+            if (ch > 0) {
+                d.l_gm_idx[S.n_gm] = i; d.l_gm_tok[S.n_gm] = ch; S.n_gm++;
+                S.gm_tokens += ch;
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- decode members in running order (scheduler.py:576-593) -----------
+    const int32_t n_dec_mem = blk_compact(RUN, n_run, d.mem_idx, [&](int32_t i) {
+        if (d.st_removed[i] == sid || !ready_of(d, i, now) || d.prefill[i] < d.kv_need[i]) return false;
+        if (returned_of(d, i)) {
+            if (d.st_stalled[i] == sid) return false;
+            if (d.st_nr[i] != sid && d.st_resumed[i] != sid) return false;
+        }
+        return true;
+    }, S.b);
+    for (int32_t k = tid; k < n_dec_mem; k += NT) d.mem_tok[k] = 1;
+    const int32_t n_gm = S.n_gm;
+    for (int32_t k = tid; k < n_gm; k += NT) {
+        d.mem_idx[n_dec_mem + k] = d.l_gm_idx[k];
+        d.mem_tok[n_dec_mem + k] = d.l_gm_tok[k];
+    }
+    __syncthreads();
+    if (tid == 0) {
+        S.n_mem = n_dec_mem + n_gm;
+        S.batch_now = n_dec_mem + S.gm_tokens;
+    }
+    __syncthreads();
+    const int64_t consumed = S.batch_now;
+
+    // ---- token-budget fill over N'_w (scheduler.py:182-200, 596-598) ------
+    {
+        const int64_t budget = d.token_budget;
+        int64_t used_base = consumed;
+        int32_t ksel = n_nwp;
+        for (int32_t base = 0; base < n_nwp; base += NT) {
+            int32_t k = base + tid;
+            int32_t ch = 0;
+            if (k < n_nwp) { int32_t i = NWP[k]; ch = d.kv_need[i] - d.prefill[i]; }
+            int32_t tot;
+            int32_t ex = blk_excl_scan(ch, &tot, S.b);
+            bool over = k < n_nwp && used_base + ex + ch > budget;
+            uint64_t mk = blk_min(over ? (uint64_t)k : ~0ull, S.b);
+            if (mk != ~0ull) { ksel = (int32_t)mk; break; }
+            used_base += tot;
+        }
+        if (tid == 0) {
+            S.k_sel = ksel;
+            S.overflow = consumed > budget ? 1 : 0;
+        }
+    }
+    __syncthreads();
+    const int32_t k_sel = S.k_sel;
+
+    // ---- participants (scheduler.py:600-638) ------------------------------
+    if (tid == 0) {
+        for (int32_t k = 0; k < k_sel; k++) {
+            int32_t i = NWP[k];
+            if (try_embed(d, S, i, n_tri, sid)) { d.l_mready[S.n_mready++] = i; continue; }
+            int64_t t = target_of(d, i), f = (int64_t)d.kv_need[i] + 1;
+            int64_t need = (t > f ? t : f) - eff_of(d, i);
+            if (need <= 0) {
+                d.l_mready[S.n_mready++] = i;
+            } else {
+                d.l_part[S.n_part] = i; d.l_part_need[S.n_part] = (int32_t)need; S.n_part++;
+                d.st_parts[i] = sid;
+            }
+        }
+        for (int32_t k = 0; k < n_nrp; k++) {
+            int32_t i = d.l_nrp[k];
+            if (d.st_removed[i] == sid || guest_of(d, i) || d.st_resumed[i] != sid) continue;
+            int64_t res = (int64_t)target_of(d, i) - eff_of(d, i) - B;
+            if (res > 0) {
+                d.l_part[S.n_part] = i; d.l_part_need[S.n_part] = (int32_t)res; S.n_part++;
+                d.st_parts[i] = sid;
+            }
+        }
+    }
+    __syncthreads();
+    // proactive_include (scheduler.py:269-279) over the post-eviction running set
+    const int64_t mpre = d.prealloc_m;
+    const int32_t n_pro = blk_compact(RUN, n_run, d.l_pro, [&](int32_t i) {
+        return d.st_removed[i] != sid && !returned_of(d, i) && eff_of(d, i) < target_of(d, i) &&
+               est_rem(d, i) <= mpre;
+    }, S.b);
+    blk_sort(d.l_pro, n_pro, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
+        k0 = (uint64_t)est_rem(d, i); k1 = (uint64_t)d.idrank[i]; k2 = 0;
+    }, d, S.b);
+    if (tid == 0) {
+        for (int32_t k = 0; k < n_pro; k++) {
+            int32_t i = d.l_pro[k];
+            if (guest_of(d, i) || d.st_parts[i] == sid) continue;
+            d.l_part[S.n_part] = i; d.l_part_need[S.n_part] = target_of(d, i) - eff_of(d, i); S.n_part++;
+            d.st_parts[i] = sid;
+        }
+    }
+    __syncthreads();
+    // pre-exhaust top-up, running order (scheduler.py:625-638)
+    {
+        const int32_t base = S.n_part;
+        const int32_t n_top = blk_compact(RUN, n_run, d.l_part + base, [&](int32_t i) {
+            return d.st_removed[i] != sid && !guest_of(d, i) && ready_of(d, i, now) &&
+                   d.prefill[i] >= d.kv_need[i] && !returned_of(d, i) &&
+                   (int64_t)eff_of(d, i) - d.used[i] <= mpre && d.st_parts[i] != sid;
+        }, S.b);
+        for (int32_t k = tid; k < n_top; k += NT) {
+            int32_t i = d.l_part[base + k];
+            int64_t t = target_of(d, i), f = (int64_t)d.used[i] + 1 + B;
+            d.l_part_need[base + k] = (int32_t)((t > f ? t : f) - eff_of(d, i));
+        }
+        __syncthreads();
+        if (tid == 0) S.n_part = base + n_top;
+        __syncthreads();
+    }
+    const int32_t n_part = S.n_part;
+
+    // ---- amortized round (scheduler.py:662-682) ---------------------------
+    int64_t ndec = 0;
+    for (int32_t k = tid; k < n_run; k += NT) {
+        int32_t i = RUN[k];
+        if (d.st_removed[i] != sid && !guest_of(d, i) && d.prefill[i] >= d.kv_need[i]) ndec++;
+    }
+    ndec = blk_sum(ndec, S.b);
+    const int32_t n_fl = blk_compact(nullptr, n_part, d.l_grp, [&](int32_t p) {
+        return d.state[d.l_part[p]] == ST_RUNNING;
+    }, S.b);
+    const int32_t n_ad = blk_compact(nullptr, n_part, d.l_grp + n_part, [&](int32_t p) {
+        return d.state[d.l_part[p]] != ST_RUNNING;
+    }, S.b);
+    if (tid == 0) {
+        S.runway = (int64_t)d.runway_iters * ndec;
+        S.f_supply = (S.free / bs) * bs;  // free >= 0 throughout planning
+    }
+    __syncthreads();
+    int64_t ftot;
+    amortize(d, S, d.l_grp, n_fl, S.f_supply, now, &ftot);
+    int64_t spent = 0;  // sum of the in-flight grants (amortize compacts grp in place)
+    for (int32_t p = tid; p < n_part; p += NT)
+        if (d.state[d.l_part[p]] == ST_RUNNING) spent += d.l_part_grant[p];
+    spent = blk_sum(spent, S.b);
+    if (tid == 0) {
+        int64_t a = S.free - spent - S.runway;
+        if (a < 0) a = 0;
+        S.a_supply = (a / bs) * bs;
+        S.f_total = ftot;
+    }
+    __syncthreads();
+    int64_t atot;
+    amortize(d, S, d.l_grp + n_part, n_ad, S.a_supply, now, &atot);
+    if (tid == 0) {
+        S.a_total = atot;
+        S.sated = (S.f_total <= S.f_supply && S.a_total <= S.a_supply) ? 1 : 0;
+    }
+    __syncthreads();
+
+    // ---- grant application + pair-release claims (scheduler.py:684-720) ---
+    const int32_t n_ful = blk_compact(RUN, n_run, d.l_ful, [&](int32_t i) {
+        return !guest_of(d, i) && !returned_of(d, i) && eff_of(d, i) >= target_of(d, i) &&
+               d.st_removed[i] != sid;
+    }, S.b);
+    for (int32_t p = 0; p < n_part; p++) {
+        if (tid == 0) {
+            S.search = 0;
+            int32_t i = d.l_part[p];
+            int64_t need = d.l_part_need[p];
+            int64_t g = d.l_part_grant[p];
+            int64_t eff = eff_of(d, i);
+            bool skip = false;
+            if (d.state[i] != ST_RUNNING) {
+                if (eff + g < (int64_t)d.kv_need[i] + 1) {
+                    skip = true;  // a partial grant that cannot start prefill
+                } else {
+                    push_act(d, S, d.holds[i] ? A_GROW : A_ALLOCATE, i, g);
+                    S.free -= cost_of(d, i, g);
+                    d.l_mready[S.n_mready++] = i;
+                }
+            } else if (g > 0) {
+                push_act(d, S, A_GROW, i, g);
+                S.free -= cost_of(d, i, g);
+                if (returned_of(d, i) && eff + g >= (int64_t)d.used[i] + 1) push_mem(d, S, i, 1);
+            }
+            if (!skip && g < need) {
+                // scheduler.py:710 rebinds `runway`; the extras gate below sees it
+                S.runway = eff + g - d.used[i];
+                S.lim = S.runway > 0 ? S.runway : 0;
+                S.resid = need - g;
+                S.cur = i;
+                S.search = 1;
+            }
+        }
+        __syncthreads();
+        if (S.search) {
+            // pair_release (scheduler.py:253-266): soonest finisher, ties by id
+            const int64_t lim = S.lim, resid = S.resid;
+            uint64_t best = ~0ull;
+            for (int32_t k = tid; k < n_ful; k += NT) {
+                int32_t q = d.l_ful[k];
+                if (d.st_claimed[q] == sid) continue;
+                int64_t er = est_rem(d, q);
+                if (er > lim || gain_of(d, q) < resid) continue;
+                uint64_t key = ((uint64_t)er << 32) | (uint64_t)(uint32_t)d.idrank[q];
+                best = key < best ? key : best;
+            }
+            best = blk_min(best, S.b);
+            if (tid == 0 && best != ~0ull) {
+                int32_t q = d.rank_to_idx[(uint32_t)best];
+                d.cl_w[S.n_cl] = S.cur; d.cl_p[S.n_cl] = q; S.n_cl++;
+                d.st_claimed[q] = sid;
+            }
+            __syncthreads();
+        }
+    }
+    if (tid == 0) {
+        for (int32_t k = 0; k < S.n_mready; k++) {
+            int32_t i = d.l_mready[k];
+            if (d.state[i] == ST_WAITING) push_mem(d, S, i, d.kv_need[i] - d.prefill[i]);
+        }
+    }
+    __syncthreads();
+
+    // ---- case 2: extras while sated (scheduler.py:726-748) ----------------
+    if (S.sated) {
+        uint64_t fl = ~0ull;
+        for (int32_t k = tid; k < n_run; k += NT) {
+            int32_t x = RUN[k];
+            if (d.st_removed[x] == sid || d.last_tok[x] < 0 || returned_of(d, x)) continue;
+            if (d.max_tbt[x] > d.slo_tbt[x]) continue;
+            if (d.slo_tbt[x] - (now - d.last_tok[x]) < 0) continue;
+            uint64_t v = (uint64_t)d.slo_tbt[x];
+            fl = v < fl ? v : fl;
+        }
+        fl = blk_min(fl, S.b);
+        if (tid == 0) { S.tbt_floor = (int64_t)fl; S.stop = 0; S.pos = k_sel; }
+        __syncthreads();
+        const int64_t batch_now = S.batch_now;
+        const bool has_floor = fl != ~0ull;
+        for (int32_t base = k_sel; base < n_nwp && !S.stop; base += NT) {
+            int32_t k = base + tid;
+            int64_t need = 0, cst = 0;
+            if (k < n_nwp) {
+                int32_t i = NWP[k];
+                int64_t t = (int64_t)target_of(d, i) - eff_of(d, i);
+                need = t > 0 ? t : 0;
+                cst = cost_of(d, i, need);
+            }
+            while (true) {
+                const int64_t room = S.free - S.runway;
+                const int32_t pos = S.pos;
+                bool ok = k < n_nwp && k >= pos && need > 0 && cst <= room;
+                uint64_t mk = blk_min(ok ? (uint64_t)k : ~0ull, S.b);
+                if (mk == ~0ull) break;
+                if (tid == 0) {
+                    int32_t i = NWP[(int32_t)mk];
+                    if (has_floor) {
+                        double proj = iter_ms(d, batch_now + d.kv_need[i]);
+                        if (__dmul_rn(proj, 1000.0) > (double)S.tbt_floor) S.stop = 1;
+                    }
+                    if (!S.stop) {
+                        int64_t t = (int64_t)target_of(d, i) - eff_of(d, i);
+                        int64_t nd = t > 0 ? t : 0;
+                        push_act(d, S, d.holds[i] ? A_GROW : A_ALLOCATE, i, nd);
+                        S.free -= cost_of(d, i, nd);
+                        S.pos = (int32_t)mk + 1;
+                    }
+                }
+                __syncthreads();
+                if (S.stop) break;
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        PlanHdr& P = *d.plan;
+        P.n_mem = S.n_mem; P.n_act = S.n_act; P.n_pre = S.n_pre; P.n_cl = S.n_cl; P.n_def = S.n_def;
+        P.batch_tokens = S.batch_now;
+        P.overflow = (S.overflow || S.batch_now > d.token_budget) ? 1 : 0;
+        P.sated = S.sated;
+        P.k_sel = k_sel;
+    }
+}
+
+}  // namespace co

@@ -1,0 +1,489 @@
+"""Drop-in engine: the reference's ``Engine`` surface (engine.py:222-672)
+backed by the device engine in libcacheopt.so.
+
+``Engine(requests, cfg)`` uploads the trace once, ``step()`` runs one device
+scheduling round, ``run()`` runs the whole trace as CUDA-graph launches and
+returns the same ``MetricsReport``.  ``events``, ``runtimes``, ``requests`` and
+``pool`` are host views materialised from device readbacks on access.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import json
+from dataclasses import dataclass
+from typing import Dict, Iterator, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _native as N
+from .config import DEVICE_POLICIES, EngineConfig
+from .core import (STATE_FROM_CODE, STRATEGY_FROM_CODE, US_PER_S, Direction, LengthEstimate,
+                   Lifecycle, Request, RequestRuntime, Strategy)
+from .hostprep import (bin_of, charge_luts, iteration_us, noise_draws, run_confidence, run_padding,
+                       sweet_spot)
+
+STRATEGY_CODE = {Strategy.SWAP: 0, Strategy.RECOMPUTE: 1}
+CAUSE_CODE = {"plan": 0, "squeeze": 1, "collision": 2}
+
+
+@dataclass
+class MetricsReport:
+    policy: str
+    seed: int
+    num_requests: int
+    completed: int
+    makespan_us: int
+    ttft_us: Dict[str, float]
+    tbt_us: Dict[str, float]
+    ttft_attainment: float
+    tbt_attainment: float
+    normalized_us_per_token: Dict[str, float]
+    preemption_total: int
+    preempted_requests: int
+    preemption_time_us: Dict[str, float]
+    throughput_rps: float
+    throughput_tps: float
+    kvc_utilization_mean: float
+    kvc_fragmentation_mean: float
+    waiting_us_mean: float
+    execution_us_mean: float
+    preemption_us_mean: float
+
+    def to_dict(self) -> dict:
+        return dataclasses.asdict(self)
+
+
+def _pct(values) -> Dict[str, float]:
+    if len(values) == 0:
+        return {"p50": 0.0, "p90": 0.0, "p99": 0.0, "max": 0.0, "mean": 0.0}
+    a = np.asarray(values, dtype=float)
+    return {"p50": float(np.percentile(a, 50)), "p90": float(np.percentile(a, 90)),
+            "p99": float(np.percentile(a, 99)), "max": float(a.max()), "mean": float(a.mean())}
+
+
+def compute_metrics(*, requests: Dict[int, Request], runtimes: Dict[int, RequestRuntime], policy: str,
+                    seed: int, makespan_us: int, capacity_tokens: int,
+                    samples: Sequence[Tuple[int, int]]) -> MetricsReport:
+    """Outcome aggregation with the reference's definitions (engine.py:132-211):
+    latency percentiles over completed requests, attainment over all of
+    them, utilization/fragmentation from per-iteration (footprint, used)."""
+    n = len(requests)
+    ttfts, gaps_all, norm, waits, execs, pdec = [], [], [], [], [], []
+    ok_ttft = ok_tbt = done = 0
+    for rid, req in requests.items():
+        rt = runtimes[rid]
+        tt = rt.token_times_us
+        gaps = [b - a for a, b in zip(tt, tt[1:])]
+        if rt.first_token_at_us is not None and rt.first_token_at_us - req.arrival_us <= req.slo_ttft_us:
+            ok_ttft += 1
+        if req.state is not Lifecycle.COMPLETED:
+            continue
+        done += 1
+        if all(g <= req.slo_tbt_us for g in gaps):
+            ok_tbt += 1
+        ttfts.append(rt.first_token_at_us - req.arrival_us)
+        gaps_all.extend(gaps)
+        norm.append((rt.completion_us - req.arrival_us) / req.true_output_len)
+        waits.append(rt.first_start_us - req.arrival_us)
+        pdec.append(rt.preemption_time_us)
+        execs.append(rt.completion_us - rt.first_start_us - rt.preemption_time_us)
+    hit = [rt for rt in runtimes.values() if rt.preemption_count > 0]
+    span_s = makespan_us / US_PER_S if makespan_us > 0 else 0.0
+    gen_total = sum(rt.generated for rt in runtimes.values())
+    if len(samples):
+        util = float(np.mean([fp / capacity_tokens for fp, _ in samples]))
+        frag = float(np.mean([(fp - u) / capacity_tokens for fp, u in samples]))
+    else:
+        util = frag = 0.0
+
+    def mean(xs):
+        return float(np.mean(xs)) if xs else 0.0
+
+    return MetricsReport(
+        policy=policy, seed=seed, num_requests=n, completed=done, makespan_us=makespan_us,
+        ttft_us=_pct(ttfts), tbt_us=_pct(gaps_all),
+        ttft_attainment=ok_ttft / n if n else 0.0, tbt_attainment=ok_tbt / n if n else 0.0,
+        normalized_us_per_token=_pct(norm),
+        preemption_total=sum(rt.preemption_count for rt in runtimes.values()),
+        preempted_requests=len(hit), preemption_time_us=_pct([rt.preemption_time_us for rt in hit]),
+        throughput_rps=done / span_s if span_s else 0.0,
+        throughput_tps=gen_total / span_s if span_s else 0.0,
+        kvc_utilization_mean=util, kvc_fragmentation_mean=frag,
+        waiting_us_mean=mean(waits), execution_us_mean=mean(execs), preemption_us_mean=mean(pdec),
+    )
+
+
+def write_events_jsonl(events: Sequence[dict], path: str) -> None:
+    """One sorted-key compact JSON object per line (engine.py:214-219)."""
+    with open(path, "w") as fh:
+        for ev in events:
+            fh.write(json.dumps(ev, sort_keys=True, separators=(",", ":")))
+            fh.write("\n")
+
+
+def _ptr(a: np.ndarray, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+class PoolView:
+    """Read-only view of the device KV pool with the BlockPool query API
+    (kvc.py:86-140)."""
+
+    def __init__(self, eng: "Engine"):
+        self._e = eng
+
+    def _f(self, name):
+        return self._e._field(name)
+
+    @property
+    def capacity(self) -> int:
+        return self._e.cfg.capacity_tokens
+
+    @property
+    def block_size(self) -> int:
+        return self._e.cfg.sched.small_block_b
+
+    @property
+    def buffer_b(self) -> int:
+        return self._e.cfg.sched.buffer_b
+
+    @property
+    def reserved_target(self) -> int:
+        return self._e.cfg.reserved_blocks
+
+    @property
+    def reserved_blocks_current(self) -> int:
+        return int(self._e._scalars().reserved_blocks_current)
+
+    @property
+    def free_tokens(self) -> int:
+        s = self._e._scalars()
+        return self.capacity - s.reserved_blocks_current * self.block_size - s.footprint_tokens
+
+    @property
+    def footprint_tokens(self) -> int:
+        return int(self._e._scalars().footprint_tokens)
+
+    @property
+    def granted_tokens(self) -> int:
+        return int(self._e._scalars().granted_tokens)
+
+    @property
+    def used_tokens(self) -> int:
+        return int(self._e._scalars().used_tokens)
+
+    def _idx(self, rid: int) -> int:
+        k = self._e._idx_of.get(rid)
+        if k is None or not self._f("HOLDS")[k]:
+            raise ValueError(f"no allocation for request {rid}")
+        return k
+
+    def holds(self, rid: int) -> bool:
+        k = self._e._idx_of.get(rid)
+        return k is not None and bool(self._f("HOLDS")[k])
+
+    def granted_of(self, rid: int) -> int:
+        return int(self._f("GRANTED")[self._idx(rid)])
+
+    def used_of(self, rid: int) -> int:
+        return int(self._f("USED")[self._idx(rid)])
+
+    def host_of(self, rid: int) -> Optional[int]:
+        h = int(self._f("HOST")[self._idx(rid)])
+        return None if h < 0 else self._e._rid[h]
+
+    def offset_of(self, rid: int) -> int:
+        k = self._idx(rid)
+        return int(self._f("EMBED_OFFSET")[k]) if self._f("HOST")[k] >= 0 else 0
+
+    def reserved_drawn_of(self, rid: int) -> int:
+        return int(self._f("RESERVED_DRAWN")[self._idx(rid)])
+
+    def guests_of(self, rid: int) -> List[int]:
+        k = self._idx(rid)
+        host = self._f("HOST")
+        holds = self._f("HOLDS")
+        return [self._e._rid[g] for g in np.nonzero((host == k) & (holds == 1))[0]]
+
+    def owners(self) -> List[int]:
+        holds = self._f("HOLDS")
+        seq = self._f("RECORD_SEQ")
+        idx = np.nonzero(holds)[0]
+        return [self._e._rid[k] for k in idx[np.argsort(seq[idx], kind="stable")]]
+
+
+class _Runtimes(dict):
+    pass
+
+
+class Engine:
+    """Device-backed drop-in for the reference Engine (policy ``cacheopt``)."""
+
+    def __init__(self, requests: Sequence[Request], cfg: EngineConfig, device: int = -1,
+                 steps_per_launch: int = 32):
+        ids = [r.id for r in requests]
+        if len(set(ids)) != len(ids):
+            raise ValueError("request ids must be unique")
+        if cfg.sched.policy not in DEVICE_POLICIES:
+            raise ValueError(f"policy {cfg.sched.policy!r} has no device implementation "
+                             f"(device policies: {DEVICE_POLICIES})")
+        if cfg.sched.invert_amortization:
+            raise ValueError("invert_amortization=True is not supported by the device planner")
+        if cfg.allow_stacking:
+            raise ValueError("allow_stacking=True is not supported by the device pool")
+        self.cfg = cfg
+        self.requests: Dict[int, Request] = {r.id: r for r in requests}
+        self._input_order = ids
+        self.steps_per_launch = steps_per_launch
+        lib = N.load()
+        n = len(requests)
+        req_id = np.array(ids, dtype=np.int64)
+        arr = np.array([r.arrival_us for r in requests], dtype=np.int64)
+        prompt = np.array([r.prompt_len for r in requests], dtype=np.int32)
+        tout = np.array([r.true_output_len for r in requests], dtype=np.int32)
+        ttft = np.array([r.slo_ttft_us for r in requests], dtype=np.int64)
+        tbt = np.array([r.slo_tbt_us for r in requests], dtype=np.int64)
+        order = np.lexsort((req_id, arr)) if n else np.zeros(0, dtype=np.int64)
+        self._rid = [int(x) for x in req_id[order]]
+        self._idx_of = {r: k for k, r in enumerate(self._rid)}
+        arr_sorted = arr[order]
+        self.confidence = run_confidence(cfg, arr_sorted)
+        self.padding = run_padding(cfg, self.confidence)
+        err, flip = noise_draws(cfg, n)
+        s_max = int((prompt.astype(np.int64) + tout).max()) if n else 1
+        luts = charge_luts(cfg, max(s_max, 1))
+        self._keep = [req_id, arr, prompt, tout, ttft, tbt, err, flip, *luts]
+        tout_s = tout[order].astype(np.int64)
+        pred_s = np.maximum(1, tout_s - err)
+        self._under = (tout_s >= pred_s) ^ (flip.astype(bool))  # estimation.py:96-98
+        sc = cfg.sched
+        edges = list(sc.buckets.slo_edges_us)
+        if len(edges) > N.MAX_SLO_EDGES:
+            raise ValueError("at most 8 SLO bucket edges are supported")
+        c = N.CoConfig()
+        c.capacity_tokens = cfg.capacity_tokens
+        c.reserved_blocks = cfg.reserved_blocks
+        c.allow_stacking = int(cfg.allow_stacking)
+        c.block_size = sc.small_block_b
+        c.buffer_b = sc.buffer_b
+        c.token_budget = sc.token_budget
+        c.preallocate_m = sc.preallocate_m
+        c.decode_runway_iters = sc.decode_runway_iters
+        c.victim_rule_fcfs = 1 if sc.victim_rule == "fcfs" else 0
+        c.epsilon_us = sc.epsilon_us
+        c.n_slo_edges = len(edges)
+        c.token_step = sc.buckets.token_step
+        for k, e in enumerate(edges):
+            c.slo_edges_us[k] = int(e)
+        c.iter_base_ms = float(cfg.iter_cost.base_ms)
+        c.iter_per_token_ms = float(cfg.iter_cost.per_token_ms)
+        c.horizon_factor = cfg.horizon_factor
+        c.validate_every = cfg.validate_every
+        c.record_events = int(cfg.record_events)
+        c.padding = self.padding
+        c.s_star = sweet_spot(cfg.truth.swap_true, cfg.truth.recompute_true)
+        c.t_i_init_us = iteration_us(cfg, sc.token_budget)
+        t = N.CoTrace()
+        t.n = n
+        t.req_id = _ptr(req_id, C.c_int64)
+        t.arrival_us = _ptr(arr, C.c_int64)
+        t.prompt_len = _ptr(prompt, C.c_int32)
+        t.true_output_len = _ptr(tout, C.c_int32)
+        t.slo_ttft_us = _ptr(ttft, C.c_int64)
+        t.slo_tbt_us = _ptr(tbt, C.c_int64)
+        t.err_draw = _ptr(err, C.c_int32)
+        t.flip_draw = _ptr(flip, C.c_uint8)
+        lu = N.CoLuts()
+        lu.s_max = max(s_max, 1)
+        lu.swap_half_us, lu.recompute_us, lu.survive_swap_us, lu.survive_rec_us = (
+            _ptr(x, C.c_int64) for x in luts)
+        h = C.c_void_p()
+        N.check(lib.co_create(C.byref(c), C.byref(t), C.byref(lu), device, C.byref(h)), "co_create")
+        self._lib = lib
+        self._h = h
+        self._n = n
+        self._events: List[dict] = []
+        self._samples: List[Tuple[int, int]] = []
+        self._cache: Dict[str, np.ndarray] = {}
+        self._sc = None
+        self.report: Optional[MetricsReport] = None
+        self.pool = PoolView(self)
+
+    # -- lifecycle -----------------------------------------------------------
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._lib.co_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _dirty(self) -> None:
+        self._cache.clear()
+        self._sc = None
+
+    def _scalars(self) -> N.CoScalars:
+        if self._sc is None:
+            s = N.CoScalars()
+            N.check(self._lib.co_get_scalars(self._h, C.byref(s)), "co_get_scalars")
+            self._sc = s
+        return self._sc
+
+    def _field(self, name: str) -> np.ndarray:
+        a = self._cache.get(name)
+        if a is None:
+            a = np.empty(self._n, dtype=np.int64)
+            N.check(self._lib.co_read_field(self._h, N.FIELD[name], _ptr(a, C.c_int64)), "co_read_field")
+            self._cache[name] = a
+        return a
+
+    # -- the reference surface ----------------------------------------------
+
+    @property
+    def now_us(self) -> int:
+        return int(self._scalars().now_us)
+
+    def step(self) -> bool:
+        r = C.c_int32()
+        self._dirty()
+        N.check(self._lib.co_step(self._h, C.byref(r)), "co_step")
+        return bool(r.value)
+
+    def run_steps(self, max_steps: int = 0, steps_per_launch: Optional[int] = None) -> int:
+        """Device loop with the run() progress guard; returns step() calls."""
+        k = steps_per_launch or self.steps_per_launch
+        done = C.c_int64()
+        self._dirty()
+        N.check(self._lib.co_run(self._h, max_steps, k, C.byref(done)), "co_run")
+        return int(done.value)
+
+    def run(self) -> MetricsReport:
+        self.run_steps(0)
+        s = self._scalars()
+        makespan = max(0, int(s.now_us) - int(s.first_arrival_us))
+        self.report = compute_metrics(
+            requests=self.requests_view(), runtimes=self.runtimes, policy=self.cfg.sched.policy,
+            seed=self.cfg.seed, makespan_us=makespan, capacity_tokens=self.cfg.capacity_tokens,
+            samples=self.samples,
+        )
+        return self.report
+
+    def last_device_ms(self) -> float:
+        ms = C.c_double()
+        N.check(self._lib.co_last_device_ms(self._h, C.byref(ms)), "co_last_device_ms")
+        return float(ms.value)
+
+    def _preempt(self, rid: int, strategy: Strategy, now_us: int, cause: str = "plan") -> None:
+        """White-box hook matching engine.py:360-384."""
+        self._dirty()
+        N.check(self._lib.co_preempt(self._h, self._idx_of[rid], STRATEGY_CODE[strategy], now_us,
+                                     CAUSE_CODE[cause]), "co_preempt")
+
+    def check_invariants(self) -> None:
+        N.check(self._lib.co_check_invariants(self._h), "check_invariants")
+
+    # -- host views ------------------------------------------------------------
+
+    def _drain(self) -> None:
+        ne, nm = C.c_int64(), C.c_int64()
+        N.check(self._lib.co_pending_events(self._h, C.byref(ne), C.byref(nm)), "co_pending_events")
+        if ne.value:
+            evs = (N.CoEvent * ne.value)()
+            mem = np.empty(2 * max(nm.value, 1), dtype=np.int32)
+            got_e, got_m = C.c_int64(), C.c_int64()
+            N.check(self._lib.co_drain_events(self._h, evs, ne.value, _ptr(mem, C.c_int32), nm.value,
+                                              C.byref(got_e), C.byref(got_m)), "co_drain_events")
+            self._events.extend(self._convert(evs, got_e.value, mem))
+        s = self._scalars()
+        if s.n_samples:
+            buf = np.empty(2 * s.n_samples, dtype=np.int64)
+            got = C.c_int64()
+            N.check(self._lib.co_drain_samples(self._h, _ptr(buf, C.c_int64), s.n_samples, C.byref(got)),
+                    "co_drain_samples")
+            self._samples.extend(zip(buf[0:2 * got.value:2].tolist(), buf[1:2 * got.value:2].tolist()))
+        self._sc = None
+
+    def _convert(self, evs, n: int, mem: np.ndarray) -> Iterator[dict]:
+        rid = self._rid
+        for k in range(n):
+            e = evs[k]
+            kind = e.kind
+            if kind == N.EV_ARRIVE:
+                yield {"ev": "arrive", "t": e.t, "req": rid[e.idx]}
+            elif kind == N.EV_ITER:
+                m = mem[2 * e.c: 2 * (e.c + e.idx)].tolist()
+                yield {"ev": "iter", "t": e.t, "end": e.a, "tokens": e.b,
+                       "members": [[rid[m[j]], m[j + 1]] for j in range(0, len(m), 2)]}
+            elif kind == N.EV_ADMIT:
+                yield {"ev": "admit", "t": e.t, "req": rid[e.idx]}
+            elif kind == N.EV_PREEMPT:
+                yield {"ev": "preempt", "t": e.t, "req": rid[e.idx],
+                       "strategy": STRATEGY_FROM_CODE[e.b].value, "kv": e.a, "cause": N.CAUSES[e.c]}
+            elif kind == N.EV_READMIT:
+                yield {"ev": "readmit", "t": e.t, "req": rid[e.idx], "ready_at": e.a}
+            else:
+                yield {"ev": "complete", "t": e.t, "req": rid[e.idx]}
+
+    @property
+    def events(self) -> List[dict]:
+        self._drain()
+        return self._events
+
+    @property
+    def samples(self) -> List[Tuple[int, int]]:
+        self._drain()
+        return self._samples
+
+    def requests_view(self) -> Dict[int, Request]:
+        st = self._field("STATE")
+        for k, r in enumerate(self._rid):
+            self.requests[r].state = STATE_FROM_CODE[int(st[k])]
+        return self.requests
+
+    @property
+    def runtimes(self) -> Dict[int, RequestRuntime]:
+        self.requests_view()
+        f = self._field
+        cols = {name: f(name).tolist() for name in (
+            "GENERATED", "ALLOCATED_KVC", "USED", "FIRST_TOKEN", "LAST_TOKEN", "MAX_TBT",
+            "PREEMPTION_COUNT", "PREEMPTION_TIME", "KV_NEED", "PREFILL_DONE", "READY_AT",
+            "PREEMPT_STARTED", "SWAP_OUT_DONE", "LAST_STRATEGY", "FIRST_START", "COMPLETION",
+            "PREDICTED", "ESTIMATED", "STATE")}
+        offs = np.empty(self._n + 1, dtype=np.int64)
+        times = np.empty(max(1, int(self._tok_total())), dtype=np.int64)
+        N.check(self._lib.co_read_token_times(self._h, _ptr(offs, C.c_int64), _ptr(times, C.c_int64)),
+                "co_read_token_times")
+        w = self.cfg.predictor.bin_width
+        out = _Runtimes()
+        none = lambda v: None if v < 0 else v  # noqa: E731
+        for k, r in enumerate(self._rid):
+            g = cols["GENERATED"][k]
+            est = None
+            if cols["STATE"][k] != 0:
+                p, e = cols["PREDICTED"][k], cols["ESTIMATED"][k]
+                lo, hi = bin_of(p, w)
+                est = LengthEstimate(predicted_len=p, range_lo=lo, range_hi=hi,
+                                     direction=Direction.UNDER if self._under[k] else Direction.OVER,
+                                     confidence=self.confidence, padding=self.padding, estimated_len=e)
+            ls = cols["LAST_STRATEGY"][k]
+            out[r] = RequestRuntime(
+                generated=g, allocated_kvc=cols["ALLOCATED_KVC"][k], used_kvc=cols["USED"][k],
+                first_token_at_us=none(cols["FIRST_TOKEN"][k]), last_token_at_us=none(cols["LAST_TOKEN"][k]),
+                max_tbt_us=cols["MAX_TBT"][k], preemption_count=cols["PREEMPTION_COUNT"][k],
+                preemption_time_us=cols["PREEMPTION_TIME"][k], estimate=est, kv_need=cols["KV_NEED"][k],
+                prefill_done=cols["PREFILL_DONE"][k], ready_at_us=cols["READY_AT"][k],
+                preempt_started_us=cols["PREEMPT_STARTED"][k], swap_out_done_us=cols["SWAP_OUT_DONE"][k],
+                last_strategy=STRATEGY_FROM_CODE.get(ls), first_start_us=none(cols["FIRST_START"][k]),
+                completion_us=none(cols["COMPLETION"][k]),
+                token_times_us=times[offs[k]:offs[k] + g].tolist(),
+            )
+        # present in the caller's input order like the reference dicts
+        return {r: out[r] for r in self._input_order}
+
+    def _tok_total(self) -> int:
+        return int(sum(r.true_output_len for r in self.requests.values()))

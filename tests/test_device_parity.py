@@ -1,0 +1,63 @@
+"""Device engine vs the CPU oracle on seeded traces: event logs, per-request
+outcomes and pool totals must be bit-identical (integer decisions)."""
+import numpy as np
+import pytest
+
+from oracle.cacheopt_oracle import CacheOptOracle
+from tests.cases import build_product, case_params, config2, final_arrays
+
+pytestmark = pytest.mark.gpu
+
+
+def _compare(eng, orc, label):
+    ev_d, ev_o = eng.events, orc.events
+    if ev_d != ev_o:
+        for k, (a, b) in enumerate(zip(ev_d, ev_o)):
+            if a != b:
+                raise AssertionError(f"{label}: first event diff at {k}:\n dev {a}\n orc {b}")
+        raise AssertionError(f"{label}: event count {len(ev_d)} vs {len(ev_o)}")
+    fo = orc.final_state()
+    fd = final_arrays(eng)
+    for k, v in fd.items():
+        assert np.array_equal(np.asarray(v), np.asarray(fo[k])), f"{label}: field {k} differs"
+    s = eng._scalars()
+    assert s.footprint_tokens == orc.fp_sum and s.used_tokens == orc.used_sum
+    assert s.reserved_blocks_current == orc.rsv_cur
+    assert eng.samples == orc.samples
+
+
+@pytest.mark.parametrize("seed", list(range(0, 24)))
+def test_random_regimes_full_run(cuda_ok, seed):
+    from paper_2503_13773_b200 import Engine
+    reqs, cfg = build_product(case_params(seed))
+    eng = Engine(reqs, cfg)
+    eng.run_steps(0)
+    orc = CacheOptOracle(reqs, cfg)
+    orc.run()
+    _compare(eng, orc, f"seed {seed}")
+    eng.close()
+
+
+@pytest.mark.parametrize("seed", [3, 7])
+def test_step_api_matches_run(cuda_ok, seed):
+    from paper_2503_13773_b200 import Engine
+    reqs, cfg = build_product(case_params(seed))
+    eng = Engine(reqs, cfg)
+    n = 0
+    while eng.step():
+        n += 1
+        assert n < 200_000
+    orc = CacheOptOracle(reqs, cfg)
+    orc.run()
+    _compare(eng, orc, f"step seed {seed}")
+
+
+def test_config2_first_60_steps(cuda_ok):
+    from paper_2503_13773_b200 import Engine
+    reqs, cfg = config2(n=65_536)
+    eng = Engine(reqs, cfg)
+    eng.run_steps(60)
+    orc = CacheOptOracle(reqs, cfg)
+    for _ in range(60):
+        orc.step()
+    _compare(eng, orc, "config2")
