@@ -128,6 +128,7 @@ typedef struct co_scalars {
     int64_t record_seq;
     int64_t n_events;               /* undrained events on the device */
     int64_t n_samples;
+    int64_t decisions;              /* sum over steps of live requests (BASELINE.md unit) */
     int32_t reserved_blocks_current;/* kvc.py:79 */
     int32_t n_live;
     int32_t n_pending;
@@ -204,6 +205,15 @@ int co_check_invariants(co_engine* eng);
 int co_last_device_ms(co_engine* eng, double* ms);
 /* Number of kernels one device step launches (for gpu_launches accounting). */
 int co_kernels_per_step(co_engine* eng, int32_t* n);
+
+/* Benchmark helper: runs k engine steps (run() semantics) as one CUDA graph
+ * with CUDA events between the stages of every step, optionally preceded per
+ * step by an L2 flush (a memset of flush_bytes), and returns the device time
+ * of each step (step_ms[k], flush excluded) and the summed device time of
+ * each stage over the k steps (stage_ms[CO_NSTAGES]).  Stages: begin+admit,
+ * classify, sort, plan, apply, check. */
+#define CO_NSTAGES 6
+int co_time_steps(co_engine* eng, int32_t k, int64_t flush_bytes, double* step_ms, double* stage_ms);
 
 const char* co_last_error(void);
 const char* co_version(void);

@@ -13,6 +13,8 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libcacheopt.so"
 
 CO_OK, CO_EINVAL, CO_ECUDA, CO_EDEVICE = 0, 1, 2, 3
 MAX_SLO_EDGES = 8
+NSTAGES = 6
+STAGES = ("begin+admit", "classify", "sort", "plan", "apply", "check")
 
 EV_ARRIVE, EV_ADMIT, EV_ITER, EV_PREEMPT, EV_READMIT, EV_COMPLETE = range(6)
 CAUSES = ("plan", "squeeze", "collision")
@@ -60,6 +62,7 @@ class CoScalars(C.Structure):
         ("t_i_max_us", C.c_int64), ("footprint_tokens", C.c_int64), ("granted_tokens", C.c_int64),
         ("used_tokens", C.c_int64), ("generated_total", C.c_int64), ("iterations", C.c_int64),
         ("steps", C.c_int64), ("record_seq", C.c_int64), ("n_events", C.c_int64), ("n_samples", C.c_int64),
+        ("decisions", C.c_int64),
         ("reserved_blocks_current", C.c_int32), ("n_live", C.c_int32), ("n_pending", C.c_int32),
         ("done", C.c_int32), ("stalled", C.c_int32), ("last_step_result", C.c_int32), ("error", C.c_int32),
         ("_pad0", C.c_int32),
@@ -74,7 +77,8 @@ class CoEvent(C.Structure):
 EXPORTS = (
     "co_create", "co_destroy", "co_step", "co_run", "co_preempt", "co_get_scalars", "co_read_field",
     "co_drain_events", "co_pending_events", "co_drain_samples", "co_read_token_times",
-    "co_check_invariants", "co_last_device_ms", "co_kernels_per_step", "co_last_error", "co_version",
+    "co_check_invariants", "co_last_device_ms", "co_kernels_per_step", "co_time_steps", "co_last_error",
+    "co_version",
 )
 
 _lib = None
@@ -109,6 +113,7 @@ def load() -> C.CDLL:
         "co_check_invariants": (C.c_int, [V]),
         "co_last_device_ms": (C.c_int, [V, C.POINTER(C.c_double)]),
         "co_kernels_per_step": (C.c_int, [V, I32P]),
+        "co_time_steps": (C.c_int, [V, C.c_int32, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "co_last_error": (C.c_char_p, []),
         "co_version": (C.c_char_p, []),
     }

@@ -100,19 +100,27 @@ static int upload(co_engine* E, T* dst, const std::vector<T>& src) {
     return CO_OK;
 }
 
-static int launch_step(co_engine* E, int32_t guard) {
+// ev (optional): CO_NSTAGES + 1 events recorded at the stage boundaries
+static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
     Dev& d = E->d;
     cudaStream_t s = E->stream;
+    if (ev) cudaEventRecord(ev[0], s);
     k_begin<<<1, 32, 0, s>>>(d, guard);
     k_admit<<<E->grid, 256, 0, s>>>(d);
+    if (ev) cudaEventRecord(ev[1], s);
     k_classify<<<E->grid, 256, 0, s>>>(d);
+    if (ev) cudaEventRecord(ev[2], s);
     size_t bytes = E->cub_bytes;
     cudaError_t e = cub::DeviceRadixSort::SortPairs(E->cub_tmp, bytes, d.keys_in, d.keys_out, d.vals_in,
                                                     d.vals_out, (int)E->n, 0, 64, s);
     if (e != cudaSuccess) return fail(CO_ECUDA, std::string("radix sort: ") + cudaGetErrorString(e));
+    if (ev) cudaEventRecord(ev[3], s);
     k_plan<<<1, NT, 0, s>>>(d);
+    if (ev) cudaEventRecord(ev[4], s);
     k_apply<<<1, NT, 0, s>>>(d);
+    if (ev) cudaEventRecord(ev[5], s);
     k_check<<<1, NT, 0, s>>>(d, 0);
+    if (ev) cudaEventRecord(ev[6], s);
     return CO_OK;
 }
 
@@ -467,6 +475,7 @@ int co_get_scalars(co_engine* E, co_scalars* o) {
     o->footprint_tokens = c.fp_sum; o->granted_tokens = c.granted_sum; o->used_tokens = c.used_sum;
     o->generated_total = c.gen_total; o->iterations = c.iters; o->steps = c.steps; o->record_seq = c.seq;
     o->n_events = c.ev_count + (int64_t)E->st_events.size(); o->n_samples = c.sample_count + E->st_samples.size() / 2;
+    o->decisions = c.decisions;
     o->reserved_blocks_current = c.rsv_cur; o->n_live = c.n_live; o->n_pending = (int32_t)(E->n - c.next_pending);
     o->done = c.done; o->stalled = c.stalled; o->last_step_result = c.done ? 0 : c.last_result; o->error = c.error;
     return CO_OK;
@@ -577,6 +586,49 @@ int co_last_device_ms(co_engine* E, double* ms) {
     if (!E || !ms) return fail(CO_EINVAL, "null argument");
     *ms = E->last_ms;
     return CO_OK;
+}
+
+int co_time_steps(co_engine* E, int32_t k, int64_t flush_bytes, double* step_ms, double* stage_ms) {
+    if (!E || k < 1) return fail(CO_EINVAL, "bad arguments");
+    const int NE = CO_NSTAGES + 1;
+    std::vector<cudaEvent_t> evs((size_t)k * NE);
+    for (auto& e : evs) CK(cudaEventCreate(&e));
+    void* flush = nullptr;
+    if (flush_bytes > 0) CK(cudaMalloc(&flush, flush_bytes));
+    cudaGraph_t g;
+    cudaGraphExec_t ge = nullptr;
+    int r = CO_OK;
+    CK(cudaStreamBeginCapture(E->stream, cudaStreamCaptureModeThreadLocal));
+    for (int32_t j = 0; j < k && !r; j++) {
+        if (flush) cudaMemsetAsync(flush, j & 0xff, flush_bytes, E->stream);
+        r = launch_step(E, 1, evs.data() + (size_t)j * NE);
+    }
+    CK(cudaStreamEndCapture(E->stream, &g));
+    if (!r) {
+        CK(cudaGraphInstantiate(&ge, g, 0));
+        CK(cudaGraphLaunch(ge, E->stream));
+        CK(cudaStreamSynchronize(E->stream));
+        for (int q = 0; q < CO_NSTAGES; q++) stage_ms[q] = 0;
+        for (int32_t j = 0; j < k; j++) {
+            cudaEvent_t* e = evs.data() + (size_t)j * NE;
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e[0], e[NE - 1]);
+            step_ms[j] = ms;
+            for (int q = 0; q < CO_NSTAGES; q++) {
+                float x = 0;
+                cudaEventElapsedTime(&x, e[q], e[q + 1]);
+                stage_ms[q] += x;
+            }
+        }
+        cudaGraphExecDestroy(ge);
+    }
+    cudaGraphDestroy(g);
+    for (auto& e : evs) cudaEventDestroy(e);
+    if (flush) cudaFree(flush);
+    if (r) return r;
+    if ((r = sync_ctl(E))) return r;
+    if (E->h_ctl->paused) return fail(CO_EDEVICE, "append buffers filled during a timed run; drain first");
+    return check_device_error(E);
 }
 
 int co_kernels_per_step(co_engine* E, int32_t* n) {

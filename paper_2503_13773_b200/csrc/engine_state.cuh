@@ -20,7 +20,7 @@ enum ActKind : int32_t { A_ALLOCATE = 0, A_GROW = 1, A_RESERVE = 2, A_EMBED = 3 
 struct Ctl {
     int64_t now, horizon, first_arrival, t_i;
     int64_t fp_sum, granted_sum, used_sum;          // kvc.py:83-84, used_tokens kvc.py:109
-    int64_t gen_total, iters, steps, seq;
+    int64_t gen_total, iters, steps, seq, decisions;
     int64_t ev_count, mem_count, sample_count;      // undrained append-buffer fill
     int64_t mark[5];                                 // engine.py:647-650 progress mark
     int64_t streak;

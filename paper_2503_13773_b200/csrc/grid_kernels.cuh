@@ -65,6 +65,7 @@ __global__ void k_begin(Dev d, int32_t guard) {
     c.adm_hi = lo;
     c.next_pending = lo;
     c.n_live += adm;
+    c.decisions += c.n_live;  // one decision per live request per step
     if (d.record_events) c.ev_count += adm;  // arrive records written by k_admit
     c.active = 1;
 }
