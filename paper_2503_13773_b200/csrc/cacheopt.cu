@@ -101,26 +101,32 @@ static int upload(co_engine* E, T* dst, const std::vector<T>& src) {
 }
 
 // ev (optional): CO_NSTAGES + 1 events recorded at the stage boundaries
+static inline void mark(cudaEvent_t e, cudaStream_t s) {
+    // an external event node when captured into a graph (a plain record
+    // inside capture is only a dependency edge and cannot be timed)
+    cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+}
+
 static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
     Dev& d = E->d;
     cudaStream_t s = E->stream;
-    if (ev) cudaEventRecord(ev[0], s);
+    if (ev) mark(ev[0], s);
     k_begin<<<1, 32, 0, s>>>(d, guard);
     k_admit<<<E->grid, 256, 0, s>>>(d);
-    if (ev) cudaEventRecord(ev[1], s);
+    if (ev) mark(ev[1], s);
     k_classify<<<E->grid, 256, 0, s>>>(d);
-    if (ev) cudaEventRecord(ev[2], s);
+    if (ev) mark(ev[2], s);
     size_t bytes = E->cub_bytes;
     cudaError_t e = cub::DeviceRadixSort::SortPairs(E->cub_tmp, bytes, d.keys_in, d.keys_out, d.vals_in,
                                                     d.vals_out, (int)E->n, 0, 64, s);
     if (e != cudaSuccess) return fail(CO_ECUDA, std::string("radix sort: ") + cudaGetErrorString(e));
-    if (ev) cudaEventRecord(ev[3], s);
+    if (ev) mark(ev[3], s);
     k_plan<<<1, NT, 0, s>>>(d);
-    if (ev) cudaEventRecord(ev[4], s);
+    if (ev) mark(ev[4], s);
     k_apply<<<1, NT, 0, s>>>(d);
-    if (ev) cudaEventRecord(ev[5], s);
+    if (ev) mark(ev[5], s);
     k_check<<<1, NT, 0, s>>>(d, 0);
-    if (ev) cudaEventRecord(ev[6], s);
+    if (ev) mark(ev[6], s);
     return CO_OK;
 }
 
@@ -612,11 +618,11 @@ int co_time_steps(co_engine* E, int32_t k, int64_t flush_bytes, double* step_ms,
         for (int32_t j = 0; j < k; j++) {
             cudaEvent_t* e = evs.data() + (size_t)j * NE;
             float ms = 0;
-            cudaEventElapsedTime(&ms, e[0], e[NE - 1]);
+            CK(cudaEventElapsedTime(&ms, e[0], e[NE - 1]));
             step_ms[j] = ms;
             for (int q = 0; q < CO_NSTAGES; q++) {
                 float x = 0;
-                cudaEventElapsedTime(&x, e[q], e[q + 1]);
+                CK(cudaEventElapsedTime(&x, e[q], e[q + 1]));
                 stage_ms[q] += x;
             }
         }
