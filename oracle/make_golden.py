@@ -1,0 +1,129 @@
+"""Generates tests/golden/ from the UNMODIFIED reference simulator.
+
+Run in the development container (where /root/reference exists):
+
+    python oracle/make_golden.py
+
+For every scenario of tests/cases.py (and a config-2 window) it builds the
+trace and config with the reference's OWN classes (kvcsim.workload.generate,
+assign_slos, EngineConfig, ...), runs kvcsim.engine.Engine, and stores the
+trace columns, the config parameters, the full event log (gzip'd sorted-key
+JSONL, exactly write_events_jsonl's bytes) and per-request final outcomes.
+The oracle is pinned against these files by tests/test_oracle_golden.py; the
+device engine is checked against the oracle on the GPU.
+"""
+from __future__ import annotations
+
+import copy
+import gzip
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "tests", "golden")
+sys.path.insert(0, ROOT)
+
+SEEDS = [0, 1, 2, 5, 9, 13, 21, 34]
+
+
+def ref_build(params):
+    sys.path.insert(0, REF)
+    from kvcsim.costmodel import TruthCosts
+    from kvcsim.engine import EngineConfig
+    from kvcsim.estimation import PredictorConfig
+    from kvcsim.preemption import RecomputeModel, SwapModel
+    from kvcsim.scheduler import SchedulerConfig
+    from kvcsim.workload import PRESETS, SloPolicy, TraceSpec, assign_slos, generate
+    t = params["trace"]
+    if t["kind"] == "preset":
+        spec = PRESETS[t["preset"]].sized(t["num_requests"], t["arrival_rate"])
+    else:
+        spec = TraceSpec(**{k: v for k, v in t.items() if k != "kind"})
+    seed = params["seed"]
+    reqs = generate(spec, seed)
+    assign_slos(reqs, params["slo"][0], params["slo"][1], SloPolicy(), seed)
+    tr = params["truth"]
+    truth = TruthCosts.default() if tr is None else TruthCosts(
+        swap_true=SwapModel(tr["gamma_s"], tr["delta_s"]),
+        recompute_true=RecomputeModel(tr["alpha_r"], tr["beta_r"], tr["kappa_r"], tr["eps_r"]))
+    cfg = EngineConfig(capacity_tokens=params["capacity"], reserved_blocks=params["reserved"],
+                       sched=SchedulerConfig(policy="cacheopt", **params["sched"]),
+                       predictor=PredictorConfig(**params["pred"]), truth=truth, seed=seed,
+                       fixed_confidence=params["fixed_confidence"],
+                       validate_every=params["validate_every"])
+    return reqs, cfg
+
+
+def jsonl_bytes(events) -> bytes:
+    return "".join(json.dumps(e, sort_keys=True, separators=(",", ":")) + "\n" for e in events).encode()
+
+
+TRACE_COLS = ("id", "arrival_us", "prompt_len", "true_output_len", "slo_ttft_us", "slo_tbt_us")
+
+
+def trace_digest(cols) -> str:
+    h = hashlib.sha256()
+    for k in TRACE_COLS:
+        h.update(np.asarray(cols[k], dtype=np.int64).tobytes())
+    return h.hexdigest()
+
+
+def run_and_store(name, params, reqs, cfg, steps=None, keep_events=True, store_trace=True):
+    from kvcsim.engine import Engine
+    trace = {k: [getattr(r, k) for r in reqs] for k in TRACE_COLS}
+    digest = trace_digest(trace)
+    if not store_trace:
+        trace = None
+    eng = Engine(copy.deepcopy(reqs), cfg)
+    if steps is None:
+        eng.run()
+    else:
+        for _ in range(steps):
+            eng.step()
+    blob = jsonl_bytes(eng.events)
+    order = sorted(range(len(reqs)), key=lambda k: (reqs[k].arrival_us, reqs[k].id))
+    final = {}
+    for f in ("generated", "preemption_count", "preemption_time_us", "max_tbt_us", "kv_need", "prefill_done"):
+        final[f] = [getattr(eng.runtimes[reqs[k].id], f) for k in order]
+    final["used"] = [eng.runtimes[reqs[k].id].used_kvc for k in order]
+    final["completion_us"] = [eng.runtimes[reqs[k].id].completion_us or -1 for k in order]
+    final["first_token_at_us"] = [
+        -1 if eng.runtimes[reqs[k].id].first_token_at_us is None else eng.runtimes[reqs[k].id].first_token_at_us
+        for k in order]
+    doc = {"name": name, "params": params, "steps": steps, "trace": trace, "trace_sha256": digest,
+           "events_sha256": hashlib.sha256(blob).hexdigest(), "n_events": len(eng.events),
+           "final": final, "pool": {"footprint": eng.pool.footprint_tokens, "used": eng.pool.used_tokens,
+                                    "reserved": eng.pool.reserved_blocks_current},
+           "samples_sha256": hashlib.sha256(json.dumps(eng._samples).encode()).hexdigest()}
+    os.makedirs(OUT, exist_ok=True)
+    with gzip.open(os.path.join(OUT, name + ".json.gz"), "wt") as fh:
+        json.dump(doc, fh)
+    if keep_events:
+        with gzip.open(os.path.join(OUT, name + ".events.jsonl.gz"), "wb") as fh:
+            fh.write(blob)
+    print(f"{name}: {len(eng.events)} events sha={doc['events_sha256'][:12]}")
+
+
+def main():
+    sys.path.insert(0, REF)
+    from tests.cases import case_params
+    for s in SEEDS:
+        p = case_params(s)
+        reqs, cfg = ref_build(p)
+        run_and_store(f"case{s:02d}", p, reqs, cfg)
+    # config 2 window: 65,536 requests, first 60 steps (digest + final state only)
+    p = {"seed": 0, "trace": {"kind": "preset", "preset": "sharegpt", "num_requests": 65536,
+                               "arrival_rate": 1e6},
+         "slo": [2_000_000, 200_000], "capacity": 166_400, "reserved": 8, "truth": None, "pred": {},
+         "sched": {"small_block_b": 16}, "fixed_confidence": None, "validate_every": 0}
+    reqs, cfg = ref_build(p)
+    run_and_store("config2_60", p, reqs, cfg, steps=60, keep_events=False, store_trace=False)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,28 @@
+"""When the reference is present (development container), run it side by
+side with the oracle on more randomised regimes than the fixtures hold."""
+import copy
+import sys
+
+import pytest
+
+from tests.conftest import REFERENCE_SRC, has_reference
+
+pytestmark = [pytest.mark.reference,
+              pytest.mark.skipif(not has_reference(), reason="reference not mounted")]
+
+
+@pytest.mark.parametrize("seed", [40, 41, 42, 43, 44, 45])
+def test_oracle_matches_live_reference(seed):
+    sys.path.insert(0, REFERENCE_SRC)
+    from kvcsim.engine import Engine
+    from oracle.cacheopt_oracle import CacheOptOracle
+    from oracle.make_golden import ref_build
+    from tests.cases import case_params
+    reqs, cfg = ref_build(case_params(seed))
+    eng = Engine(copy.deepcopy(reqs), cfg)
+    eng.run()
+    orc = CacheOptOracle(reqs, cfg)   # the oracle accepts the reference's own config objects
+    orc.run()
+    assert orc.events == eng.events
+    for k, rid in enumerate(orc.rid):
+        assert orc.token_times[k] == eng.runtimes[rid].token_times_us
