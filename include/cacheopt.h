@@ -196,6 +196,11 @@ int co_drain_samples(co_engine* eng, int64_t* out /* 2 per sample */, int64_t ma
 /* token timestamps: offsets[n+1] and the Σ true_output_len slab; callers
  * use generated[i] to know how many entries of request i are valid. */
 int co_read_token_times(co_engine* eng, int64_t* offsets, int64_t* times);
+/* N1 physical block tables (no reference counterpart):
+ * lens[n] pages per request (sorted order), their page ids concatenated in
+ * request order into pages[], and the free stack bottom..top. */
+int co_read_block_tables(co_engine* eng, int32_t* lens, int32_t* pages, int64_t max_pages,
+                         int32_t* free_pages, int32_t* n_free);
 /* kvc.py:336-375 BlockPool.check_invariants on the device; CO_EDEVICE on
  * a violation with the reason in co_last_error(). */
 int co_check_invariants(co_engine* eng);

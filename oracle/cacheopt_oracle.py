@@ -216,6 +216,11 @@ class CacheOptOracle:
         self.rsv = np.zeros(n, dtype=I64)
         self.rec_seq = np.zeros(n, dtype=I64)
         self.guests: Dict[int, List[int]] = {}
+        # N1 block tables (defined by this framework):
+        # LIFO free stack of page ids, popped 0, 1, 2, ... initially
+        self.n_pages = self.capacity // self.bs
+        self.free_pages: List[int] = list(range(self.n_pages - 1, -1, -1))
+        self.tables: Dict[int, List[int]] = {}
         self.seq = 0
         self.fp_sum = 0
         self.granted_sum = 0
@@ -256,6 +261,15 @@ class CacheOptOracle:
     def free_tokens(self):
         """kvc.py:92-98."""
         return self.capacity - self.rsv_cur * self.bs - self.fp_sum
+
+    def _pop_pages(self, i, k):
+        tab = self.tables.setdefault(i, [])
+        for _ in range(k):
+            tab.append(self.free_pages.pop())
+
+    def _push_pages(self, i):
+        for pg in reversed(self.tables.pop(i, [])):
+            self.free_pages.append(pg)
 
     def _new_record(self, i, granted, host=-1, off=0):
         self.holds[i] = True
@@ -301,6 +315,7 @@ class CacheOptOracle:
         self._new_record(i, n)
         self.fp_sum += fp
         self.granted_sum += n
+        self._pop_pages(i, fp // self.bs)
         return True
 
     def find_host(self, triples, prompt, out):
@@ -356,8 +371,10 @@ class CacheOptOracle:
         g = int(self.granted[i])
         old = self._fp(g) if g else 0
         self.granted[i] = g + tokens
-        self.fp_sum += self._fp(g + tokens) - old
+        dfp = self._fp(g + tokens) - old
+        self.fp_sum += dfp
         self.granted_sum += tokens
+        self._pop_pages(i, dfp // self.bs)
         return True
 
     def pool_grow(self, i, n):
@@ -373,6 +390,7 @@ class CacheOptOracle:
             self.granted[i] = g + n
             self.fp_sum += delta
             self.granted_sum += n
+            self._pop_pages(i, delta // self.bs)
             return True
         floor = int(self.used[h]) + self.buffer_b
         for gid in self.guests.get(h, ()):
@@ -397,6 +415,7 @@ class CacheOptOracle:
         self.host[i] = -1
         self.off[i] = 0
         self.fp_sum += fp
+        self._pop_pages(i, fp // self.bs)
         return True
 
     def pool_release(self, i):
@@ -412,10 +431,13 @@ class CacheOptOracle:
             self.host[i] = -1
             self._drop_record(i)
             return
+        self._push_pages(i)
         for gid in self.guests.get(i, ()):
             self.host[gid] = -1
             self.off[gid] = 0
-            self.fp_sum += self._fp(int(self.granted[gid]))
+            gfp = self._fp(int(self.granted[gid]))
+            self.fp_sum += gfp
+            self._pop_pages(gid, gfp // self.bs)
         self.fp_sum -= self._fp(int(self.granted[i]))
         self.granted_sum -= int(self.granted[i])
         refill = min(int(self.rsv[i]), self.rsv_target - self.rsv_cur)
@@ -429,6 +451,10 @@ class CacheOptOracle:
         self.used_sum += u - int(self.used[i])
         self.used[i] = u
 
+    def block_tables(self):
+        """N1 state: ({req_id: pages}, free stack bottom..top)."""
+        return ({self.rid[i]: list(t) for i, t in sorted(self.tables.items()) if t}, list(self.free_pages))
+
     def check_invariants(self):
         """kvc.py:336-375."""
         owners = np.nonzero(self.holds)[0]
@@ -439,6 +465,20 @@ class CacheOptOracle:
             raise ValueError("free tokens negative")
         if not 0 <= self.rsv_cur <= self.rsv_target:
             raise ValueError("reserve out of range")
+        # N1: standalone records own exactly fp(granted)/bs distinct pages
+        seen = set(self.free_pages)
+        if len(seen) != len(self.free_pages):
+            raise ValueError("duplicate free page")
+        for i, t in self.tables.items():
+            want = self._fp(int(self.granted[i])) // self.bs if (self.holds[i] and self.host[i] < 0) else 0
+            if len(t) != want:
+                raise ValueError(f"table of {self.rid[i]} has {len(t)} pages, footprint needs {want}")
+            for pg in t:
+                if pg in seen:
+                    raise ValueError("page owned twice")
+                seen.add(pg)
+        if len(seen) != self.n_pages or self.fp_sum // self.bs != self.n_pages - len(self.free_pages):
+            raise ValueError("page conservation")
         for i in owners:
             if self.used[i] > self.granted[i]:
                 raise ValueError("used exceeds granted")

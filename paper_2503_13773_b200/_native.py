@@ -78,7 +78,7 @@ EXPORTS = (
     "co_create", "co_destroy", "co_step", "co_run", "co_preempt", "co_get_scalars", "co_read_field",
     "co_drain_events", "co_pending_events", "co_drain_samples", "co_read_token_times",
     "co_check_invariants", "co_last_device_ms", "co_kernels_per_step", "co_time_steps", "co_last_error",
-    "co_version",
+    "co_version", "co_read_block_tables",
 )
 
 _lib = None
@@ -114,6 +114,7 @@ def load() -> C.CDLL:
         "co_last_device_ms": (C.c_int, [V, C.POINTER(C.c_double)]),
         "co_kernels_per_step": (C.c_int, [V, I32P]),
         "co_time_steps": (C.c_int, [V, C.c_int32, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+        "co_read_block_tables": (C.c_int, [V, I32P, I32P, C.c_int64, I32P, I32P]),
         "co_last_error": (C.c_char_p, []),
         "co_version": (C.c_char_p, []),
     }

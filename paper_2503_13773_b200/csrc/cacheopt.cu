@@ -71,6 +71,7 @@ struct co_engine {
     int64_t tok_total = 0;
     std::vector<int64_t> perm;         // sorted position -> caller position
     std::vector<int64_t> tok_off_host;
+    int64_t n_chunks = 0;
     std::vector<co_event> st_events;   // host staging of drained device events
     std::vector<int32_t> st_members;
     std::vector<int64_t> st_samples;
@@ -250,6 +251,9 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
         max_s = std::max<int64_t>(max_s, (int64_t)prompt[k] + tout[k]);
     }
     if (lu->s_max < max_s) return fail(CO_EINVAL, "LUTs do not cover max(prompt_len + true_output_len)");
+    const int32_t n_pages = (int32_t)(cfg->capacity_tokens / cfg->block_size);
+    const int32_t dir_w = (n_pages + TCHUNK - 1) / TCHUNK + 1;
+    const int64_t n_chunks = (int64_t)n_pages / TCHUNK + n + 2;
     int64_t first = n ? arr[0] : 0, horizon = 0;
     if (n) {
         int64_t span = arr[n - 1] - first;
@@ -317,6 +321,11 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     AL(d.tok_times, E->tok_total);
     AL(d.holds, n); AL(d.granted, n); AL(d.host, n); AL(d.off, n); AL(d.rsv, n); AL(d.guest, n); AL(d.rec_seq, n);
     AL(d.claim_w, n); AL(d.claim_ep, n); AL(d.epoch, n);
+    AL(d.chunk_pool, n_chunks * TCHUNK); AL(d.chunk_stack, n_chunks); AL(d.dir, (int64_t)n * dir_w);
+    AL(d.tab_len, n); AL(d.free_stack, n_pages);
+    d.n_pages = n_pages;
+    d.dir_w = dir_w;
+    E->n_chunks = n_chunks;
     AL(d.st_nr, n); AL(d.st_crit, n); AL(d.st_removed, n); AL(d.st_embedded, n); AL(d.st_resumed, n);
     AL(d.st_stalled, n); AL(d.st_parts, n); AL(d.st_claimed, n); AL(d.st_failed, n); AL(d.st_seen, n);
     AL(d.st_acted, n); AL(d.st_deferred, n);
@@ -362,11 +371,22 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     for (int64_t* p : {d.max_tbt, d.ready_at, d.pstart, d.swap_done, d.ptime, d.rec_seq}) memset_all(p, 0, n8);
     for (int64_t* p : {d.first_tok, d.last_tok, d.first_start, d.completion}) memset_all(p, 0xff, n8);
     memset_all(d.holds, 0, n);
+    memset_all(d.tab_len, 0, n4);
+    {
+        std::vector<int32_t> fs(n_pages);
+        for (int32_t k = 0; k < n_pages; k++) fs[k] = n_pages - 1 - k;  // pop order 0, 1, 2, ...
+        if ((r = upload(E, d.free_stack, fs))) { co_destroy(E); return r; }
+        std::vector<int32_t> cs(n_chunks);
+        for (int64_t k = 0; k < n_chunks; k++) cs[k] = (int32_t)(n_chunks - 1 - k);
+        if ((r = upload(E, d.chunk_stack, cs))) { co_destroy(E); return r; }
+    }
     memset_all(d.plan, 0, sizeof(PlanHdr));
     Ctl c0;
     std::memset(&c0, 0, sizeof(c0));
     c0.now = first; c0.horizon = horizon; c0.first_arrival = first; c0.t_i = cfg->t_i_init_us;
     c0.rsv_cur = cfg->reserved_blocks;
+    c0.free_top = n_pages;
+    c0.chunk_top = (int32_t)n_chunks;
     *E->h_ctl = c0;
     if (cudaMemcpyAsync(d.ctl, E->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, E->stream) != cudaSuccess) {
         co_destroy(E);
@@ -635,6 +655,35 @@ int co_time_steps(co_engine* E, int32_t k, int64_t flush_bytes, double* step_ms,
     if ((r = sync_ctl(E))) return r;
     if (E->h_ctl->paused) return fail(CO_EDEVICE, "append buffers filled during a timed run; drain first");
     return check_device_error(E);
+}
+
+int co_read_block_tables(co_engine* E, int32_t* lens, int32_t* pages, int64_t max_pages, int32_t* free_pages,
+                         int32_t* n_free) {
+    if (!E || !lens || !n_free) return fail(CO_EINVAL, "null argument");
+    int r = sync_ctl(E);
+    if (r) return r;
+    const int64_t n = E->n;
+    const int32_t W = E->d.dir_w;
+    std::vector<int32_t> dir((size_t)n * W), pool((size_t)E->n_chunks * TCHUNK);
+    if (n) {
+        CK(cudaMemcpyAsync(lens, E->d.tab_len, n * sizeof(int32_t), cudaMemcpyDeviceToHost, E->stream));
+        CK(cudaMemcpyAsync(dir.data(), E->d.dir, dir.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, E->stream));
+    }
+    CK(cudaMemcpyAsync(pool.data(), E->d.chunk_pool, pool.size() * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                       E->stream));
+    const int32_t nf = E->h_ctl->free_top;
+    if (free_pages && nf)
+        CK(cudaMemcpyAsync(free_pages, E->d.free_stack, nf * sizeof(int32_t), cudaMemcpyDeviceToHost, E->stream));
+    CK(cudaStreamSynchronize(E->stream));
+    *n_free = nf;
+    int64_t w = 0;
+    for (int64_t i = 0; i < n; i++) {
+        if (w + lens[i] > max_pages) return fail(CO_EINVAL, "page buffer too small");
+        for (int32_t k = 0; k < lens[i]; k++)
+            if (pages) pages[w + k] = pool[(size_t)dir[(size_t)i * W + k / TCHUNK] * TCHUNK + k % TCHUNK];
+        w += lens[i];
+    }
+    return CO_OK;
 }
 
 int co_kernels_per_step(co_engine* E, int32_t* n) {

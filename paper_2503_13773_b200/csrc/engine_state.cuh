@@ -10,7 +10,8 @@
 
 namespace co {
 
-constexpr int NT = 1024;           // threads of the single-CTA planner / apply kernels
+constexpr int NT = 1024;
+constexpr int TCHUNK = 64;        // pages per block-table chunk           // threads of the single-CTA planner / apply kernels
 constexpr int ST_PENDING = CO_PENDING, ST_WAITING = CO_WAITING, ST_RUNNING = CO_RUNNING,
               ST_PREEMPTED = CO_PREEMPTED, ST_COMPLETED = CO_COMPLETED;
 
@@ -32,6 +33,8 @@ struct Ctl {
     int32_t cnt_nw, cnt_nwp, cnt_run;                 // classify counts
     int32_t sid;                                      // stamp id of the current step
     int32_t check_due;
+    int32_t free_top;                                 // N1: pages on the free stack
+    int32_t chunk_top;                                // N1: free table chunks
     int32_t err_info[4];
 };
 
@@ -65,6 +68,18 @@ struct Dev {
     uint8_t* holds;
     int32_t *granted, *host, *off, *rsv, *guest;
     int64_t* rec_seq;
+    // N1 physical block tables (standalone records only; a guest is a view
+    // into its host's pages).  Request i's k-th page is
+    //   chunk_pool[dir[i * dir_w + k / TCHUNK] * TCHUNK + k % TCHUNK]
+    // with 64-page chunks drawn from a shared chunk stack, because a grant
+    // can be as large as the whole supply (scheduler.py:237 shares are not
+    // capped by the demand).
+    int32_t* chunk_pool;
+    int32_t* chunk_stack;
+    int32_t* dir;
+    int32_t* tab_len;
+    int32_t* free_stack;
+    int32_t n_pages, dir_w;
     // claims provider -> waiter (engine.py:246) with lazy invalidation epochs
     int32_t *claim_w, *claim_ep, *epoch;
     // per-step membership stamps (compared with Ctl::sid, never cleared)
@@ -96,6 +111,10 @@ struct Dev {
 // ---------------------------------------------------------------------------
 // per-request view quantities (engine.py:284-317, scheduler.py:99-118);
 // valid while the pool is not mutated (planning phase) or at the instant read
+
+__device__ __forceinline__ int32_t page_of(const Dev& d, int i, int32_t k) {
+    return d.chunk_pool[(int64_t)d.dir[(int64_t)i * d.dir_w + k / TCHUNK] * TCHUNK + k % TCHUNK];
+}
 
 __device__ __forceinline__ int64_t fp_tokens(int64_t t, int bs) { return ((t + bs - 1) / bs) * bs; }
 

@@ -10,6 +10,42 @@
 
 namespace co {
 
+// -- N1 block tables ----------------------------------------------------------
+// Pages 0..P-1 (P = capacity // block_size) live on a LIFO free stack; the
+// pool pops exactly Delta(footprint)/block_size pages whenever a standalone
+// record's footprint grows and pushes a record's pages back in reverse table
+// order when it is released, so sum(tab_len) == footprint_sum / block_size.
+__device__ __forceinline__ void pop_pages(const Dev& d, int i, int64_t k) {
+    Ctl& c = *d.ctl;
+    if (k <= 0) return;
+    int32_t len = d.tab_len[i];
+    if (k > c.free_top || (len + k + TCHUNK - 1) / TCHUNK > d.dir_w) {
+        c.error = 5; c.err_info[0] = i; c.err_info[1] = (int32_t)k;
+        return;
+    }
+    int32_t* dir = d.dir + (int64_t)i * d.dir_w;
+    const int32_t top = c.free_top;
+    for (int64_t j = 0; j < k; j++, len++) {
+        if (len % TCHUNK == 0) dir[len / TCHUNK] = d.chunk_stack[--c.chunk_top];
+        d.chunk_pool[(int64_t)dir[len / TCHUNK] * TCHUNK + len % TCHUNK] = d.free_stack[top - 1 - j];
+    }
+    c.free_top = top - (int32_t)k;
+    d.tab_len[i] = len;
+}
+__device__ __forceinline__ void push_table(const Dev& d, int i) {
+    Ctl& c = *d.ctl;
+    const int32_t len = d.tab_len[i];
+    const int32_t* dir = d.dir + (int64_t)i * d.dir_w;
+    const int32_t top = c.free_top;
+    for (int32_t j = 0; j < len; j++) {
+        int32_t k = len - 1 - j;
+        d.free_stack[top + j] = d.chunk_pool[(int64_t)dir[k / TCHUNK] * TCHUNK + k % TCHUNK];
+        if (k % TCHUNK == 0) d.chunk_stack[c.chunk_top++] = dir[k / TCHUNK];
+    }
+    c.free_top = top + len;
+    d.tab_len[i] = 0;
+}
+
 __device__ __forceinline__ void new_record(const Dev& d, int i, int32_t granted, int32_t host, int32_t off) {
     d.holds[i] = 1;
     d.granted[i] = granted;
@@ -32,6 +68,7 @@ __device__ bool pool_allocate(const Dev& d, int i, int64_t n) {
     new_record(d, i, (int32_t)n, -1, 0);
     d.ctl->fp_sum += fp;
     d.ctl->granted_sum += n;
+    pop_pages(d, i, fp / d.bs);
     return true;
 }
 
@@ -59,8 +96,10 @@ __device__ bool pool_draw_reserved(const Dev& d, int i, int32_t nb) {
     int64_t g = d.granted[i];
     int64_t old = g ? fp_tokens(g, d.bs) : 0;
     d.granted[i] = (int32_t)(g + tokens);
-    c.fp_sum += fp_tokens(g + tokens, d.bs) - old;
+    const int64_t dfp = fp_tokens(g + tokens, d.bs) - old;
+    c.fp_sum += dfp;
     c.granted_sum += tokens;
+    pop_pages(d, i, dfp / d.bs);
     return true;
 }
 
@@ -76,6 +115,7 @@ __device__ bool pool_grow(const Dev& d, int i, int64_t n) {
         d.granted[i] = (int32_t)(g + n);
         c.fp_sum += delta;
         c.granted_sum += n;
+        pop_pages(d, i, delta / d.bs);
         return true;
     }
     // guests grow downward to the host's used region plus the buffer; with
@@ -97,6 +137,7 @@ __device__ bool pool_promote(const Dev& d, int i) {
     d.host[i] = -1;
     d.off[i] = 0;
     d.ctl->fp_sum += fp;
+    pop_pages(d, i, fp / d.bs);
     return true;
 }
 
@@ -112,11 +153,14 @@ __device__ void pool_release(const Dev& d, int i) {
         return;
     }
     int32_t g = d.guest[i];
-    if (g >= 0) {  // the guest is re-homed in place (kvc.py:311-317)
+    push_table(d, i);
+    if (g >= 0) {  // the guest is re-homed (kvc.py:311-317) into pages of its own
         d.host[g] = -1;
         d.off[g] = 0;
-        c.fp_sum += fp_tokens(d.granted[g], d.bs);
+        const int64_t gfp = fp_tokens(d.granted[g], d.bs);
+        c.fp_sum += gfp;
         d.guest[i] = -1;
+        pop_pages(d, g, gfp / d.bs);
     }
     c.fp_sum -= fp_tokens(d.granted[i], d.bs);
     c.granted_sum -= d.granted[i];

@@ -384,6 +384,22 @@ class Engine:
         N.check(self._lib.co_preempt(self._h, self._idx_of[rid], STRATEGY_CODE[strategy], now_us,
                                      CAUSE_CODE[cause]), "co_preempt")
 
+    def block_tables(self):
+        """N1 readback: ({req_id: [page ids]}, free stack bottom..top)."""
+        lens = np.empty(max(self._n, 1), dtype=np.int32)
+        npg = self.cfg.capacity_tokens // self.cfg.sched.small_block_b
+        pages = np.empty(max(npg, 1), dtype=np.int32)
+        free = np.empty(max(npg, 1), dtype=np.int32)
+        nf = C.c_int32()
+        N.check(self._lib.co_read_block_tables(self._h, _ptr(lens, C.c_int32), _ptr(pages, C.c_int32), npg,
+                                               _ptr(free, C.c_int32), C.byref(nf)), "co_read_block_tables")
+        out, w = {}, 0
+        for k in range(self._n):
+            if lens[k]:
+                out[self._rid[k]] = pages[w:w + lens[k]].tolist()
+                w += int(lens[k])
+        return out, free[:nf.value].tolist()
+
     def check_invariants(self) -> None:
         N.check(self._lib.co_check_invariants(self._h), "check_invariants")
 

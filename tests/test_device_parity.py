@@ -24,6 +24,8 @@ def _compare(eng, orc, label):
     assert s.footprint_tokens == orc.fp_sum and s.used_tokens == orc.used_sum
     assert s.reserved_blocks_current == orc.rsv_cur
     assert eng.samples == orc.samples
+    # N1: identical physical block tables and free stack
+    assert eng.block_tables() == orc.block_tables(), f"{label}: block tables differ"
 
 
 @pytest.mark.parametrize("seed", list(range(0, 24)))

@@ -54,3 +54,20 @@ def test_fixture_set_covers_the_decision_kinds():
             kinds.add(e["ev"] if e["ev"] != "preempt" else f"preempt/{e['cause']}/{e['strategy']}")
     for k in ("arrive", "admit", "iter", "complete", "readmit", "preempt/plan/recompute", "preempt/plan/swap"):
         assert k in kinds, k
+
+
+@pytest.mark.parametrize("name", [n for n in CASES if n.startswith("case")][:5])
+def test_block_tables_conserve_pages_every_step(name):
+    """N1 restatement invariants (no reference counterpart): every standalone
+    record owns exactly fp(granted)/bs distinct pages, every page is owned
+    once or free, checked after every step of a golden scenario."""
+    doc = G.load(name)
+    reqs, cfg = G.requests_from(doc)
+    orc = CacheOptOracle(reqs, cfg)
+    while orc.step():
+        orc.check_invariants()
+    orc.check_invariants()
+    tabs, free = orc.block_tables()
+    standalone = {orc.rid[i] for i in range(orc.n) if orc.holds[i] and orc.host[i] < 0 and orc.granted[i] > 0}
+    assert set(tabs) == standalone
+    assert sorted(free + [p for t in tabs.values() for p in t]) == list(range(orc.n_pages))
