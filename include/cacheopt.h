@@ -83,6 +83,15 @@ typedef struct co_config {
     int32_t _pad0;
     int64_t s_star;                 /* scheduler.py:381-393 sweet spot */
     int64_t t_i_init_us;            /* engine.py:268-270 */
+    /* N2/N3 KV data plane (no reference counterpart; 0 layers = off).
+     * Page layout [layer][K|V][kv_head][slot][head_dim] bf16. */
+    int32_t kv_layers;
+    int32_t kv_heads;
+    int32_t q_heads;                /* multiple of kv_heads, <= 16 per kv head */
+    int32_t head_dim;               /* must be 128 */
+    int64_t host_swap_pages;        /* pinned host swap pool, in pages */
+    int32_t decode;                 /* run the paged decode for each step's decode members */
+    int32_t decode_split;           /* tokens per split-KV work item */
 } co_config;
 
 /* One trace, any order (the library sorts by (arrival_us, id) like
@@ -201,6 +210,19 @@ int co_read_token_times(co_engine* eng, int64_t* offsets, int64_t* times);
  * request order into pages[], and the free stack bottom..top. */
 int co_read_block_tables(co_engine* eng, int32_t* lens, int32_t* pages, int64_t max_pages,
                          int32_t* free_pages, int32_t* n_free);
+/* N2/N3 data plane readbacks (CO_EINVAL when the data plane is off):
+ * stats[8] = {swap-out bytes, swap-in bytes, fill bytes, move bytes,
+ *             decode steps, decode member-steps, decode context tokens, 0} */
+int co_data_stats(co_engine* eng, int64_t* stats);
+/* counts KV elements of every holder's tokens [0, used) that differ from the
+ * synthetic content (0 = the data path never lost or misplaced a byte) */
+int co_kv_verify(co_engine* eng, int64_t* mismatches, int64_t* checked);
+/* the last step's paged-decode outputs: member indices (sorted order),
+ * context lengths, and out[member][layer][q_head][head_dim] fp32 */
+int co_read_decode(co_engine* eng, int32_t* members, int32_t* ctx, float* out, int64_t max_members,
+                   int64_t* n_members, int64_t* step_id);
+/* pinned-memory cudaMemcpyAsync bandwidth of this GPU's host link (GB/s) */
+int co_host_link_gbs(int64_t bytes, double* d2h, double* h2d);
 /* kvc.py:336-375 BlockPool.check_invariants on the device; CO_EDEVICE on
  * a violation with the reason in co_last_error(). */
 int co_check_invariants(co_engine* eng);
@@ -216,8 +238,8 @@ int co_kernels_per_step(co_engine* eng, int32_t* n);
  * step by an L2 flush (a memset of flush_bytes), and returns the device time
  * of each step (step_ms[k], flush excluded) and the summed device time of
  * each stage over the k steps (stage_ms[CO_NSTAGES]).  Stages: begin+admit,
- * classify, sort, plan, apply, check. */
-#define CO_NSTAGES 6
+ * classify, sort, plan, apply, check, data (N2 moves + KV fills), decode (N3). */
+#define CO_NSTAGES 8
 int co_time_steps(co_engine* eng, int32_t k, int64_t flush_bytes, double* step_ms, double* stage_ms);
 
 const char* co_last_error(void);

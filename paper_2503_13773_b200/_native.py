@@ -13,8 +13,8 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libcacheopt.so"
 
 CO_OK, CO_EINVAL, CO_ECUDA, CO_EDEVICE = 0, 1, 2, 3
 MAX_SLO_EDGES = 8
-NSTAGES = 6
-STAGES = ("begin+admit", "classify", "sort", "plan", "apply", "check")
+NSTAGES = 8
+STAGES = ("begin+admit", "classify", "sort", "plan", "apply", "check", "data", "decode")
 
 EV_ARRIVE, EV_ADMIT, EV_ITER, EV_PREEMPT, EV_READMIT, EV_COMPLETE = range(6)
 CAUSES = ("plan", "squeeze", "collision")
@@ -39,7 +39,8 @@ class CoConfig(C.Structure):
         ("slo_edges_us", C.c_int64 * MAX_SLO_EDGES), ("iter_base_ms", C.c_double),
         ("iter_per_token_ms", C.c_double), ("horizon_factor", C.c_int64), ("validate_every", C.c_int32),
         ("record_events", C.c_int32), ("padding", C.c_int32), ("_pad0", C.c_int32), ("s_star", C.c_int64),
-        ("t_i_init_us", C.c_int64),
+        ("t_i_init_us", C.c_int64), ("kv_layers", C.c_int32), ("kv_heads", C.c_int32), ("q_heads", C.c_int32),
+        ("head_dim", C.c_int32), ("host_swap_pages", C.c_int64), ("decode", C.c_int32), ("decode_split", C.c_int32),
     ]
 
 
@@ -78,7 +79,7 @@ EXPORTS = (
     "co_create", "co_destroy", "co_step", "co_run", "co_preempt", "co_get_scalars", "co_read_field",
     "co_drain_events", "co_pending_events", "co_drain_samples", "co_read_token_times",
     "co_check_invariants", "co_last_device_ms", "co_kernels_per_step", "co_time_steps", "co_last_error",
-    "co_version", "co_read_block_tables",
+    "co_version", "co_read_block_tables", "co_data_stats", "co_kv_verify", "co_read_decode", "co_host_link_gbs",
 )
 
 _lib = None
@@ -115,6 +116,10 @@ def load() -> C.CDLL:
         "co_kernels_per_step": (C.c_int, [V, I32P]),
         "co_time_steps": (C.c_int, [V, C.c_int32, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "co_read_block_tables": (C.c_int, [V, I32P, I32P, C.c_int64, I32P, I32P]),
+        "co_data_stats": (C.c_int, [V, I64P]),
+        "co_kv_verify": (C.c_int, [V, I64P, I64P]),
+        "co_read_decode": (C.c_int, [V, I32P, I32P, C.POINTER(C.c_float), C.c_int64, I64P, I64P]),
+        "co_host_link_gbs": (C.c_int, [C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "co_last_error": (C.c_char_p, []),
         "co_version": (C.c_char_p, []),
     }

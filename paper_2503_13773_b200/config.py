@@ -169,6 +169,41 @@ class SchedulerConfig:
             raise ValueError("epsilon_us must be >= 0")
 
 
+@dataclass(frozen=True)
+class KVLayout:
+    """KV data plane of an instance (no reference counterpart: the reference
+    only counts tokens, kvc.py:1-16).  Pages hold block_size tokens laid out
+    [layer][K|V][kv_head][slot][head_dim] in bf16.  Presets: Llama-2-13B
+    (40 layers, 40/40 heads) and Llama-2-70B (80 layers, 64 q / 8 kv heads)."""
+    layers: int
+    kv_heads: int
+    q_heads: int
+    head_dim: int = 128
+    host_swap_pages: int = 1024
+    decode: bool = True
+    decode_split: int = 512
+
+    def __post_init__(self) -> None:
+        if self.layers < 1 or self.kv_heads < 1:
+            raise ValueError("layers and kv_heads must be >= 1")
+        if self.head_dim != 128:
+            raise ValueError("head_dim must be 128")
+        if self.q_heads % self.kv_heads or self.q_heads // self.kv_heads > 16:
+            raise ValueError("q_heads must be a multiple (at most 16x) of kv_heads")
+
+    @property
+    def bytes_per_token(self) -> int:
+        return self.layers * 2 * self.kv_heads * self.head_dim * 2
+
+    @staticmethod
+    def llama2_13b(**kw) -> "KVLayout":
+        return KVLayout(layers=40, kv_heads=40, q_heads=40, **kw)
+
+    @staticmethod
+    def llama2_70b(**kw) -> "KVLayout":
+        return KVLayout(layers=80, kv_heads=8, q_heads=64, **kw)
+
+
 @dataclass
 class EngineConfig:
     capacity_tokens: int = 16_384

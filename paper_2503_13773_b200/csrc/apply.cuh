@@ -173,10 +173,14 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
         bool token = false;
         int32_t nu;
         if (d.prefill[i] < d.kv_need[i]) {
+            d.l_fill_t0[k] = d.prefill[i];  // N2: the chunk's KV is written this iteration
+            d.l_fill_n[k] = tok;
             d.prefill[i] += tok;
             nu = d.prefill[i];
             token = d.prefill[i] >= d.kv_need[i] && d.gen[i] == 0;
         } else {
+            d.l_fill_t0[k] = d.used[i];     // decode writes the KV of position used
+            d.l_fill_n[k] = -1;             // (negative: decode member)
             nu = d.used[i] + 1;
             token = true;
         }
@@ -203,6 +207,18 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
     if (tid == 0) {
         c.used_sum += dused;
         c.gen_total += dgen;
+        if (d.dp.on) {
+            // guests' KV goes into their host's pages now, before a completing
+            // host re-homes them or a colliding host evicts them
+            for (int32_t k = 0; k < ns; k++) {
+                const int32_t i = d.l_surv_idx[k];
+                if (d.host[i] >= 0) {
+                    int32_t n = d.l_fill_n[k];
+                    log_fill(d, d.dp, i, d.l_fill_t0[k], n < 0 ? 1 : n);
+                    d.l_fill_n[k] = n < 0 ? -2 : 0;  // logged
+                }
+            }
+        }
         for (int32_t k = 0; k < n_done; k++) do_complete(d, d.l_done[k], end);
     }
     __syncthreads();
@@ -224,6 +240,33 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
             if (g < 0 || d.used[h] < d.off[g]) continue;
             if (pool_promote(d, g)) continue;
             if (d.state[g] == ST_RUNNING) do_preempt(d, g, strategy_of(d, g), end, CO_CAUSE_COLLISION);
+        }
+        if (d.dp.on) {
+            // standalone members' KV at their final pages, then this
+            // iteration's decode set (members that decoded and still hold)
+            DataCtl& dc = *d.dctl;
+            int32_t nd = 0, items = 0;
+            for (int32_t k = 0; k < ns; k++) {
+                const int32_t i = d.l_surv_idx[k];
+                const int32_t n = d.l_fill_n[k];
+                if (!d.holds[i] || d.state[i] != ST_RUNNING) continue;
+                if (n > 0 || n == -1) log_fill(d, d.dp, i, d.l_fill_t0[k], n < 0 ? 1 : n);
+                if ((n == -1 || n == -2) && d.dp.decode_on && nd < d.dp.dec_cap) {
+                    const int32_t ctx = d.used[i];
+                    const int32_t need = ((ctx + d.dp.split - 1) / d.dp.split) * d.dp.L * d.dp.Hkv;
+                    if (items + need > d.dp.dec_item_cap) { c.error = 8; break; }
+                    d.dp.dec_idx[nd] = i;
+                    d.dp.dec_ctx[nd] = ctx;
+                    d.dp.dec_item_off[nd] = items;
+                    items += need;
+                    nd++;
+                }
+            }
+            d.dp.dec_item_off[nd] = items;
+            dc.n_dec = nd;
+            dc.dec_items = items;
+            if (nd) { dc.dec_steps += 1; dc.dec_members += nd; }
+            for (int32_t k = 0; k < nd; k++) dc.dec_tokens += d.dp.dec_ctx[k];
         }
         // engine.py:636-640
         int64_t sp = c.sample_count++;

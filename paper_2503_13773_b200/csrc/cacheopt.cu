@@ -25,6 +25,7 @@
 #include "grid_kernels.cuh"
 #include "planner.cuh"
 #include "apply.cuh"
+#include "data_plane.cuh"
 
 using namespace co;
 
@@ -72,6 +73,9 @@ struct co_engine {
     std::vector<int64_t> perm;         // sorted position -> caller position
     std::vector<int64_t> tok_off_host;
     int64_t n_chunks = 0;
+    int sms = 148;
+    void* host_pool = nullptr;
+    int64_t page_bytes = 0;
     std::vector<co_event> st_events;   // host staging of drained device events
     std::vector<int32_t> st_members;
     std::vector<int64_t> st_samples;
@@ -128,6 +132,18 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
     if (ev) mark(ev[5], s);
     k_check<<<1, NT, 0, s>>>(d, 0);
     if (ev) mark(ev[6], s);
+    if (d.dp.on) {
+        k_data<<<E->sms, 512, 0, s>>>(d, d.dp, d.dctl);
+        if (ev) mark(ev[7], s);
+        if (d.dp.decode_on) {
+            k_decode<<<E->sms * 8, DEC_T, 0, s>>>(d, d.dp, d.dctl);
+            k_decode_reduce<<<E->sms * 8, 128, 0, s>>>(d, d.dp, d.dctl);
+        }
+        if (ev) mark(ev[8], s);
+    } else if (ev) {
+        mark(ev[7], s);
+        mark(ev[8], s);
+    }
     return CO_OK;
 }
 
@@ -191,6 +207,7 @@ int co_destroy(co_engine* E) {
     if (E->graph) cudaGraphExecDestroy(E->graph);
     for (void* p : E->allocs) cudaFree(p);
     if (E->cub_tmp) cudaFree(E->cub_tmp);
+    if (E->host_pool) cudaFreeHost(E->host_pool);
     if (E->h_ctl) cudaFreeHost(E->h_ctl);
     if (E->ev0) cudaEventDestroy(E->ev0);
     if (E->ev1) cudaEventDestroy(E->ev1);
@@ -287,6 +304,7 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, E->device);
     E->grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8));
+    E->sms = sms;
 
     Dev& d = E->d;
     d.n = (int32_t)n; d.bs = cfg->block_size; d.B = cfg->block_size; d.buffer_b = cfg->buffer_b;
@@ -338,6 +356,48 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     AL(d.l_defer, n); AL(d.l_pro, n); AL(d.l_ful, n); AL(d.l_part, n3); AL(d.l_part_need, n3);
     AL(d.l_part_grant, n3); AL(d.l_mready, n2); AL(d.l_gm_idx, n); AL(d.l_gm_tok, n); AL(d.l_acted, n3);
     AL(d.l_surv_idx, n3); AL(d.l_surv_tok, n3); AL(d.l_done, n3); AL(d.l_coll, n); AL(d.l_grp, 2 * n3);
+    AL(d.l_fill_t0, n3); AL(d.l_fill_n, n3);
+    AL(d.dctl, 1);
+    std::memset(&d.dp, 0, sizeof(d.dp));
+    if (cfg->kv_layers > 0) {
+        DataCfg& x = d.dp;
+        if (cfg->head_dim != 128) { co_destroy(E); return fail(CO_EINVAL, "head_dim must be 128"); }
+        if (cfg->kv_heads < 1 || cfg->q_heads % cfg->kv_heads || cfg->q_heads / cfg->kv_heads > DEC_GMAX) {
+            co_destroy(E);
+            return fail(CO_EINVAL, "q_heads must be a multiple (<= 16x) of kv_heads");
+        }
+        x.on = 1;
+        x.decode_on = cfg->decode;
+        x.L = cfg->kv_layers; x.Hkv = cfg->kv_heads; x.Hq = cfg->q_heads; x.D = cfg->head_dim;
+        x.rows = x.L * 2 * x.Hkv;
+        x.page_elems = (int64_t)x.rows * cfg->block_size * x.D;
+        x.split = cfg->decode_split > 0 ? cfg->decode_split : 512;
+        const int64_t page_bytes = x.page_elems * 2;
+        AL(x.kv, (int64_t)n_pages * x.page_elems);
+        x.h_pages = (int32_t)std::max<int64_t>(cfg->host_swap_pages, 1);
+        cudaError_t he = cudaHostAlloc(&E->host_pool, (size_t)x.h_pages * page_bytes, cudaHostAllocMapped);
+        if (he != cudaSuccess) { co_destroy(E); return fail(CO_ECUDA, "pinned host swap pool allocation failed"); }
+        void* hdev = nullptr;
+        cudaHostGetDevicePointer(&hdev, E->host_pool, 0);
+        x.hkv = static_cast<uint16_t*>(hdev);
+        x.stage_tokens = max_s + 1;
+        AL(x.stage, x.stage_tokens * x.rows * x.D);
+        x.op_cap = 8 * n + 4096;
+        x.snap_cap = 16 * (int64_t)n_pages + 8 * n + 65536;
+        AL(x.ops, x.op_cap); AL(x.snap, x.snap_cap); AL(x.hstack, x.h_pages);
+        x.hdir_w = (int32_t)((max_s + cfg->block_size - 1) / cfg->block_size + 1);
+        AL(x.hdir, (int64_t)n * x.hdir_w); AL(x.hsaved, n);
+        x.dec_cap = (int32_t)std::min<int64_t>(n, 4096);
+        x.dec_item_cap = 1 << 20;
+        AL(x.dec_idx, x.dec_cap + 1); AL(x.dec_ctx, x.dec_cap + 1); AL(x.dec_item_off, x.dec_cap + 1);
+        const int G = x.Hq / x.Hkv;
+        if (x.decode_on) {
+            AL(x.dec_part, x.dec_item_cap * G * (x.D + 2));
+            AL(x.dec_out, (int64_t)x.dec_cap * x.L * x.Hq * x.D);
+        }
+        AL(x.gbar, 2);
+        E->page_bytes = page_bytes;
+    }
     AL(d.l_tri_key, n); AL(d.am_rhi, n3); AL(d.am_rlo, n3); AL(d.rank_to_idx, n);
     AL(d.sk0, n3); AL(d.sk1, n3); AL(d.sk2, n3); AL(d.sk_item, n3);
     AL(d.events, d.ev_cap); AL(d.members, 2 * d.mem_cap); AL(d.samples, 2 * d.sample_cap);
@@ -371,6 +431,18 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     for (int64_t* p : {d.max_tbt, d.ready_at, d.pstart, d.swap_done, d.ptime, d.rec_seq}) memset_all(p, 0, n8);
     for (int64_t* p : {d.first_tok, d.last_tok, d.first_start, d.completion}) memset_all(p, 0xff, n8);
     memset_all(d.holds, 0, n);
+    memset_all(d.dctl, 0, sizeof(DataCtl));
+    if (d.dp.on) {
+        memset_all(d.dp.gbar, 0, 8);
+        memset_all(d.dp.hsaved, 0, n4);
+        std::vector<int32_t> hs(d.dp.h_pages);
+        for (int32_t k = 0; k < d.dp.h_pages; k++) hs[k] = d.dp.h_pages - 1 - k;
+        if ((r = upload(E, d.dp.hstack, hs))) { co_destroy(E); return r; }
+        DataCtl dc0;
+        std::memset(&dc0, 0, sizeof(dc0));
+        dc0.htop = d.dp.h_pages;
+        CK(cudaMemcpy(d.dctl, &dc0, sizeof(dc0), cudaMemcpyHostToDevice));
+    }
     memset_all(d.tab_len, 0, n4);
     {
         std::vector<int32_t> fs(n_pages);
@@ -410,6 +482,10 @@ static int check_device_error(co_engine* E) {
     const char* what = err == 3 ? "no progress after 1000000 rounds (engine.py:653-656)"
                      : err == 4 ? "pool invariant violated (kvc.py:336-375)"
                      : err == 2 ? "set_used outside [0, granted] (kvc.py:326-332)"
+                     : err == 5 ? "block table capacity exceeded"
+                     : err == 6 ? "data-op log or snapshot buffer full"
+                     : err == 7 ? "host swap pool exhausted (raise KVLayout.host_swap_pages)"
+                     : err == 8 ? "decode work-item buffer full"
                                 : "device engine error";
     snprintf(buf, sizeof(buf), "%s [code %d, info %d %d]", what, err, E->h_ctl->err_info[0], E->h_ctl->err_info[1]);
     return fail(CO_EDEVICE, buf);
@@ -683,6 +759,92 @@ int co_read_block_tables(co_engine* E, int32_t* lens, int32_t* pages, int64_t ma
             if (pages) pages[w + k] = pool[(size_t)dir[(size_t)i * W + k / TCHUNK] * TCHUNK + k % TCHUNK];
         w += lens[i];
     }
+    return CO_OK;
+}
+
+int co_data_stats(co_engine* E, int64_t* st) {
+    if (!E || !st) return fail(CO_EINVAL, "null argument");
+    if (!E->d.dp.on) return fail(CO_EINVAL, "data plane is off (kv_layers = 0)");
+    DataCtl dc;
+    CK(cudaMemcpyAsync(&dc, E->d.dctl, sizeof(dc), cudaMemcpyDeviceToHost, E->stream));
+    CK(cudaStreamSynchronize(E->stream));
+    st[0] = dc.bytes_out; st[1] = dc.bytes_in; st[2] = dc.bytes_fill; st[3] = dc.bytes_move;
+    st[4] = dc.dec_steps; st[5] = dc.dec_members; st[6] = dc.dec_tokens; st[7] = 0;
+    return CO_OK;
+}
+
+int co_kv_verify(co_engine* E, int64_t* bad, int64_t* checked) {
+    if (!E || !bad || !checked) return fail(CO_EINVAL, "null argument");
+    if (!E->d.dp.on) return fail(CO_EINVAL, "data plane is off (kv_layers = 0)");
+    unsigned long long* cnt = nullptr;
+    CK(cudaMalloc(&cnt, 16));
+    CK(cudaMemsetAsync(cnt, 0, 16, E->stream));
+    k_kv_verify<<<E->sms * 4, 256, 0, E->stream>>>(E->d, E->d.dp, cnt, cnt + 1);
+    unsigned long long h[2];
+    CK(cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, E->stream));
+    CK(cudaStreamSynchronize(E->stream));
+    cudaFree(cnt);
+    *bad = (int64_t)h[0];
+    *checked = (int64_t)h[1];
+    return CO_OK;
+}
+
+int co_read_decode(co_engine* E, int32_t* members, int32_t* ctx, float* out, int64_t max_members, int64_t* n,
+                   int64_t* step_id) {
+    if (!E || !n) return fail(CO_EINVAL, "null argument");
+    const DataCfg& x = E->d.dp;
+    if (!x.on || !x.decode_on) return fail(CO_EINVAL, "decode is off");
+    DataCtl dc;
+    CK(cudaMemcpyAsync(&dc, E->d.dctl, sizeof(dc), cudaMemcpyDeviceToHost, E->stream));
+    int r = sync_ctl(E);
+    if (r) return r;
+    *n = dc.n_dec;
+    if (step_id) *step_id = E->h_ctl->steps;
+    if (dc.n_dec > max_members) return fail(CO_EINVAL, "decode buffers too small");
+    if (dc.n_dec) {
+        if (members) CK(cudaMemcpyAsync(members, x.dec_idx, dc.n_dec * 4, cudaMemcpyDeviceToHost, E->stream));
+        if (ctx) CK(cudaMemcpyAsync(ctx, x.dec_ctx, dc.n_dec * 4, cudaMemcpyDeviceToHost, E->stream));
+        if (out)
+            CK(cudaMemcpyAsync(out, x.dec_out, (size_t)dc.n_dec * x.L * x.Hq * x.D * sizeof(float),
+                               cudaMemcpyDeviceToHost, E->stream));
+        CK(cudaStreamSynchronize(E->stream));
+    }
+    return CO_OK;
+}
+
+int co_host_link_gbs(int64_t bytes, double* d2h, double* h2d) {
+    if (bytes <= 0 || !d2h || !h2d) return fail(CO_EINVAL, "bad arguments");
+    void *dev = nullptr, *host = nullptr;
+    cudaStream_t s;
+    cudaEvent_t a, b;
+    CK(cudaMalloc(&dev, bytes));
+    CK(cudaHostAlloc(&host, bytes, cudaHostAllocDefault));
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    float best_d2h = 1e30f, best_h2d = 1e30f;
+    for (int rep = 0; rep < 5; rep++) {
+        float ms;
+        cudaEventRecord(a, s);
+        cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, s);
+        cudaEventRecord(b, s);
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+        best_d2h = std::min(best_d2h, ms);
+        cudaEventRecord(a, s);
+        cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, s);
+        cudaEventRecord(b, s);
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+        best_h2d = std::min(best_h2d, ms);
+    }
+    *d2h = bytes / (best_d2h * 1e-3) / 1e9;
+    *h2d = bytes / (best_h2d * 1e-3) / 1e9;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaStreamDestroy(s);
+    cudaFree(dev);
+    cudaFreeHost(host);
     return CO_OK;
 }
 

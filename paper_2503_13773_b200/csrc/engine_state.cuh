@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "../../include/cacheopt.h"
+#include "dp_types.cuh"
 
 namespace co {
 
@@ -95,12 +96,15 @@ struct Dev {
     // planner / apply scratch (n-sized unless noted)
     int32_t *l_nr, *l_nrp, *l_pend, *l_tri, *l_tri_taken, *l_vict, *l_defer, *l_pro, *l_ful,
         *l_part, *l_part_need, *l_part_grant, *l_mready, *l_gm_idx, *l_gm_tok, *l_acted,
-        *l_surv_idx, *l_surv_tok, *l_done, *l_coll, *l_grp;
+        *l_surv_idx, *l_surv_tok, *l_done, *l_coll, *l_grp, *l_fill_t0, *l_fill_n;
     int64_t* l_tri_key;
     uint64_t *am_rhi, *am_rlo;   // amortize remainders (128-bit), by participant position
     int32_t* rank_to_idx;        // inverse of idrank
     uint64_t *sk0, *sk1, *sk2;   // generic sort keys
     int32_t* sk_item;
+    // N2/N3 data plane
+    DataCfg dp;
+    DataCtl* dctl;
     // outputs
     co_event* events;
     int32_t* members;   // (idx, tok) pairs

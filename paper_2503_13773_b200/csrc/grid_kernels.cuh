@@ -36,6 +36,7 @@ __global__ void k_begin(Dev d, int32_t guard) {
     }
     c.last_result = 0;
     c.sid += 1;
+    if (d.dp.on) { d.dctl->n_dec = 0; d.dctl->dec_items = 0; }
     c.cnt_nw = c.cnt_nwp = c.cnt_run = 0;
     if (guard) {
         // engine.py:644-659 no-progress guard, evaluated before each step()

@@ -7,6 +7,7 @@
 // (engine.py:448-467); the ones the engine does not swallow set ctl->error.
 #pragma once
 #include "engine_state.cuh"
+#include "data_plane.cuh"
 
 namespace co {
 
@@ -133,11 +134,16 @@ __device__ bool pool_promote(const Dev& d, int i) {
     int64_t fp = fp_tokens(d.granted[i], d.bs);
     if (fp > free_tokens(d)) return false;
     int32_t h = d.host[i];
+    int64_t vsnap = 0;
+    int32_t vend = 0;
+    const int32_t gused = d.used[i];
+    if (d.dp.on && gused > 0) vsnap = snap_view(d, d.dp, h, d.off[i] + d.granted[i], gused, &vend);
     d.guest[h] = -1;
     d.host[i] = -1;
     d.off[i] = 0;
     d.ctl->fp_sum += fp;
     pop_pages(d, i, fp / d.bs);
+    if (d.dp.on && gused > 0) log_move(d, d.dp, i, gused, vsnap, vend);  // N2: the guest's KV follows it
     return true;
 }
 
@@ -153,6 +159,12 @@ __device__ void pool_release(const Dev& d, int i) {
         return;
     }
     int32_t g = d.guest[i];
+    int64_t vsnap = 0;
+    int32_t vend = 0, gused = 0;
+    if (g >= 0 && d.dp.on) {
+        gused = d.used[g];
+        if (gused > 0) vsnap = snap_view(d, d.dp, i, d.off[g] + d.granted[g], gused, &vend);
+    }
     push_table(d, i);
     if (g >= 0) {  // the guest is re-homed (kvc.py:311-317) into pages of its own
         d.host[g] = -1;
@@ -161,6 +173,7 @@ __device__ void pool_release(const Dev& d, int i) {
         c.fp_sum += gfp;
         d.guest[i] = -1;
         pop_pages(d, g, gfp / d.bs);
+        if (d.dp.on && gused > 0) log_move(d, d.dp, g, gused, vsnap, vend);
     }
     c.fp_sum -= fp_tokens(d.granted[i], d.bs);
     c.granted_sum -= d.granted[i];
@@ -208,6 +221,7 @@ __device__ void do_preempt(const Dev& d, int i, int32_t strat, int64_t now, int3
     d.prefill[i] = u;
     if (u > d.kv_need[i]) d.kv_need[i] = u;
     d.swap_done[i] = strat == CO_SWAP ? now + lut(d.lut_swap_half, restored, d.s_max) : 0;
+    if (strat == CO_SWAP) log_swap_out(d, d.dp, i);  // N2: KV leaves before its pages do
     if (d.holds[i]) pool_release(d, i);
     d.used[i] = 0;
     d.alloc_kvc[i] = 0;
@@ -232,6 +246,7 @@ __device__ void do_readmit(const Dev& d, int i) {
     d.ptime[i] += ra - d.pstart[i];
     int32_t u = d.prefill[i] < d.granted[i] ? d.prefill[i] : d.granted[i];
     set_used(d, i, u);
+    log_readmit(d, d.dp, i, d.last_strat[i] == CO_SWAP);  // N2: swap-in or recompute fill
     emit_event(d, CO_EV_READMIT, i, now, ra);
 }
 

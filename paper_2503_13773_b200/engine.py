@@ -221,7 +221,7 @@ class Engine:
     """Device-backed drop-in for the reference Engine (policy ``cacheopt``)."""
 
     def __init__(self, requests: Sequence[Request], cfg: EngineConfig, device: int = -1,
-                 steps_per_launch: int = 32):
+                 steps_per_launch: int = 32, kv: Optional["KVLayout"] = None):
         ids = [r.id for r in requests]
         if len(set(ids)) != len(ids):
             raise ValueError("request ids must be unique")
@@ -284,6 +284,12 @@ class Engine:
         c.padding = self.padding
         c.s_star = sweet_spot(cfg.truth.swap_true, cfg.truth.recompute_true)
         c.t_i_init_us = iteration_us(cfg, sc.token_budget)
+        self.kv = kv
+        if kv is not None:
+            c.kv_layers, c.kv_heads, c.q_heads, c.head_dim = kv.layers, kv.kv_heads, kv.q_heads, kv.head_dim
+            c.host_swap_pages = kv.host_swap_pages
+            c.decode = int(kv.decode)
+            c.decode_split = kv.decode_split
         t = N.CoTrace()
         t.n = n
         t.req_id = _ptr(req_id, C.c_int64)
@@ -399,6 +405,34 @@ class Engine:
                 out[self._rid[k]] = pages[w:w + lens[k]].tolist()
                 w += int(lens[k])
         return out, free[:nf.value].tolist()
+
+    # -- N2/N3 data plane --------------------------------------------------------
+
+    def data_stats(self) -> Dict[str, int]:
+        st = np.zeros(8, dtype=np.int64)
+        N.check(self._lib.co_data_stats(self._h, _ptr(st, C.c_int64)), "co_data_stats")
+        keys = ("swap_out_bytes", "swap_in_bytes", "fill_bytes", "move_bytes", "decode_steps",
+                "decode_member_steps", "decode_ctx_tokens")
+        return dict(zip(keys, (int(v) for v in st)))
+
+    def kv_verify(self) -> Tuple[int, int]:
+        bad, chk = C.c_int64(), C.c_int64()
+        N.check(self._lib.co_kv_verify(self._h, C.byref(bad), C.byref(chk)), "co_kv_verify")
+        return int(bad.value), int(chk.value)
+
+    def last_decode(self):
+        """(member req_ids, ctx lengths, out[m][layer][q_head][128] fp32, step id)."""
+        kv = self.kv
+        cap = min(self._n, 4096)
+        mem = np.empty(max(cap, 1), dtype=np.int32)
+        ctx = np.empty(max(cap, 1), dtype=np.int32)
+        out = np.empty((max(cap, 1), kv.layers, kv.q_heads, kv.head_dim), dtype=np.float32)
+        n, sid = C.c_int64(), C.c_int64()
+        N.check(self._lib.co_read_decode(self._h, _ptr(mem, C.c_int32), _ptr(ctx, C.c_int32),
+                                         out.ctypes.data_as(C.POINTER(C.c_float)), cap, C.byref(n), C.byref(sid)),
+                "co_read_decode")
+        k = int(n.value)
+        return [self._rid[i] for i in mem[:k]], ctx[:k].copy(), out[:k].copy(), int(sid.value)
 
     def check_invariants(self) -> None:
         N.check(self._lib.co_check_invariants(self._h), "check_invariants")
