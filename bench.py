@@ -160,6 +160,84 @@ def workload_config(world):
             "l2": "flushed (256 MiB memset) before every timed step", "parallelism": f"{world} independent instances"}
 
 
+def long_output_trace(n=200, rate=1.0, seed=0):
+    """BASELINE config 5 trace: prompt 512 [16, 4096], output 4096 [1024, 8192], cv 0.5."""
+    import paper_2503_13773_b200 as P
+    spec = P.TraceSpec(arrival_rate=rate, num_requests=n, input_mean=512, input_min=16, input_max=4096,
+                       output_mean=4096, output_min=1024, output_max=8192, length_cv=0.5)
+    reqs = P.generate(spec, seed)
+    P.assign_slos(reqs, 2_000_000, 100_000, P.SloPolicy(), seed)
+    return reqs
+
+
+def swap_leg(dev):
+    """N2: swap-out/in of the mean swapped sequence of the long-output trace
+    (4,731 tokens, Llama-2-70B layout: 1.55 GB) through the engine's own data
+    kernel, against the pinned cudaMemcpyAsync peak of this host link."""
+    import ctypes as C
+    import paper_2503_13773_b200 as P
+    from paper_2503_13773_b200 import _native as N
+    lib = N.load()
+    d2h, h2d = C.c_double(), C.c_double()
+    N.check(lib.co_host_link_gbs(1 << 30, C.byref(d2h), C.byref(h2d)), "host link")
+    kv = P.KVLayout.llama2_70b(host_swap_pages=320, decode=False)
+    cfg = P.EngineConfig(capacity_tokens=65_536, reserved_blocks=8, sched=P.SchedulerConfig(small_block_b=16))
+    eng = P.Engine(long_output_trace(n=8), cfg, device=dev, kv=kv)
+    ntok = 4731
+    out_ms, in_ms = eng.swap_bench(ntok, iters=5)
+    eng.close()
+    nbytes = ntok * kv.bytes_per_token
+    out_gbs, in_gbs = nbytes / out_ms / 1e6, nbytes / in_ms / 1e6
+    return {"metric": "KV swap GB/s", "tokens": ntok, "bytes": nbytes,
+            "swap_out_gbs": out_gbs, "swap_in_gbs": in_gbs,
+            "host_link_peak_gbs": {"d2h": d2h.value, "h2d": h2d.value, "how": "pinned cudaMemcpyAsync 1 GiB, best of 5"},
+            "roofline": {"bound": "host-link", "frac_out": out_gbs / d2h.value, "frac_in": in_gbs / h2d.value},
+            "kernel": "k_data (SM copy through mapped pinned host pages)"}
+
+
+def decode_leg(dev, warm_steps=6000, k=10):
+    """N3: paged decode over the engine's block tables, Llama-2-70B layout,
+    long-output trace; decode enabled only for the k timed steps."""
+    import ctypes as C
+    import paper_2503_13773_b200 as P
+    from paper_2503_13773_b200 import _native as N
+    kv = P.KVLayout.llama2_70b(host_swap_pages=4096, decode=True, decode_split=512)
+    cfg = P.EngineConfig(capacity_tokens=65_536, reserved_blocks=8, sched=P.SchedulerConfig(small_block_b=16),
+                         record_events=False)
+    eng = P.Engine(long_output_trace(), cfg, device=dev, kv=kv)
+    eng.set_decode(False)
+    eng.run_steps(warm_steps)
+    eng.set_decode(True)
+    st0 = eng.data_stats()
+    step_ms = (C.c_double * k)()
+    stage_ms = (C.c_double * N.NSTAGES)()
+    eng._dirty()
+    N.check(eng._lib.co_time_steps(eng._h, k, L2_FLUSH_BYTES, step_ms, stage_ms), "co_time_steps")
+    st1 = eng.data_stats()
+    bad, checked = eng.kv_verify()
+    eng.close()
+    members = st1["decode_member_steps"] - st0["decode_member_steps"]
+    ctx = st1["decode_ctx_tokens"] - st0["decode_ctx_tokens"]
+    dec_ms = stage_ms[7]
+    nbytes = ctx * kv.bytes_per_token
+    peak, kind = load_peaks()
+    gbs = nbytes / (dec_ms * 1e-3) / 1e9 if dec_ms else 0.0
+    return {"metric": "paged-decode tokens/s", "value": members / (dec_ms * 1e-3) if dec_ms else 0.0,
+            "unit": "tokens/s", "steps": k, "members_per_step": members / k, "mean_ctx": ctx / max(members, 1),
+            "decode_ms_per_step": dec_ms / k,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                         "frac": gbs / peak, "peak_kind": peak_kind_label(kind),
+                         "algorithmic_bytes_per_launch": nbytes // k},
+            "kv_integrity": {"mismatches": bad, "checked": checked},
+            "config": "BASELINE config 5: Llama-2-70B KV layout (80 layers, 64 q / 8 kv heads), long-output trace "
+                      "200 reqs @1 req/s, pool 65,536 tokens (21.5 GB), decode on for the timed steps after "
+                      f"{warm_steps} warm steps"}
+
+
+def peak_kind_label(kind):
+    return f"{kind} (MEASURED_PEAKS.json hbm_gbs)" if kind == "measured" else kind
+
+
 def device_arm(args, rank, world, dist):
     import ctypes as C
     import torch
@@ -224,6 +302,16 @@ def device_arm(args, rank, world, dist):
     ach = algo / (stages[dom] * 1e-3) / 1e9 if algo else 0.0
     cpu_val, cpu_steps, cpu_dt = run_cpu_baseline(*make_trace(0, 1), budget_s=10.0)
     iter_ev_bytes = 40 + 8 * 30
+    extra = {}
+    if not args.skip_legs:
+        try:
+            extra["swap"] = swap_leg(dev)
+        except Exception as exc:  # reported, never silently replaced
+            extra["swap"] = {"error": repr(exc)}
+        try:
+            extra["decode"] = decode_leg(dev)
+        except Exception as exc:
+            extra["decode"] = {"error": repr(exc)}
     line = {
         "metric": METRIC, "value": decisions / (dev_ms * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
@@ -242,6 +330,7 @@ def device_arm(args, rank, world, dist):
         "gpu_launches": args.steps * 6,
         "gpu_launches_note": "6 own kernels per step (begin, admit, classify, plan, apply, check) + CUB onesweep sort kernels",
         "clocks": clocks.summary(),
+        **extra,
     }
     print(json.dumps(line))
 
@@ -252,6 +341,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--skip-legs", action="store_true", help="only the scheduler leg")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -221,6 +221,12 @@ int co_kv_verify(co_engine* eng, int64_t* mismatches, int64_t* checked);
  * context lengths, and out[member][layer][q_head][head_dim] fp32 */
 int co_read_decode(co_engine* eng, int32_t* members, int32_t* ctx, float* out, int64_t max_members,
                    int64_t* n_members, int64_t* step_id);
+/* turn the per-step decode on/off at run time (configured with decode = 1) */
+int co_set_decode(co_engine* eng, int32_t on);
+/* swap micro-benchmark: one gather (HBM pages -> pinned host) and one scatter
+ * (back) of ntok tokens through the engine's own data kernel; mean device
+ * ms of each over `iters` rounds.  Clobbers KV contents. */
+int co_swap_bench(co_engine* eng, int64_t ntok, int32_t iters, double* out_ms, double* in_ms);
 /* pinned-memory cudaMemcpyAsync bandwidth of this GPU's host link (GB/s) */
 int co_host_link_gbs(int64_t bytes, double* d2h, double* h2d);
 /* kvc.py:336-375 BlockPool.check_invariants on the device; CO_EDEVICE on

@@ -80,6 +80,7 @@ EXPORTS = (
     "co_drain_events", "co_pending_events", "co_drain_samples", "co_read_token_times",
     "co_check_invariants", "co_last_device_ms", "co_kernels_per_step", "co_time_steps", "co_last_error",
     "co_version", "co_read_block_tables", "co_data_stats", "co_kv_verify", "co_read_decode", "co_host_link_gbs",
+    "co_set_decode", "co_swap_bench",
 )
 
 _lib = None
@@ -120,6 +121,8 @@ def load() -> C.CDLL:
         "co_kv_verify": (C.c_int, [V, I64P, I64P]),
         "co_read_decode": (C.c_int, [V, I32P, I32P, C.POINTER(C.c_float), C.c_int64, I64P, I64P]),
         "co_host_link_gbs": (C.c_int, [C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+        "co_set_decode": (C.c_int, [V, C.c_int32]),
+        "co_swap_bench": (C.c_int, [V, C.c_int64, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "co_last_error": (C.c_char_p, []),
         "co_version": (C.c_char_p, []),
     }

@@ -133,7 +133,7 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
     k_check<<<1, NT, 0, s>>>(d, 0);
     if (ev) mark(ev[6], s);
     if (d.dp.on) {
-        k_data<<<E->sms, 512, 0, s>>>(d, d.dp, d.dctl);
+        k_data<<<E->sms, 512, 0, s>>>(d, d.dp, d.dctl, 0);
         if (ev) mark(ev[7], s);
         if (d.dp.decode_on) {
             k_decode<<<E->sms * 8, DEC_T, 0, s>>>(d, d.dp, d.dctl);
@@ -441,6 +441,7 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
         DataCtl dc0;
         std::memset(&dc0, 0, sizeof(dc0));
         dc0.htop = d.dp.h_pages;
+        dc0.decode_enabled = d.dp.decode_on;
         CK(cudaMemcpy(d.dctl, &dc0, sizeof(dc0), cudaMemcpyHostToDevice));
     }
     memset_all(d.tab_len, 0, n4);
@@ -845,6 +846,60 @@ int co_host_link_gbs(int64_t bytes, double* d2h, double* h2d) {
     cudaStreamDestroy(s);
     cudaFree(dev);
     cudaFreeHost(host);
+    return CO_OK;
+}
+
+int co_set_decode(co_engine* E, int32_t on) {
+    if (!E || !E->d.dp.on || !E->d.dp.decode_on) return fail(CO_EINVAL, "decode is not configured");
+    int32_t v = on ? 1 : 0;
+    CK(cudaMemcpyAsync(&E->d.dctl->decode_enabled, &v, 4, cudaMemcpyHostToDevice, E->stream));
+    CK(cudaStreamSynchronize(E->stream));
+    return CO_OK;
+}
+
+// Swap data path micro-benchmark: ONE GATHER (device pages -> pinned host
+// pages) and ONE SCATTER (back) of ntok tokens through k_data, the same
+// kernel the engine runs, on the first pages of the pool.  Clobbers KV
+// contents: use a dedicated instance.
+int co_swap_bench(co_engine* E, int64_t ntok, int32_t iters, double* out_ms, double* in_ms) {
+    if (!E || !out_ms || !in_ms || iters < 1) return fail(CO_EINVAL, "bad arguments");
+    DataCfg& x = E->d.dp;
+    if (!x.on) return fail(CO_EINVAL, "data plane is off");
+    const int bs = E->d.bs;
+    const int64_t np = (ntok + bs - 1) / bs;
+    if (np > E->d.n_pages || np > x.h_pages || ntok > (1ll << 30)) return fail(CO_EINVAL, "ntok too large");
+    std::vector<int32_t> snap(2 * np);
+    for (int64_t k = 0; k < np; k++) { snap[k] = (int32_t)k; snap[np + k] = (int32_t)k; }
+    CK(cudaMemcpyAsync(x.snap, snap.data(), snap.size() * 4, cudaMemcpyHostToDevice, E->stream));
+    DOp ops[2];
+    for (int q = 0; q < 2; q++) {
+        ops[q].kind = q == 0 ? D_GATHER : D_SCATTER; ops[q].req = 0; ops[q].ntok = (int32_t)ntok; ops[q].t0 = 0;
+        ops[q].src_end = ops[q].dst_end = -1;
+        ops[q].src_where = q == 0 ? W_DEV : W_HOST; ops[q].dst_where = q == 0 ? W_HOST : W_DEV;
+        ops[q].src_snap = q == 0 ? 0 : np; ops[q].dst_snap = q == 0 ? np : 0;
+    }
+    DataCtl saved;
+    CK(cudaMemcpyAsync(&saved, E->d.dctl, sizeof(saved), cudaMemcpyDeviceToHost, E->stream));
+    CK(cudaStreamSynchronize(E->stream));
+    float t_out = 0, t_in = 0;
+    for (int it = 0; it < iters + 1; it++) {
+        for (int q = 0; q < 2; q++) {
+            CK(cudaMemcpyAsync(x.ops, &ops[q], sizeof(DOp), cudaMemcpyHostToDevice, E->stream));
+            int32_t one = 1;
+            CK(cudaMemcpyAsync(&E->d.dctl->n_ops, &one, 4, cudaMemcpyHostToDevice, E->stream));
+            CK(cudaEventRecord(E->ev0, E->stream));
+            k_data<<<E->sms, 512, 0, E->stream>>>(E->d, x, E->d.dctl, 1);
+            CK(cudaEventRecord(E->ev1, E->stream));
+            CK(cudaEventSynchronize(E->ev1));
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, E->ev0, E->ev1));
+            if (it > 0) (q == 0 ? t_out : t_in) += ms;  // first round is warm-up
+        }
+    }
+    CK(cudaMemcpyAsync(E->d.dctl, &saved, sizeof(saved), cudaMemcpyHostToDevice, E->stream));
+    CK(cudaStreamSynchronize(E->stream));
+    *out_ms = t_out / iters;
+    *in_ms = t_in / iters;
     return CO_OK;
 }
 

@@ -205,9 +205,9 @@ __device__ __forceinline__ int64_t loc_elem(const Dev& d, const DataCfg& x, int3
     return (int64_t)page * x.page_elems + ((int64_t)row * bs + slot) * x.D;
 }
 
-__global__ void __launch_bounds__(512, 1) k_data(Dev d, DataCfg x, DataCtl* dc) {
+__global__ void __launch_bounds__(512, 1) k_data(Dev d, DataCfg x, DataCtl* dc, int force = 0) {
     const Ctl& c = *d.ctl;
-    if (!c.active || !x.on) return;
+    if (!(c.active || force) || !x.on) return;
     const int32_t nops = dc->n_ops;
     if (nops == 0) return;
     const int64_t units_per_tok = (int64_t)x.rows * (x.D / 8);  // 16-byte units
@@ -297,7 +297,7 @@ constexpr int DEC_GMAX = 16;
 
 __global__ void __launch_bounds__(DEC_T) k_decode(Dev d, DataCfg x, DataCtl* dc) {
     const Ctl& c = *d.ctl;
-    if (!c.active || !x.decode_on) return;
+    if (!c.active || !x.decode_on || !dc->decode_enabled) return;
     const int32_t nitems = dc->dec_items;
     const int G = x.Hq / x.Hkv;
     const int D = x.D;  // 128
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(DEC_T) k_decode(Dev d, DataCfg x, DataCtl* dc)
 // combine the splits of every (member, layer, q head)
 __global__ void k_decode_reduce(Dev d, DataCfg x, DataCtl* dc) {
     const Ctl& c = *d.ctl;
-    if (!c.active || !x.decode_on) return;
+    if (!c.active || !x.decode_on || !dc->decode_enabled) return;
     const int G = x.Hq / x.Hkv, D = x.D;
     const int32_t nm = dc->n_dec;
     const int64_t total = (int64_t)nm * x.L * x.Hq;

@@ -41,7 +41,7 @@ struct DataCfg {
 };
 
 struct DataCtl {
-    int32_t n_ops, n_dec, htop, dec_items, _pad;
+    int32_t n_ops, n_dec, htop, dec_items, decode_enabled;
     int64_t n_snap;
     int64_t bytes_out, bytes_in, bytes_fill, bytes_move;
     int64_t dec_steps, dec_members, dec_tokens;

@@ -415,6 +415,15 @@ class Engine:
                 "decode_member_steps", "decode_ctx_tokens")
         return dict(zip(keys, (int(v) for v in st)))
 
+    def set_decode(self, on: bool) -> None:
+        N.check(self._lib.co_set_decode(self._h, int(on)), "co_set_decode")
+
+    def swap_bench(self, ntok: int, iters: int = 5) -> Tuple[float, float]:
+        """(gather ms, scatter ms) of ntok tokens through the engine's data kernel."""
+        a, b = C.c_double(), C.c_double()
+        N.check(self._lib.co_swap_bench(self._h, ntok, iters, C.byref(a), C.byref(b)), "co_swap_bench")
+        return float(a.value), float(b.value)
+
     def kv_verify(self) -> Tuple[int, int]:
         bad, chk = C.c_int64(), C.c_int64()
         N.check(self._lib.co_kv_verify(self._h, C.byref(bad), C.byref(chk)), "co_kv_verify")
