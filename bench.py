@@ -249,6 +249,10 @@ def device_arm(args, rank, world, dist):
     reqs, cfg = make_trace(rank, world)
     cfg.record_events = True
     eng = Engine(reqs, cfg, device=dev)
+    if dist:
+        # N4: per-iteration global-reserve all-reduce inside the step graph
+        from paper_2503_13773_b200.multi import attach_global_reserve
+        attach_global_reserve(eng, rank, world)
     pre = max(0, WINDOW_START - args.warmup)
     with ClockSampler(dev) as clocks:
         eng.run_steps(pre)
@@ -270,6 +274,11 @@ def device_arm(args, rank, world, dist):
         s1 = eng._scalars()
     dev_ms = float(sum(step_ms))
     decisions = s1.decisions - d0
+    coll = None
+    if dist:
+        gfree, grsv, calls = eng.global_reserve()
+        coll = {"op": "ncclAllReduce(sum, int64[2]={free_tokens, reserved_blocks}) per iteration, side stream",
+                "calls": calls, "global_free_tokens": gfree, "global_reserved_blocks": grsv}
     live = s1.n_live
     # e2e: the public per-step API (step() + event drain into host dicts),
     # on the steps that follow the timed window
@@ -303,7 +312,7 @@ def device_arm(args, rank, world, dist):
     cpu_val, cpu_steps, cpu_dt = run_cpu_baseline(*make_trace(0, 1), budget_s=10.0)
     iter_ev_bytes = 40 + 8 * 30
     extra = {}
-    if not args.skip_legs:
+    if not args.skip_legs and world == 1:
         try:
             extra["swap"] = swap_leg(dev)
         except Exception as exc:  # reported, never silently replaced
@@ -330,6 +339,7 @@ def device_arm(args, rank, world, dist):
         "gpu_launches": args.steps * 6,
         "gpu_launches_note": "6 own kernels per step (begin, admit, classify, plan, apply, check) + CUB onesweep sort kernels",
         "clocks": clocks.summary(),
+        "collective": coll,
         **extra,
     }
     print(json.dumps(line))

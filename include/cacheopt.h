@@ -227,6 +227,18 @@ int co_set_decode(co_engine* eng, int32_t on);
  * (back) of ntok tokens through the engine's own data kernel; mean device
  * ms of each over `iters` rounds.  Clobbers KV contents. */
 int co_swap_bench(co_engine* eng, int64_t ntok, int32_t iters, double* out_ms, double* in_ms);
+/* N4 (no reference counterpart; kvc.py:76-79 is one instance): a 128-byte
+ * ncclUniqueId for rank 0 to broadcast, and attaching the instance to an
+ * NCCL communicator, after which every step all-reduces (sum) the instance's
+ * [free_tokens, reserved_blocks_current] on a side stream captured into the
+ * step graph.  Telemetry only: decisions never read it, so each instance stays
+ * bit-exact against its own CPU reference.  Every rank must then launch the
+ * same number of steps (co_run requires max_steps > 0). */
+int co_nccl_unique_id(uint8_t* out /* 128 bytes */);
+int co_attach_nccl(co_engine* eng, const uint8_t* uid, int32_t nranks, int32_t rank);
+/* last all-reduced totals {free_tokens, reserved_blocks_current} and how
+ * many all-reduces were enqueued */
+int co_global_reserve(co_engine* eng, int64_t* out /* 2 */, int64_t* calls);
 /* pinned-memory cudaMemcpyAsync bandwidth of this GPU's host link (GB/s) */
 int co_host_link_gbs(int64_t bytes, double* d2h, double* h2d);
 /* kvc.py:336-375 BlockPool.check_invariants on the device; CO_EDEVICE on

@@ -80,7 +80,7 @@ EXPORTS = (
     "co_drain_events", "co_pending_events", "co_drain_samples", "co_read_token_times",
     "co_check_invariants", "co_last_device_ms", "co_kernels_per_step", "co_time_steps", "co_last_error",
     "co_version", "co_read_block_tables", "co_data_stats", "co_kv_verify", "co_read_decode", "co_host_link_gbs",
-    "co_set_decode", "co_swap_bench",
+    "co_set_decode", "co_swap_bench", "co_nccl_unique_id", "co_attach_nccl", "co_global_reserve",
 )
 
 _lib = None
@@ -123,6 +123,9 @@ def load() -> C.CDLL:
         "co_host_link_gbs": (C.c_int, [C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "co_set_decode": (C.c_int, [V, C.c_int32]),
         "co_swap_bench": (C.c_int, [V, C.c_int64, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+        "co_nccl_unique_id": (C.c_int, [U8P]),
+        "co_attach_nccl": (C.c_int, [V, U8P, C.c_int32, C.c_int32]),
+        "co_global_reserve": (C.c_int, [V, I64P, I64P]),
         "co_last_error": (C.c_char_p, []),
         "co_version": (C.c_char_p, []),
     }

@@ -10,6 +10,7 @@
 // done or paused (an append buffer needs draining), so no host round trip is
 // needed inside a launch.
 #include <cub/device/device_radix_sort.cuh>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -46,6 +47,14 @@ static int fail(int code, const std::string& msg) {
 __global__ void k_preempt_one(Dev d, int32_t i, int32_t strat, int64_t now, int32_t cause) {
     if (threadIdx.x == 0 && blockIdx.x == 0) do_preempt(d, i, strat, now, cause);
 }
+// N4: this instance's [free_tokens, reserved_blocks_current] (kvc.py:92-98,
+// :79) into the all-reduce send buffer, every step whether or not it ran
+__global__ void k_reserve_pack(Dev d, int64_t* send) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        send[0] = free_tokens(d);
+        send[1] = d.ctl->rsv_cur;
+    }
+}
 __global__ void k_reset_drained(Dev d, int64_t ev, int64_t mem, int64_t smp) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         d.ctl->ev_count -= ev;
@@ -75,6 +84,12 @@ struct co_engine {
     int64_t n_chunks = 0;
     int sms = 148;
     void* host_pool = nullptr;
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    int64_t* red = nullptr;  // [send 2][recv 2]
+    int64_t reduce_calls = 0;
     int64_t page_bytes = 0;
     std::vector<co_event> st_events;   // host staging of drained device events
     std::vector<int32_t> st_members;
@@ -132,6 +147,16 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
     if (ev) mark(ev[5], s);
     k_check<<<1, NT, 0, s>>>(d, 0);
     if (ev) mark(ev[6], s);
+    if (E->comm) {
+        // global reserve telemetry: overlaps the data plane on a side stream
+        cudaEventRecord(E->fork, s);
+        cudaStreamWaitEvent(E->side, E->fork, 0);
+        k_reserve_pack<<<1, 32, 0, E->side>>>(d, E->red);
+        ncclResult_t nr = ncclAllReduce(E->red, E->red + 2, 2, ncclInt64, ncclSum, E->comm, E->side);
+        if (nr != ncclSuccess) return fail(CO_ECUDA, std::string("ncclAllReduce: ") + ncclGetErrorString(nr));
+        cudaEventRecord(E->join, E->side);
+        E->reduce_calls++;
+    }
     if (d.dp.on) {
         k_data<<<E->sms, 512, 0, s>>>(d, d.dp, d.dctl, 0);
         if (ev) mark(ev[7], s);
@@ -144,6 +169,7 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
         mark(ev[7], s);
         mark(ev[8], s);
     }
+    if (E->comm) cudaStreamWaitEvent(s, E->join, 0);
     return CO_OK;
 }
 
@@ -205,6 +231,11 @@ const char* co_version(void) { return "cacheopt-b200 0.1 (sm_100a)"; }
 int co_destroy(co_engine* E) {
     if (!E) return CO_OK;
     if (E->graph) cudaGraphExecDestroy(E->graph);
+    if (E->comm) ncclCommDestroy(E->comm);
+    if (E->side) cudaStreamDestroy(E->side);
+    if (E->fork) cudaEventDestroy(E->fork);
+    if (E->join) cudaEventDestroy(E->join);
+    if (E->red) cudaFree(E->red);
     for (void* p : E->allocs) cudaFree(p);
     if (E->cub_tmp) cudaFree(E->cub_tmp);
     if (E->host_pool) cudaFreeHost(E->host_pool);
@@ -517,6 +548,8 @@ int co_step(co_engine* E, int32_t* result) {
 
 int co_run(co_engine* E, int64_t max_steps, int32_t K, int64_t* steps_done) {
     if (!E) return fail(CO_EINVAL, "null argument");
+    if (E->comm && max_steps <= 0)
+        return fail(CO_EINVAL, "with a communicator every rank must run the same fixed number of steps");
     if (K < 1) K = 1;
     int r = sync_ctl(E);
     if (r) return r;
@@ -554,7 +587,7 @@ int co_run(co_engine* E, int64_t max_steps, int32_t K, int64_t* steps_done) {
             if ((r = drain_device(E))) return r;
             continue;
         }
-        if (E->h_ctl->done) break;
+        if (E->h_ctl->done && !(E->comm && max_steps > 0)) break;
     }
     E->last_ms = total_ms;
     if (steps_done) *steps_done = E->h_ctl->steps - steps0;
@@ -900,6 +933,43 @@ int co_swap_bench(co_engine* E, int64_t ntok, int32_t iters, double* out_ms, dou
     CK(cudaStreamSynchronize(E->stream));
     *out_ms = t_out / iters;
     *in_ms = t_in / iters;
+    return CO_OK;
+}
+
+int co_nccl_unique_id(uint8_t* out) {
+    if (!out) return fail(CO_EINVAL, "null argument");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return fail(CO_ECUDA, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    std::memcpy(out, id.internal, NCCL_UNIQUE_ID_BYTES);
+    return CO_OK;
+}
+
+int co_attach_nccl(co_engine* E, const uint8_t* uid, int32_t nranks, int32_t rank) {
+    if (!E || !uid || nranks < 1 || rank < 0 || rank >= nranks) return fail(CO_EINVAL, "bad arguments");
+    if (E->comm) return fail(CO_EINVAL, "already attached");
+    ncclUniqueId id;
+    std::memcpy(id.internal, uid, NCCL_UNIQUE_ID_BYTES);
+    cudaSetDevice(E->device);
+    ncclResult_t r = ncclCommInitRank(&E->comm, nranks, id, rank);
+    if (r != ncclSuccess) { E->comm = nullptr; return fail(CO_ECUDA, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)); }
+    CK(cudaStreamCreateWithFlags(&E->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&E->fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&E->join, cudaEventDisableTiming));
+    CK(cudaMalloc(&E->red, 4 * sizeof(int64_t)));
+    CK(cudaMemset(E->red, 0, 4 * sizeof(int64_t)));
+    E->nranks = nranks;
+    E->rank = rank;
+    if (E->graph) { cudaGraphExecDestroy(E->graph); E->graph = nullptr; }  // recapture with the collective
+    return CO_OK;
+}
+
+int co_global_reserve(co_engine* E, int64_t* out, int64_t* calls) {
+    if (!E || !out) return fail(CO_EINVAL, "null argument");
+    if (!E->comm) return fail(CO_EINVAL, "no communicator attached");
+    CK(cudaStreamSynchronize(E->side));
+    CK(cudaMemcpy(out, E->red + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (calls) *calls = E->reduce_calls;
     return CO_OK;
 }
 

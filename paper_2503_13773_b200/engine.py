@@ -415,6 +415,19 @@ class Engine:
                 "decode_member_steps", "decode_ctx_tokens")
         return dict(zip(keys, (int(v) for v in st)))
 
+    # -- N4 global reserve telemetry ---------------------------------------------
+
+    def attach_nccl(self, uid: bytes, nranks: int, rank: int) -> None:
+        buf = (C.c_uint8 * len(uid)).from_buffer_copy(uid)
+        N.check(self._lib.co_attach_nccl(self._h, buf, nranks, rank), "co_attach_nccl")
+
+    def global_reserve(self) -> Tuple[int, int, int]:
+        """(sum of free_tokens, sum of reserved_blocks_current, all-reduce calls)."""
+        out = np.zeros(2, dtype=np.int64)
+        calls = C.c_int64()
+        N.check(self._lib.co_global_reserve(self._h, _ptr(out, C.c_int64), C.byref(calls)), "co_global_reserve")
+        return int(out[0]), int(out[1]), int(calls.value)
+
     def set_decode(self, on: bool) -> None:
         N.check(self._lib.co_set_decode(self._h, int(on)), "co_set_decode")
 
