@@ -27,6 +27,8 @@
 #include "planner.cuh"
 #include "apply.cuh"
 #include "data_plane.cuh"
+#include "decode_tc.cuh"
+#include <cudaTypedefs.h>
 
 using namespace co;
 
@@ -90,6 +92,8 @@ struct co_engine {
     cudaEvent_t fork = nullptr, join = nullptr;
     int64_t* red = nullptr;  // [send 2][recv 2]
     int64_t reduce_calls = 0;
+    CUtensorMap kvmap;
+    bool tc_decode = false;
     int64_t page_bytes = 0;
     std::vector<co_event> st_events;   // host staging of drained device events
     std::vector<int32_t> st_members;
@@ -161,7 +165,10 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
         k_data<<<E->sms, 512, 0, s>>>(d, d.dp, d.dctl, 0);
         if (ev) mark(ev[7], s);
         if (d.dp.decode_on) {
-            k_decode<<<E->sms * 8, DEC_T, 0, s>>>(d, d.dp, d.dctl);
+            if (E->tc_decode)
+                k_decode_tc<<<E->sms, TC_WARPS * 32, TC_SMEM, s>>>(d, d.dp, d.dctl, E->kvmap);
+            else
+                k_decode<<<E->sms * 8, DEC_T, 0, s>>>(d, d.dp, d.dctl);
             k_decode_reduce<<<E->sms * 8, 128, 0, s>>>(d, d.dp, d.dctl);
         }
         if (ev) mark(ev[8], s);
@@ -428,6 +435,27 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
         }
         AL(x.gbar, 2);
         E->page_bytes = page_bytes;
+        const int bs = cfg->block_size;
+        if (x.decode_on && (16 % bs == 0 || bs % 16 == 0)) {
+            // TMA view of the pool: [n_pages * rows * bs][128] bf16, 128B-swizzled boxes
+            void* fn = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+                co_destroy(E);
+                return fail(CO_ECUDA, "cuTensorMapEncodeTiled unavailable");
+            }
+            cuuint64_t gdim[2] = {(cuuint64_t)x.D, (cuuint64_t)n_pages * x.rows * bs};
+            cuuint64_t gstride[1] = {(cuuint64_t)x.D * 2};
+            cuuint32_t box[2] = {64, (cuuint32_t)(bs < 16 ? bs : 16)};
+            cuuint32_t estride[2] = {1, 1};
+            CUresult cr = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn)(
+                &E->kvmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x.kv, gdim, gstride, box, estride,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (cr != CUDA_SUCCESS) { co_destroy(E); return fail(CO_ECUDA, "tensor map encode failed"); }
+            cudaFuncSetAttribute(k_decode_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+            E->tc_decode = true;
+        }
     }
     AL(d.l_tri_key, n); AL(d.am_rhi, n3); AL(d.am_rlo, n3); AL(d.rank_to_idx, n);
     AL(d.sk0, n3); AL(d.sk1, n3); AL(d.sk2, n3); AL(d.sk_item, n3);
@@ -465,6 +493,7 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     memset_all(d.dctl, 0, sizeof(DataCtl));
     if (d.dp.on) {
         memset_all(d.dp.gbar, 0, 8);
+        memset_all(d.dp.kv, 0, (size_t)d.n_pages * d.dp.page_elems * 2);
         memset_all(d.dp.hsaved, 0, n4);
         std::vector<int32_t> hs(d.dp.h_pages);
         for (int32_t k = 0; k < d.dp.h_pages; k++) hs[k] = d.dp.h_pages - 1 - k;
