@@ -1,11 +1,11 @@
 // N3 paged decode on tensor cores.
 //
 // Work item = (decode member, layer, kv head, split of `split` tokens), one
-// WARP per item (4 independent warps per CTA).  The KV pool is addressed by
+// WARP per item (8 independent warps per CTA).  The KV pool is addressed by
 // TMA as a 2-D tensor [n_pages * rows * bs][128] bf16: a 16-position tile of
 // one (layer, K|V, kv head) is 1 box of 16 rows (bs >= 16) or 16/bs boxes of
 // bs rows, split into two 64-column halves, 128B-swizzled.  Each warp runs a
-// 4-stage mbarrier pipeline of K+V tiles (8 KB per stage); the G query heads
+// 3-stage mbarrier pipeline of K+V tiles (8 KB per stage); the G query heads
 // that share the KV head are the M rows (padded to 16) of
 //   S = Q K^T   (mma.sync m16n8k16 bf16 -> fp32, 16 per tile)
 //   O += P V    (16 per tile; P re-packed from S's accumulator fragments)
@@ -17,8 +17,8 @@
 
 namespace co {
 
-constexpr int TC_WARPS = 4;
-constexpr int TC_STAGES = 4;
+constexpr int TC_WARPS = 8;
+constexpr int TC_STAGES = 3;
 constexpr int TC_TILE_BYTES = 16 * 128 * 2;                 // one K or V tile
 constexpr int TC_STAGE_BYTES = 2 * TC_TILE_BYTES;           // K + V
 constexpr int TC_SMEM = TC_WARPS * TC_STAGES * TC_STAGE_BYTES + 1024 + TC_WARPS * TC_STAGES * 8;
