@@ -12,6 +12,36 @@
 
 namespace co {
 
+// kvc.py:336-375 check_invariants over every record (validate_every)
+__device__ void check_pool(const Dev& d, BlkShared& sb) {
+    Ctl& c = *d.ctl;
+    int64_t fp = 0, bad = 0;
+    for (int32_t i = threadIdx.x; i < d.n; i += NT) {
+        if (!d.holds[i]) continue;
+        if (d.host[i] < 0) fp += fp_tokens(d.granted[i], d.bs);
+        if (d.used[i] > d.granted[i]) bad |= 1;
+        int32_t h = d.host[i];
+        if (h >= 0) {
+            if (d.guest[i] >= 0) bad |= 2;
+            if (!d.holds[h] || d.guest[h] != i) bad |= 4;
+            else if (d.off[i] < 0 || (int64_t)d.off[i] + d.granted[i] > d.granted[h]) bad |= 8;
+        } else if (d.tab_len[i] * (int64_t)d.bs != fp_tokens(d.granted[i], d.bs)) {
+            bad |= 32;  // N1: the table covers exactly the footprint
+        }
+        int32_t g = d.guest[i];
+        if (g >= 0 && d.off[g] < d.used[i]) bad |= 16;
+    }
+    fp = blk_sum(fp, sb);
+    bad = blk_sum(bad ? 1 : 0, sb);
+    if (threadIdx.x == 0) {
+        if (fp != c.fp_sum) bad += 1;
+        if (free_tokens(d) < 0) bad += 1;
+        if (c.rsv_cur < 0 || c.rsv_cur > d.rsv_target) bad += 1;
+        if ((int64_t)c.free_top * d.bs != (int64_t)d.n_pages * d.bs - c.fp_sum) bad += 1;
+        if (bad) { c.error = 4; c.done = 1; }
+    }
+}
+
 struct ApplySh {
     BlkShared b;
     int64_t batch, end;
@@ -67,37 +97,92 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
             int32_t i = d.l_acted[k];
             if (d.state[i] == ST_PREEMPTED) do_readmit(d, i);
         }
-        // member filter (engine.py:500-531)
-        int32_t ns = 0;
-        int64_t batch = 0;
-        for (int32_t m = 0; m < P.n_mem; m++) {
-            const int32_t i = d.mem_idx[m];
-            const int32_t tok = d.mem_tok[m];
-            if (d.st_failed[i] == sid || d.st_seen[i] == sid) continue;
-            d.st_seen[i] = sid;
-            int8_t s = d.state[i];
-            if (!live_state(s)) continue;
-            if (s == ST_WAITING) {
-                if (!d.holds[i] || d.granted[i] < d.prefill[i] + tok) continue;
-                d.state[i] = ST_RUNNING;
-                if (d.first_start[i] < 0) {
-                    d.first_start[i] = now;
-                    emit_event(d, CO_EV_ADMIT, i, now);
+        S.n_acted = n_acted;
+    }
+    __syncthreads();
+
+    // ---- member filter (engine.py:500-531), block-parallel ------------------
+    // A position is examined iff its request is not failed and it is the
+    // request's first position (the reference's `seen`); each examined member's
+    // outcome depends only on its own post-action state, and admit events and
+    // survivors keep member order through ordered compactions.
+    const int32_t nm = P.n_mem;
+    const uint64_t stamp = (uint64_t)(uint32_t)sid << 24;
+    for (int32_t m = tid; m < nm; m += NT) atomicMax((unsigned long long*)&d.seen64[d.mem_idx[m]],
+                                                      (unsigned long long)(stamp | (0xFFFFFFu - (uint32_t)m)));
+    __syncthreads();
+    for (int32_t m = tid; m < nm; m += NT) {
+        const int32_t i = d.mem_idx[m];
+        const int32_t tok = d.mem_tok[m];
+        int32_t f = 0;  // bit0 survive, bit1 admit event
+        if (d.st_failed[i] != sid && d.seen64[i] == (stamp | (0xFFFFFFu - (uint32_t)m))) {
+            const int8_t st = d.state[i];
+            bool go = live_state(st);
+            if (go && st == ST_WAITING) {
+                if (!d.holds[i] || d.granted[i] < d.prefill[i] + tok) {
+                    go = false;
+                } else {
+                    f |= 4;  // becomes RUNNING
+                    if (d.first_start[i] < 0) f |= 2;
                 }
-            } else if (s != ST_RUNNING) {
-                continue;
+            } else if (go && st != ST_RUNNING) {
+                go = false;
             }
-            if (d.ready_at[i] > now) continue;
-            if (d.prefill[i] >= d.kv_need[i]) {
-                if (eff_of(d, i) < d.used[i] + 1) continue;
-            } else if (d.granted[i] < d.prefill[i] + tok) {
-                continue;
+            if (go && d.ready_at[i] > now) go = false;
+            if (go) {
+                if (d.prefill[i] >= d.kv_need[i]) {
+                    if (eff_of(d, i) < d.used[i] + 1) go = false;
+                } else if (d.granted[i] < d.prefill[i] + tok) {
+                    go = false;
+                }
             }
-            d.l_surv_idx[ns] = i;
-            d.l_surv_tok[ns] = tok;
-            ns++;
-            batch += tok;
+            if (go) f |= 1;
         }
+        d.l_mflag[m] = f;
+    }
+    __syncthreads();
+    for (int32_t m = tid; m < nm; m += NT) {
+        const int32_t f = d.l_mflag[m];
+        if (f & 4) {
+            const int32_t i = d.mem_idx[m];
+            d.state[i] = ST_RUNNING;
+            if (f & 2) d.first_start[i] = now;
+        }
+    }
+    int32_t n_admit = 0;
+    if (d.record_events) {
+        const int64_t ev_base = c.ev_count;
+        int32_t base = 0;
+        for (int32_t c0 = 0; c0 < nm; c0 += NT) {
+            const int32_t m = c0 + tid;
+            const int32_t fl = (m < nm && (d.l_mflag[m] & 2)) ? 1 : 0;
+            int32_t tot;
+            const int32_t p = blk_excl_scan(fl, &tot, S.b);
+            if (fl) {
+                co_event e;
+                e.kind = CO_EV_ADMIT; e.idx = d.mem_idx[m]; e.t = now; e.a = e.b = e.c = 0;
+                d.events[ev_base + base + p] = e;
+            }
+            base += tot;
+        }
+        n_admit = base;
+    }
+    // survivors in member order: positions first, then (idx, tokens)
+    const int32_t ns0 = blk_compact(nullptr, nm, d.l_surv_tok, [&](int32_t m) { return (d.l_mflag[m] & 1) != 0; }, S.b);
+    int64_t bsum = 0;
+    for (int32_t k = tid; k < ns0; k += NT) bsum += d.mem_tok[d.l_surv_tok[k]];
+    bsum = blk_sum(bsum, S.b);
+    for (int32_t k = tid; k < ns0; k += NT) {
+        const int32_t m = d.l_surv_tok[k];
+        d.l_surv_idx[k] = d.mem_idx[m];
+    }
+    __syncthreads();
+    for (int32_t k = tid; k < ns0; k += NT) d.l_surv_tok[k] = d.mem_tok[d.l_surv_tok[k]];  // position -> tokens
+    __syncthreads();
+    if (tid == 0) {
+        const int32_t ns = ns0;
+        const int64_t batch = bsum;
+        c.ev_count += n_admit;
         // claims (engine.py:533-535): setdefault(provider, waiter)
         for (int32_t k = 0; k < P.n_cl; k++) {
             int32_t w = d.cl_w[k], p = d.cl_p[k];
@@ -277,35 +362,13 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
         c.now = end;
         c.last_result = 1;
     }
+    __syncthreads();
+    if (c.check_due) check_pool(d, S.b);
 }
 
-// kvc.py:336-375 check_invariants over every record (debug / validate_every)
-__global__ void __launch_bounds__(NT, 1) k_check(Dev d, int32_t force) {
+__global__ void __launch_bounds__(NT, 1) k_check(Dev d) {
     __shared__ BlkShared sb;
-    Ctl& c = *d.ctl;
-    if (!force && !(c.active && c.check_due)) return;
-    int64_t fp = 0, bad = 0;
-    for (int32_t i = threadIdx.x; i < d.n; i += NT) {
-        if (!d.holds[i]) continue;
-        if (d.host[i] < 0) fp += fp_tokens(d.granted[i], d.bs);
-        if (d.used[i] > d.granted[i]) bad |= 1;
-        int32_t h = d.host[i];
-        if (h >= 0) {
-            if (d.guest[i] >= 0) bad |= 2;
-            if (!d.holds[h] || d.guest[h] != i) bad |= 4;
-            else if (d.off[i] < 0 || (int64_t)d.off[i] + d.granted[i] > d.granted[h]) bad |= 8;
-        }
-        int32_t g = d.guest[i];
-        if (g >= 0 && d.off[g] < d.used[i]) bad |= 16;
-    }
-    fp = blk_sum(fp, sb);
-    bad = blk_sum(bad ? 1 : 0, sb);
-    if (threadIdx.x == 0) {
-        if (fp != c.fp_sum) bad += 1;
-        if (free_tokens(d) < 0) bad += 1;
-        if (c.rsv_cur < 0 || c.rsv_cur > d.rsv_target) bad += 1;
-        if (bad) { c.error = 4; c.done = 1; }
-    }
+    check_pool(d, sb);
 }
 
 }  // namespace co

@@ -136,21 +136,19 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
     cudaStream_t s = E->stream;
     if (ev) mark(ev[0], s);
     k_begin<<<1, 32, 0, s>>>(d, guard);
-    k_admit<<<E->grid, 256, 0, s>>>(d);
     if (ev) mark(ev[1], s);
     k_classify<<<E->grid, 256, 0, s>>>(d);
     if (ev) mark(ev[2], s);
     size_t bytes = E->cub_bytes;
     cudaError_t e = cub::DeviceRadixSort::SortPairs(E->cub_tmp, bytes, d.keys_in, d.keys_out, d.vals_in,
-                                                    d.vals_out, (int)E->n, 0, 64, s);
+                                                    d.vals_out, (int)E->n, 0, d.key_bits, s);
     if (e != cudaSuccess) return fail(CO_ECUDA, std::string("radix sort: ") + cudaGetErrorString(e));
     if (ev) mark(ev[3], s);
     k_plan<<<1, NT, 0, s>>>(d);
     if (ev) mark(ev[4], s);
     k_apply<<<1, NT, 0, s>>>(d);
     if (ev) mark(ev[5], s);
-    k_check<<<1, NT, 0, s>>>(d, 0);
-    if (ev) mark(ev[6], s);
+    if (ev) mark(ev[6], s);  // (the validate_every check runs inside k_apply)
     if (E->comm) {
         // global reserve telemetry: overlaps the data plane on a side stream
         cudaEventRecord(E->fork, s);
@@ -317,10 +315,12 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     // composite classify key: [class:2][flag:1][time:61-idbits][idrank:idbits]
     int idbits = 1;
     while ((1ll << idbits) < n) idbits++;
-    const int timebits = 61 - idbits;
     double max_iter_ms = cfg->iter_base_ms + cfg->iter_per_token_ms * (double)tot_tokens;
     double bound = std::max((double)maxD, (double)horizon + max_iter_ms * 1000.0 + 2.0 + (double)max_tbt_slo);
+    int timebits = 1;
+    while (timebits < 61 - idbits && std::ldexp(1.0, timebits) <= bound) timebits++;
     if (bound >= std::ldexp(1.0, timebits)) return fail(CO_EINVAL, "trace time range exceeds the sort-key budget");
+    const int key_bits = 3 + timebits + idbits;  // class(2) | blown(1) | time | id rank
 
     co_engine* E = new co_engine();
     E->n = n;
@@ -348,7 +348,7 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     d.n = (int32_t)n; d.bs = cfg->block_size; d.B = cfg->block_size; d.buffer_b = cfg->buffer_b;
     d.token_budget = cfg->token_budget; d.prealloc_m = cfg->preallocate_m; d.runway_iters = cfg->decode_runway_iters;
     d.fcfs = cfg->victim_rule_fcfs; d.record_events = cfg->record_events; d.validate_every = cfg->validate_every;
-    d.pad = cfg->padding; d.idbits = idbits; d.n_edges = cfg->n_slo_edges; d.token_step = cfg->token_step;
+    d.pad = cfg->padding; d.idbits = idbits; d.key_bits = key_bits; d.n_edges = cfg->n_slo_edges; d.token_step = cfg->token_step;
     d.rsv_target = cfg->reserved_blocks; d.eps = cfg->epsilon_us; d.capacity = cfg->capacity_tokens;
     d.s_star = cfg->s_star; d.s_max = lu->s_max;
     for (int k = 0; k < CO_MAX_SLO_EDGES; k++) d.edges[k] = k < cfg->n_slo_edges ? cfg->slo_edges_us[k] : 0;
@@ -383,7 +383,7 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     d.dir_w = dir_w;
     E->n_chunks = n_chunks;
     AL(d.st_nr, n); AL(d.st_crit, n); AL(d.st_removed, n); AL(d.st_embedded, n); AL(d.st_resumed, n);
-    AL(d.st_stalled, n); AL(d.st_parts, n); AL(d.st_claimed, n); AL(d.st_failed, n); AL(d.st_seen, n);
+    AL(d.st_stalled, n); AL(d.st_parts, n); AL(d.st_claimed, n); AL(d.st_failed, n); AL(d.seen64, n);
     AL(d.st_acted, n); AL(d.st_deferred, n);
     AL(d.keys_in, n); AL(d.keys_out, n); AL(d.vals_in, n); AL(d.vals_out, n);
     AL(d.plan, 1);
@@ -394,7 +394,7 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     AL(d.l_defer, n); AL(d.l_pro, n); AL(d.l_ful, n); AL(d.l_part, n3); AL(d.l_part_need, n3);
     AL(d.l_part_grant, n3); AL(d.l_mready, n2); AL(d.l_gm_idx, n); AL(d.l_gm_tok, n); AL(d.l_acted, n3);
     AL(d.l_surv_idx, n3); AL(d.l_surv_tok, n3); AL(d.l_done, n3); AL(d.l_coll, n); AL(d.l_grp, 2 * n3);
-    AL(d.l_fill_t0, n3); AL(d.l_fill_n, n3);
+    AL(d.l_fill_t0, n3); AL(d.l_fill_n, n3); AL(d.l_mflag, n3);
     AL(d.dctl, 1);
     std::memset(&d.dp, 0, sizeof(d.dp));
     if (cfg->kv_layers > 0) {
@@ -485,11 +485,12 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
         memset_all(p, 0, n4);
     for (int32_t* p : {d.host, d.guest, d.claim_w}) memset_all(p, 0xff, n4);
     for (int32_t* p : {d.st_nr, d.st_crit, d.st_removed, d.st_embedded, d.st_resumed, d.st_stalled, d.st_parts,
-                       d.st_claimed, d.st_failed, d.st_seen, d.st_acted, d.st_deferred})
+                       d.st_claimed, d.st_failed, d.st_acted, d.st_deferred})
         memset_all(p, 0, n4);
     for (int64_t* p : {d.max_tbt, d.ready_at, d.pstart, d.swap_done, d.ptime, d.rec_seq}) memset_all(p, 0, n8);
     for (int64_t* p : {d.first_tok, d.last_tok, d.first_start, d.completion}) memset_all(p, 0xff, n8);
     memset_all(d.holds, 0, n);
+    memset_all(d.seen64, 0, n8);
     memset_all(d.dctl, 0, sizeof(DataCtl));
     if (d.dp.on) {
         memset_all(d.dp.gbar, 0, 8);
@@ -526,8 +527,8 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
         return fail(CO_ECUDA, "ctl upload");
     }
     size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, d.keys_in, d.keys_out, d.vals_in, d.vals_out, (int)n, 0, 64,
-                                    E->stream);
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, d.keys_in, d.keys_out, d.vals_in, d.vals_out, (int)n, 0,
+                                    key_bits, E->stream);
     E->cub_bytes = std::max<size_t>(bytes, 256);
     if (cudaMalloc(&E->cub_tmp, E->cub_bytes) != cudaSuccess) { co_destroy(E); return fail(CO_ECUDA, "cub temp"); }
     cudaError_t e = cudaStreamSynchronize(E->stream);
@@ -740,7 +741,7 @@ int co_read_token_times(co_engine* E, int64_t* offsets, int64_t* times) {
 
 int co_check_invariants(co_engine* E) {
     if (!E) return fail(CO_EINVAL, "null argument");
-    k_check<<<1, NT, 0, E->stream>>>(E->d, 1);
+    k_check<<<1, NT, 0, E->stream>>>(E->d);
     CK(cudaGetLastError());
     int r = sync_ctl(E);
     if (r) return r;
@@ -1004,7 +1005,7 @@ int co_global_reserve(co_engine* E, int64_t* out, int64_t* calls) {
 
 int co_kernels_per_step(co_engine* E, int32_t* n) {
     if (!E || !n) return fail(CO_EINVAL, "null argument");
-    *n = 7;  // begin, admit, classify, sort (counted as one stage), plan, apply, check
+    *n = 4;  // begin, classify(+admit), plan, apply(+check); plus the CUB sort passes
     return CO_OK;
 }
 

@@ -49,6 +49,7 @@ struct Dev {
     // configuration (co_config + derived)
     int32_t n, bs, B, buffer_b, token_budget, prealloc_m, runway_iters, fcfs;
     int32_t record_events, validate_every, pad, idbits, n_edges, token_step, rsv_target;
+    int32_t key_bits;            // composite sort key width: class(2) | blown(1) | time | idrank
     int64_t eps, capacity, s_star, s_max, ev_cap, mem_cap, sample_cap;
     int64_t edges[CO_MAX_SLO_EDGES];
     double base_ms, per_token_ms;
@@ -85,7 +86,8 @@ struct Dev {
     int32_t *claim_w, *claim_ep, *epoch;
     // per-step membership stamps (compared with Ctl::sid, never cleared)
     int32_t *st_nr, *st_crit, *st_removed, *st_embedded, *st_resumed, *st_stalled, *st_parts,
-        *st_claimed, *st_failed, *st_seen, *st_acted, *st_deferred;
+        *st_claimed, *st_failed, *st_acted, *st_deferred;
+    uint64_t* seen64;            // member-filter first occurrence: (sid << 24) | (2^24-1-pos)
     // classify + sort
     uint64_t *keys_in, *keys_out;
     uint32_t *vals_in, *vals_out;
@@ -96,7 +98,7 @@ struct Dev {
     // planner / apply scratch (n-sized unless noted)
     int32_t *l_nr, *l_nrp, *l_pend, *l_tri, *l_tri_taken, *l_vict, *l_defer, *l_pro, *l_ful,
         *l_part, *l_part_need, *l_part_grant, *l_mready, *l_gm_idx, *l_gm_tok, *l_acted,
-        *l_surv_idx, *l_surv_tok, *l_done, *l_coll, *l_grp, *l_fill_t0, *l_fill_n;
+        *l_surv_idx, *l_surv_tok, *l_done, *l_coll, *l_grp, *l_fill_t0, *l_fill_n, *l_mflag;
     int64_t* l_tri_key;
     uint64_t *am_rhi, *am_rlo;   // amortize remainders (128-bit), by participant position
     int32_t* rank_to_idx;        // inverse of idrank

@@ -71,31 +71,26 @@ __global__ void k_begin(Dev d, int32_t guard) {
     c.active = 1;
 }
 
-__global__ void k_admit(Dev d) {
-    const Ctl& c = *d.ctl;
-    if (!c.active) return;
-    const int32_t lo = c.adm_lo, hi = c.adm_hi;
-    const int64_t ev0 = c.ev_count - (hi - lo);
-    for (int32_t i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += gridDim.x * blockDim.x) {
-        // estimation.py:92-99 + 122-128 with the host-drawn noise
-        int32_t t = d.tout[i];
-        int32_t p = t - d.err[i];
-        if (p < 1) p = 1;
-        bool under = t >= p;
-        if (d.flip[i]) under = !under;
-        int32_t e = under ? p + d.pad : (p - d.pad > 1 ? p - d.pad : 1);
-        d.pred[i] = p;
-        d.est[i] = e;
-        d.state[i] = ST_WAITING;
-        if (d.record_events) {
-            co_event ev;
-            ev.kind = CO_EV_ARRIVE; ev.idx = i; ev.t = d.arr[i]; ev.a = ev.b = ev.c = 0;
-            d.events[ev0 + (i - lo)] = ev;
-        }
+// estimation.py:92-99 + 122-128 with the host-drawn noise, and the arrive
+// event (engine.py:353); runs inside k_classify for the admission window
+__device__ __forceinline__ void admit_one(const Dev& d, int32_t i, int32_t lo, int64_t ev0) {
+    int32_t t = d.tout[i];
+    int32_t p = t - d.err[i];
+    if (p < 1) p = 1;
+    bool under = t >= p;
+    if (d.flip[i]) under = !under;
+    int32_t e = under ? p + d.pad : (p - d.pad > 1 ? p - d.pad : 1);
+    d.pred[i] = p;
+    d.est[i] = e;
+    d.state[i] = ST_WAITING;
+    if (d.record_events) {
+        co_event ev;
+        ev.kind = CO_EV_ARRIVE; ev.idx = i; ev.t = d.arr[i]; ev.a = ev.b = ev.c = 0;
+        d.events[ev0 + (i - lo)] = ev;
     }
 }
 
-// class codes in the top two key bits
+// class codes in the top two key bits: [class:2][blown:1][time][id rank]
 constexpr uint64_t K_NW = 0, K_NWP = 1, K_RUN = 2;
 
 __global__ void k_classify(Dev d) {
@@ -103,10 +98,14 @@ __global__ void k_classify(Dev d) {
     if (!c.active) return;
     const int64_t now = c.now, ti = c.t_i, eps = d.eps;
     const int ib = d.idbits;
+    const int cs = d.key_bits - 2, fs = d.key_bits - 3;  // class / blown-flag bit positions
     int32_t cw = 0, cwp = 0, cr = 0;
     const int32_t hi_live = c.next_pending;
+    const int32_t alo = c.adm_lo, ahi = c.adm_hi;
+    const int64_t ev0 = c.ev_count - (ahi - alo);
     for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < d.n; i += gridDim.x * blockDim.x) {
         uint64_t key = ~0ull;
+        if (i >= alo && i < ahi) admit_one(d, i, alo, ev0);
         if (i < hi_live) {
             int8_t s = d.state[i];
             if (s == ST_WAITING || s == ST_PREEMPTED) {
@@ -115,17 +114,17 @@ __global__ void k_classify(Dev d) {
                 int64_t rt = D - now;
                 uint64_t id = (uint64_t)d.idrank[i];
                 if (rt >= -eps && rt - ti < eps) {
-                    key = (K_NW << 62) | ((uint64_t)D << ib) | id;
+                    key = (K_NW << cs) | ((uint64_t)D << ib) | id;
                     cw++;
                 } else {
                     // queue_key (scheduler.py:151-157): (0, rt, id) / (1, arrival, id)
                     uint64_t flag = rt < 0 ? 1 : 0;
                     uint64_t v = flag ? (uint64_t)d.arr[i] : (uint64_t)D;
-                    key = (K_NWP << 62) | (flag << 61) | (v << ib) | id;
+                    key = (K_NWP << cs) | (flag << fs) | (v << ib) | id;
                     cwp++;
                 }
             } else if (s == ST_RUNNING) {
-                key = (K_RUN << 62) | (uint64_t)i;
+                key = (K_RUN << cs) | (uint64_t)i;
                 cr++;
             }
         }
