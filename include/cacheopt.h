@@ -248,6 +248,9 @@ int co_check_invariants(co_engine* eng);
 /* Device time of the last co_run/co_step launch sequence (CUDA events on
  * the engine stream), milliseconds. */
 int co_last_device_ms(co_engine* eng, double* ms);
+/* development aid: phase timestamps (ns) of the planner/apply kernels of
+ * the last step; enable = 1 allocates the stamp buffer */
+int co_phase_profile(co_engine* eng, int32_t enable, int64_t* out /* 64 */);
 /* Number of kernels one device step launches (for gpu_launches accounting). */
 int co_kernels_per_step(co_engine* eng, int32_t* n);
 

@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
     const int32_t n_nw = c.cnt_nw, n_nwp = c.cnt_nwp, n_run = c.cnt_run;
     const int32_t* RUN = reinterpret_cast<const int32_t*>(d.vals_out) + n_nw + n_nwp;
 
+    prof_mark(d, 32);
     if (tid == 0) {
         for (int32_t k = 0; k < P.n_pre; k++) do_preempt(d, d.pre_idx[k], d.pre_strat[k], now, CO_CAUSE_PLAN);
         int32_t n_acted = 0;
@@ -101,6 +102,7 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
     }
     __syncthreads();
 
+    prof_mark(d, 33);
     // ---- member filter (engine.py:500-531), block-parallel ------------------
     // A position is examined iff its request is not failed and it is the
     // request's first position (the reference's `seen`); each examined member's
@@ -225,6 +227,7 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
         return;
     }
 
+    prof_mark(d, 34);
     // ---- iteration charge and event (engine.py:627-633) -------------------
     const int32_t ns = S.n_surv;
     int64_t mem0 = 0;
@@ -250,6 +253,7 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
         }
     }
 
+    prof_mark(d, 35);
     // ---- emission (engine.py:553-571), members are distinct ---------------
     int64_t dused = 0, dgen = 0;
     for (int32_t k = tid; k < ns; k += NT) {
@@ -308,6 +312,7 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
     }
     __syncthreads();
 
+    prof_mark(d, 36);
     // ---- collisions (engine.py:573-591), hosts in record-creation order ----
     const int32_t n_coll = blk_compact(RUN, n_run, d.l_coll, [&](int32_t h) {
         if (d.state[h] != ST_RUNNING || !d.holds[h] || d.host[h] >= 0) return false;
@@ -363,6 +368,7 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
         c.last_result = 1;
     }
     __syncthreads();
+    prof_mark(d, 37);
     if (c.check_due) check_pool(d, S.b);
 }
 

@@ -13,8 +13,9 @@ struct BlkShared {
     uint64_t ured[32];
     int32_t scan[32];
     // rank-sort tile
-    static constexpr int TILE = 1024;
+    static constexpr int TILE = 512;
     uint64_t t0[TILE], t1[TILE], t2[TILE];
+    int32_t it[TILE];
 };
 
 __device__ __forceinline__ int64_t warp_sum64(int64_t v) {
@@ -120,6 +121,27 @@ __device__ int32_t blk_compact(const int32_t* src, int32_t m, int32_t* dst, Pred
 template <class KeyFn>
 __device__ void blk_sort(int32_t* items, int32_t m, KeyFn kf, const Dev& d, BlkShared& s) {
     if (m <= 1) return;
+    if (m <= BlkShared::TILE) {
+        // small set: keys and items live in shared memory, one rank per thread
+        for (int32_t k = threadIdx.x; k < m; k += NT) {
+            uint64_t a, b, c;
+            kf(items[k], a, b, c);
+            s.t0[k] = a; s.t1[k] = b; s.t2[k] = c;
+            s.it[k] = items[k];
+        }
+        __syncthreads();
+        for (int32_t k = threadIdx.x; k < m; k += NT) {
+            const uint64_t a0 = s.t0[k], b0 = s.t1[k], c0 = s.t2[k];
+            int32_t rank = 0;
+            for (int32_t j = 0; j < m; j++) {
+                const uint64_t a = s.t0[j], b = s.t1[j], c = s.t2[j];
+                rank += (a < a0 || (a == a0 && (b < b0 || (b == b0 && c < c0)))) ? 1 : 0;
+            }
+            items[rank] = s.it[k];
+        }
+        __syncthreads();
+        return;
+    }
     for (int32_t k = threadIdx.x; k < m; k += NT) {
         uint64_t a, b, c;
         kf(items[k], a, b, c);

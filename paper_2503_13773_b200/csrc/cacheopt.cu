@@ -144,7 +144,7 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
                                                     d.vals_out, (int)E->n, 0, d.key_bits, s);
     if (e != cudaSuccess) return fail(CO_ECUDA, std::string("radix sort: ") + cudaGetErrorString(e));
     if (ev) mark(ev[3], s);
-    k_plan<<<1, NT, 0, s>>>(d);
+    k_plan<<<1, NT, sizeof(PlanSh), s>>>(d);
     if (ev) mark(ev[4], s);
     k_apply<<<1, NT, 0, s>>>(d);
     if (ev) mark(ev[5], s);
@@ -241,6 +241,7 @@ int co_destroy(co_engine* E) {
     if (E->fork) cudaEventDestroy(E->fork);
     if (E->join) cudaEventDestroy(E->join);
     if (E->red) cudaFree(E->red);
+    if (E->d.prof) cudaFree(E->d.prof);
     for (void* p : E->allocs) cudaFree(p);
     if (E->cub_tmp) cudaFree(E->cub_tmp);
     if (E->host_pool) cudaFreeHost(E->host_pool);
@@ -531,6 +532,7 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
                                     key_bits, E->stream);
     E->cub_bytes = std::max<size_t>(bytes, 256);
     if (cudaMalloc(&E->cub_tmp, E->cub_bytes) != cudaSuccess) { co_destroy(E); return fail(CO_ECUDA, "cub temp"); }
+    cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PlanSh));
     cudaError_t e = cudaStreamSynchronize(E->stream);
     if (e != cudaSuccess) { co_destroy(E); return fail(CO_ECUDA, cudaGetErrorString(e)); }
     *out = E;
@@ -1000,6 +1002,21 @@ int co_global_reserve(co_engine* E, int64_t* out, int64_t* calls) {
     CK(cudaStreamSynchronize(E->side));
     CK(cudaMemcpy(out, E->red + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
     if (calls) *calls = E->reduce_calls;
+    return CO_OK;
+}
+
+// development aid: enable/read the %globaltimer phase stamps of k_plan/k_apply
+int co_phase_profile(co_engine* E, int32_t enable, int64_t* out /* 64 */) {
+    if (!E) return fail(CO_EINVAL, "null argument");
+    if (enable && !E->d.prof) {
+        CK(cudaMalloc(&E->d.prof, 64 * sizeof(int64_t)));
+        CK(cudaMemset(E->d.prof, 0, 64 * sizeof(int64_t)));
+        if (E->graph) { cudaGraphExecDestroy(E->graph); E->graph = nullptr; }
+    }
+    if (out && E->d.prof) {
+        CK(cudaMemcpyAsync(out, E->d.prof, 64 * sizeof(int64_t), cudaMemcpyDeviceToHost, E->stream));
+        CK(cudaStreamSynchronize(E->stream));
+    }
     return CO_OK;
 }
 

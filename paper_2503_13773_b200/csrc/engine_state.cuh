@@ -112,6 +112,7 @@ struct Dev {
     int32_t* members;   // (idx, tok) pairs
     int64_t* samples;   // (footprint, used) pairs
     Ctl* ctl;
+    int64_t* prof;   // optional phase timestamps (ns, %globaltimer), 64 slots per kernel
 };
 
 // ---------------------------------------------------------------------------
@@ -176,6 +177,13 @@ __device__ __forceinline__ int32_t strategy_of(const Dev& d, int i) {
 }
 __device__ __forceinline__ int64_t lut(const int64_t* t, int64_t s, int64_t smax) {
     return t[s < smax ? s : smax];
+}
+__device__ __forceinline__ void prof_mark(const Dev& d, int slot) {
+    if (d.prof && threadIdx.x == 0) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        d.prof[slot] = (int64_t)t;
+    }
 }
 // costmodel.py:51-55 iteration_latency in IEEE double, no contraction
 __device__ __forceinline__ double iter_ms(const Dev& d, int64_t tokens) {

@@ -11,8 +11,56 @@
 
 namespace co {
 
+// Planner view of one request (engine.py:284-317 fields the planner reads),
+// computed in parallel into shared memory so thread 0's ordered loops read
+// shared memory instead of chasing HBM.  The pool is not mutated while
+// planning, so a view stays valid for the whole plan.
+struct PV {
+    int32_t i, eff, target, er, kvn, pre, used, granted, pcount, pg, idrank, flags;
+    int64_t rt;
+};
+enum : int32_t { PV_HOLDS = 1, PV_GUEST = 2, PV_RETURNED = 4, PV_RUNNING = 8, PV_WAITING = 16 };
+constexpr int PV_CAP = 1024;
+struct FV {  // fulfilled provider candidate (scheduler.py:685-689, 711-716)
+    int64_t gain;
+    int32_t er, idrank, i, _pad;
+};
+constexpr int FV_CAP = 1024;
+
+__device__ __forceinline__ PV make_pv(const Dev& d, int32_t i, int64_t now) {
+    PV v;
+    v.i = i;
+    v.eff = eff_of(d, i);
+    v.er = est_rem(d, i);
+    v.kvn = d.kv_need[i];
+    v.pre = d.prefill[i];
+    v.used = d.used[i];
+    v.target = (v.used > v.kvn ? v.used : v.kvn) + v.er;
+    v.granted = d.holds[i] ? d.granted[i] : 0;
+    v.pcount = d.pcount[i];
+    v.pg = d.pred[i] - d.gen[i];
+    v.idrank = d.idrank[i];
+    const int8_t st = d.state[i];
+    v.flags = (d.holds[i] ? PV_HOLDS : 0) | (guest_of(d, i) ? PV_GUEST : 0) |
+              (st == ST_RUNNING ? PV_RUNNING : 0) | (st == ST_WAITING ? PV_WAITING : 0) |
+              ((st == ST_RUNNING && v.eff < v.used + 1) ? PV_RETURNED : 0);
+    v.rt = rt_of(d, i, now);
+    return v;
+}
+__device__ __forceinline__ int64_t pv_cost(const PV& v, int64_t grant, int bs) {  // scheduler.py:350-354
+    if (v.flags & PV_GUEST) return 0;
+    return fp_tokens(v.granted + grant, bs) - fp_tokens(v.granted, bs);
+}
+
 struct PlanSh {
     BlkShared b;
+    PV pv[PV_CAP];
+    FV fv[FV_CAP];
+    int32_t pneed[PV_CAP], pgrant[PV_CAP];
+    int64_t tri_key[PV_CAP];     // host triples (a_j - u_j), cached when n_tri <= PV_CAP
+    int32_t tri_idx[PV_CAP], tri_taken[PV_CAP];
+    int32_t n_tri_cached;
+    unsigned __int128 wsum;
     int64_t free, shortfall, runway, batch_now, gm_tokens;
     int64_t f_total, a_total, f_supply, a_supply, tbt_floor, lim, resid;
     int32_t rsvb, n_mem, n_act, n_pre, n_cl, n_def, n_gm, n_pend, n_mready, n_part;
@@ -35,25 +83,29 @@ __device__ __forceinline__ void push_mem(const Dev& d, PlanSh& S, int32_t i, int
 // Without stacking a host is feasible iff (a_j - u_j) >= b + need + out, so
 // with the hosts sorted by (a_j - u_j, id) the argmin is the first free entry
 // at or after a lower bound.
-__device__ bool try_embed(const Dev& d, PlanSh& S, int32_t i, int32_t n_tri, int32_t sid) {
-    if (eff_of(d, i) > 0 || d.pcount[i] > 0) return false;
-    int32_t er = est_rem(d, i);
-    int32_t pg = d.pred[i] - d.gen[i];
-    int32_t out = er > pg ? er : pg;
+__device__ bool try_embed(const Dev& d, PlanSh& S, const PV& v, int32_t n_tri, int32_t sid) {
+    const int32_t i = v.i;
+    if (v.eff > 0 || v.pcount > 0) return false;
+    int32_t out = v.er > v.pg ? v.er : v.pg;
     if (out < 1) out = 1;
-    int64_t need = (int64_t)d.kv_need[i] + out;
+    int64_t need = (int64_t)v.kvn + out;
     int64_t thr = (int64_t)d.buffer_b + need + out;
+    const bool cached = S.n_tri_cached;
     int32_t lo = 0, hi = n_tri;
     while (lo < hi) {
         int32_t mid = (lo + hi) >> 1;
-        if (d.l_tri_key[mid] < thr) lo = mid + 1; else hi = mid;
+        if ((cached ? S.tri_key[mid] : d.l_tri_key[mid]) < thr) lo = mid + 1; else hi = mid;
     }
-    while (lo < n_tri && (d.l_tri_taken[lo] || d.st_removed[d.l_tri[lo]] == sid)) lo++;
+    if (cached) {
+        while (lo < n_tri && (S.tri_taken[lo] || d.st_removed[S.tri_idx[lo]] == sid)) lo++;
+    } else {
+        while (lo < n_tri && (d.l_tri_taken[lo] || d.st_removed[d.l_tri[lo]] == sid)) lo++;
+    }
     if (lo >= n_tri) return false;
-    int32_t h = d.l_tri[lo];
-    push_act(d, S, A_EMBED, i, need, 0, h, (int64_t)d.granted[h] - need);
+    int32_t h = cached ? S.tri_idx[lo] : d.l_tri[lo];
+    push_act(d, S, A_EMBED, i, need, 0, h, (cached ? S.tri_key[lo] : d.l_tri_key[lo]) + d.used[h] - need);
     d.st_embedded[i] = sid;
-    d.l_tri_taken[lo] = 1;  // one guest per host per plan (scheduler.py:446-448)
+    if (cached) S.tri_taken[lo] = 1; else d.l_tri_taken[lo] = 1;  // one guest per host per plan (scheduler.py:446-448)
     return true;
 }
 
@@ -62,11 +114,14 @@ __device__ __forceinline__ int64_t nw_need(const Dev& d, int32_t i) {  // schedu
     return v > 0 ? v : 0;
 }
 
-__device__ __forceinline__ void amort_weight(const Dev& d, int32_t i, int64_t now, uint64_t& w) {
-    int64_t rt = rt_of(d, i, now);   // scheduler.py:645: max(1, rt_us), max(1, kv_need)
-    if (rt < 1) rt = 1;
-    int64_t pr = d.kv_need[i] < 1 ? 1 : d.kv_need[i];
-    w = (uint64_t)rt * (uint64_t)pr;
+// participant view by position: cached for p < PV_CAP, recomputed beyond
+__device__ __forceinline__ PV part_pv(const Dev& d, const PlanSh& S, int32_t p, int64_t now) {
+    return p < PV_CAP ? S.pv[p] : make_pv(d, d.l_part[p], now);
+}
+__device__ __forceinline__ uint64_t amort_weight(const PV& v) {
+    int64_t rt = v.rt < 1 ? 1 : v.rt;  // scheduler.py:645: max(1, rt_us), max(1, kv_need)
+    int64_t pr = v.kvn < 1 ? 1 : v.kvn;
+    return (uint64_t)rt * (uint64_t)pr;
 }
 
 // allocate_remaining (scheduler.py:211-243) + block flooring
@@ -90,6 +145,11 @@ __device__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64
     nlive = blk_sum(nlive, S.b);
     *total_out = tot;
     if (nlive == 0) return;
+    if (supply == 0) {
+        // a' = 0: every share a'*w/W and remainder is 0, nothing is left over
+        // and the block floor keeps 0 (scheduler.py:229-243, 653-659)
+        return;
+    }
     if (live_tot <= supply) {
         for (int32_t k = tid; k < m; k += NT) {
             int32_t p = grp[k];
@@ -99,34 +159,47 @@ __device__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64
         __syncthreads();
         return;
     }
-    if (tid == 0) {
-        int32_t w = 0;
-        for (int32_t k = 0; k < m; k++)
-            if (d.l_part_need[grp[k]] > 0) grp[w++] = grp[k];
-        S.g_nlive = w;
-        unsigned __int128 W = 0;
-        for (int32_t k = 0; k < w; k++) {
-            uint64_t wi;
-            amort_weight(d, d.l_part[grp[k]], now, wi);
-            W += (unsigned __int128)wi;
+    // live demands only, order-preserving (the ranking below is total)
+    const int32_t w = blk_compact(grp, m, d.sk_item, [&](int32_t p) { return d.l_part_need[p] > 0; }, S.b);
+    for (int32_t k = tid; k < w; k += NT) grp[k] = d.sk_item[k];
+    if (tid == 0) S.wsum = 0;
+    __syncthreads();
+    // W = sum of weights (u128): per-thread partial sums, then one atomic-free
+    // serial fold of the 32 warp totals
+    unsigned __int128 part = 0;
+    for (int32_t k = tid; k < w; k += NT) part += (unsigned __int128)amort_weight(part_pv(d, S, grp[k], now));
+    {
+        uint64_t lo = (uint64_t)part, hi = (uint64_t)(part >> 64);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            uint64_t lo2 = __shfl_xor_sync(0xffffffffu, lo, o), hi2 = __shfl_xor_sync(0xffffffffu, hi, o);
+            uint64_t nl = lo + lo2;
+            hi = hi + hi2 + (nl < lo ? 1 : 0);
+            lo = nl;
         }
-        int64_t sq = 0;
-        for (int32_t k = 0; k < w; k++) {
-            int32_t p = grp[k];
-            uint64_t wi;
-            amort_weight(d, d.l_part[p], now, wi);
-            unsigned __int128 x = (unsigned __int128)(uint64_t)supply * (unsigned __int128)wi;
-            unsigned __int128 q = x / W, r = x % W;
-            d.l_part_grant[p] = (int32_t)(uint64_t)q;
-            sq += (int64_t)(uint64_t)q;
-            d.am_rhi[p] = (uint64_t)(r >> 64);
-            d.am_rlo[p] = (uint64_t)r;
-        }
-        S.g_left = (int32_t)(supply - sq);
+        if ((tid & 31) == 0) { S.b.ured[tid >> 5] = lo; S.b.red[tid >> 5] = (int64_t)hi; }
     }
     __syncthreads();
-    const int32_t w = S.g_nlive;
-    const int32_t left = S.g_left;
+    if (tid == 0) {
+        unsigned __int128 W = 0;
+        for (int k = 0; k < NT / 32; k++)
+            W += ((unsigned __int128)(uint64_t)S.b.red[k] << 64) | (unsigned __int128)S.b.ured[k];
+        S.wsum = W;
+    }
+    __syncthreads();
+    const unsigned __int128 W = S.wsum;
+    int64_t sq = 0;
+    for (int32_t k = tid; k < w; k += NT) {
+        const int32_t p = grp[k];
+        const unsigned __int128 x = (unsigned __int128)(uint64_t)supply * amort_weight(part_pv(d, S, p, now));
+        const unsigned __int128 q = x / W, r = x % W;
+        d.l_part_grant[p] = (int32_t)(uint64_t)q;
+        sq += (int64_t)(uint64_t)q;
+        d.am_rhi[p] = (uint64_t)(r >> 64);
+        d.am_rlo[p] = (uint64_t)r;
+    }
+    sq = blk_sum(sq, S.b);
+    const int64_t left = supply - sq;
     // largest remainder first, ties by req_id (scheduler.py:240-242)
     blk_sort(grp, w, [&](int32_t p, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
         k0 = ~d.am_rhi[p];
@@ -162,7 +235,8 @@ __device__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64
 }
 
 __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
-    __shared__ PlanSh S;
+    extern __shared__ __align__(16) uint8_t plan_smem[];
+    PlanSh& S = *reinterpret_cast<PlanSh*>(plan_smem);
     const Ctl& c = *d.ctl;
     if (!c.active) return;
     const int tid = threadIdx.x;
@@ -181,6 +255,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     }
     __syncthreads();
 
+    prof_mark(d, 0);
     // ---- returned running (scheduler.py:142-150, 161-162) ------------------
     auto crit_rt = [&](int64_t r) { return r >= -eps && r - ti < eps; };
     const int32_t n_nr = blk_compact(RUN, n_run, d.l_nr, [&](int32_t i) {
@@ -198,6 +273,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     }, d, S.b);
     for (int32_t k = tid; k < n_nr; k += NT) d.st_nr[d.l_nr[k]] = sid;
 
+    prof_mark(d, 1);
     // ---- embedding hosts (scheduler.py:425-430) sorted by (a_j - u_j, id) --
     const int32_t n_tri = blk_compact(RUN, n_run, d.l_tri, [&](int32_t i) {
         return !guest_of(d, i) && d.holds[i] && d.prefill[i] >= d.kv_need[i];
@@ -205,18 +281,26 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     blk_sort(d.l_tri, n_tri, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
         k0 = (uint64_t)((int64_t)d.granted[i] - d.used[i] + (1ll << 40)); k1 = (uint64_t)d.idrank[i]; k2 = 0;
     }, d, S.b);
+    const bool tri_cached = n_tri <= PV_CAP;
     for (int32_t k = tid; k < n_tri; k += NT) {
         int32_t h = d.l_tri[k];
-        d.l_tri_key[k] = (int64_t)d.granted[h] - d.used[h];
-        d.l_tri_taken[k] = d.guest[h] >= 0 ? 1 : 0;  // already hosting: skipped without stacking
+        const int64_t key = (int64_t)d.granted[h] - d.used[h];
+        const int32_t taken = d.guest[h] >= 0 ? 1 : 0;  // already hosting: skipped without stacking
+        if (tri_cached) {
+            S.tri_key[k] = key; S.tri_idx[k] = h; S.tri_taken[k] = taken;
+        } else {
+            d.l_tri_key[k] = key; d.l_tri_taken[k] = taken;
+        }
     }
+    if (tid == 0) S.n_tri_cached = tri_cached ? 1 : 0;
     __syncthreads();
 
+    prof_mark(d, 2);
     // ---- critical waiting: embed first (scheduler.py:451-457) -------------
     if (tid == 0) {
         for (int32_t k = 0; k < n_nw; k++) {
             int32_t i = NW[k];
-            if (try_embed(d, S, i, n_tri, sid)) {
+            if (try_embed(d, S, make_pv(d, i, now), n_tri, sid)) {
                 int32_t ch = d.kv_need[i] - d.prefill[i];
                 d.l_gm_idx[S.n_gm] = i; d.l_gm_tok[S.n_gm] = ch; S.n_gm++;
                 S.gm_tokens += ch;
@@ -228,6 +312,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     __syncthreads();
     const int32_t n_pend0 = S.n_pend;
 
+    prof_mark(d, 3);
     // ---- exact-consumption demand and reserve (scheduler.py:459-472) ------
     int64_t dem = 0;
     for (int32_t k = tid; k < n_pend0; k += NT) { int32_t i = d.l_pend[k]; dem += cost_of(d, i, nw_need(d, i)); }
@@ -241,6 +326,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     }
     __syncthreads();
 
+    prof_mark(d, 4);
     // ---- victims and deferral (scheduler.py:474-507) ----------------------
     if (S.shortfall > 0) {
         for (int32_t k = tid; k < n_pend0; k += NT) d.st_crit[d.l_pend[k]] = sid;
@@ -300,6 +386,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         }
     }
 
+    prof_mark(d, 5);
     // ---- continuation, resumption, critical admission (scheduler.py:515-574)
     if (tid == 0) {
         const int32_t nb_B = (B + bs - 1) / bs;
@@ -364,6 +451,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     }
     __syncthreads();
 
+    prof_mark(d, 6);
     // ---- decode members in running order (scheduler.py:576-593) -----------
     const int32_t n_dec_mem = blk_compact(RUN, n_run, d.mem_idx, [&](int32_t i) {
         if (d.st_removed[i] == sid || !ready_of(d, i, now) || d.prefill[i] < d.kv_need[i]) return false;
@@ -387,6 +475,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     __syncthreads();
     const int64_t consumed = S.batch_now;
 
+    prof_mark(d, 7);
     // ---- token-budget fill over N'_w (scheduler.py:182-200, 596-598) ------
     {
         const int64_t budget = d.token_budget;
@@ -411,13 +500,17 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     __syncthreads();
     const int32_t k_sel = S.k_sel;
 
+    prof_mark(d, 8);
     // ---- participants (scheduler.py:600-638) ------------------------------
+    for (int32_t k = tid; k < k_sel && k < PV_CAP; k += NT) S.pv[k] = make_pv(d, NWP[k], now);
+    __syncthreads();
     if (tid == 0) {
         for (int32_t k = 0; k < k_sel; k++) {
-            int32_t i = NWP[k];
-            if (try_embed(d, S, i, n_tri, sid)) { d.l_mready[S.n_mready++] = i; continue; }
-            int64_t t = target_of(d, i), f = (int64_t)d.kv_need[i] + 1;
-            int64_t need = (t > f ? t : f) - eff_of(d, i);
+            const PV v = k < PV_CAP ? S.pv[k] : make_pv(d, NWP[k], now);
+            const int32_t i = v.i;
+            if (try_embed(d, S, v, n_tri, sid)) { d.l_mready[S.n_mready++] = i; continue; }
+            int64_t t = v.target, f = (int64_t)v.kvn + 1;
+            int64_t need = (t > f ? t : f) - v.eff;
             if (need <= 0) {
                 d.l_mready[S.n_mready++] = i;
             } else {
@@ -436,6 +529,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         }
     }
     __syncthreads();
+    prof_mark(d, 9);
     // proactive_include (scheduler.py:269-279) over the post-eviction running set
     const int64_t mpre = d.prealloc_m;
     const int32_t n_pro = blk_compact(RUN, n_run, d.l_pro, [&](int32_t i) {
@@ -454,6 +548,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         }
     }
     __syncthreads();
+    prof_mark(d, 10);
     // pre-exhaust top-up, running order (scheduler.py:625-638)
     {
         const int32_t base = S.n_part;
@@ -472,7 +567,15 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         __syncthreads();
     }
     const int32_t n_part = S.n_part;
+    prof_mark(d, 11);
+    // participant views, cached
+    for (int32_t p = tid; p < n_part && p < PV_CAP; p += NT) {
+        S.pv[p] = make_pv(d, d.l_part[p], now);
+        S.pneed[p] = d.l_part_need[p];
+    }
+    __syncthreads();
 
+    prof_mark(d, 12);
     // ---- amortized round (scheduler.py:662-682) ---------------------------
     int64_t ndec = 0;
     for (int32_t k = tid; k < n_run; k += NT) {
@@ -480,12 +583,10 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         if (d.st_removed[i] != sid && !guest_of(d, i) && d.prefill[i] >= d.kv_need[i]) ndec++;
     }
     ndec = blk_sum(ndec, S.b);
-    const int32_t n_fl = blk_compact(nullptr, n_part, d.l_grp, [&](int32_t p) {
-        return d.state[d.l_part[p]] == ST_RUNNING;
-    }, S.b);
-    const int32_t n_ad = blk_compact(nullptr, n_part, d.l_grp + n_part, [&](int32_t p) {
-        return d.state[d.l_part[p]] != ST_RUNNING;
-    }, S.b);
+    auto part_running = [&](int32_t p) { return (part_pv(d, S, p, now).flags & PV_RUNNING) != 0; };
+    const int32_t n_fl = blk_compact(nullptr, n_part, d.l_grp, [&](int32_t p) { return part_running(p); }, S.b);
+    const int32_t n_ad = blk_compact(nullptr, n_part, d.l_grp + n_part, [&](int32_t p) { return !part_running(p); },
+                                     S.b);
     if (tid == 0) {
         S.runway = (int64_t)d.runway_iters * ndec;
         S.f_supply = (S.free / bs) * bs;  // free >= 0 throughout planning
@@ -495,7 +596,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     amortize(d, S, d.l_grp, n_fl, S.f_supply, now, &ftot);
     int64_t spent = 0;  // sum of the in-flight grants (amortize compacts grp in place)
     for (int32_t p = tid; p < n_part; p += NT)
-        if (d.state[d.l_part[p]] == ST_RUNNING) spent += d.l_part_grant[p];
+        if (part_running(p)) spent += d.l_part_grant[p];
     spent = blk_sum(spent, S.b);
     if (tid == 0) {
         int64_t a = S.free - spent - S.runway;
@@ -510,63 +611,100 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         S.a_total = atot;
         S.sated = (S.f_total <= S.f_supply && S.a_total <= S.a_supply) ? 1 : 0;
     }
+    for (int32_t p = tid; p < n_part && p < PV_CAP; p += NT) S.pgrant[p] = d.l_part_grant[p];
     __syncthreads();
 
+    prof_mark(d, 13);
     // ---- grant application + pair-release claims (scheduler.py:684-720) ---
     const int32_t n_ful = blk_compact(RUN, n_run, d.l_ful, [&](int32_t i) {
         return !guest_of(d, i) && !returned_of(d, i) && eff_of(d, i) >= target_of(d, i) &&
                d.st_removed[i] != sid;
     }, S.b);
-    for (int32_t p = 0; p < n_part; p++) {
+    const bool ful_cached = n_ful <= FV_CAP;
+    if (ful_cached) {
+        for (int32_t k = tid; k < n_ful; k += NT) {
+            const int32_t q = d.l_ful[k];
+            FV f;
+            f.gain = gain_of(d, q);
+            f.er = est_rem(d, q);
+            f.idrank = d.idrank[q];
+            f.i = q;
+            f._pad = 0;  // claimed this plan
+            S.fv[k] = f;
+        }
+    }
+    __syncthreads();
+    // one participant's grant (thread 0); returns whether a provider search is due
+    auto grant_one = [&](int32_t p) -> bool {
+        const PV v = part_pv(d, S, p, now);
+        const int32_t i = v.i;
+        const int64_t need = p < PV_CAP ? S.pneed[p] : d.l_part_need[p];
+        const int64_t g = p < PV_CAP ? S.pgrant[p] : d.l_part_grant[p];
+        const int64_t eff = v.eff;
+        if (!(v.flags & PV_RUNNING)) {
+            if (eff + g < (int64_t)v.kvn + 1) return false;  // a partial grant that cannot start prefill
+            push_act(d, S, (v.flags & PV_HOLDS) ? A_GROW : A_ALLOCATE, i, g);
+            S.free -= pv_cost(v, g, bs);
+            d.l_mready[S.n_mready++] = i;
+        } else if (g > 0) {
+            push_act(d, S, A_GROW, i, g);
+            S.free -= pv_cost(v, g, bs);
+            if ((v.flags & PV_RETURNED) && eff + g >= (int64_t)v.used + 1) push_mem(d, S, i, 1);
+        }
+        if (g < need) {
+            // scheduler.py:710 rebinds `runway`; the extras gate below sees it
+            S.runway = eff + g - v.used;
+            S.lim = S.runway > 0 ? S.runway : 0;
+            S.resid = need - g;
+            S.cur = i;
+            return true;
+        }
+        return false;
+    };
+    if (ful_cached) {
+        // every provider candidate is in shared memory: thread 0 runs the
+        // whole ordered loop, pair_release (scheduler.py:253-266) as a scan
         if (tid == 0) {
-            S.search = 0;
-            int32_t i = d.l_part[p];
-            int64_t need = d.l_part_need[p];
-            int64_t g = d.l_part_grant[p];
-            int64_t eff = eff_of(d, i);
-            bool skip = false;
-            if (d.state[i] != ST_RUNNING) {
-                if (eff + g < (int64_t)d.kv_need[i] + 1) {
-                    skip = true;  // a partial grant that cannot start prefill
-                } else {
-                    push_act(d, S, d.holds[i] ? A_GROW : A_ALLOCATE, i, g);
-                    S.free -= cost_of(d, i, g);
-                    d.l_mready[S.n_mready++] = i;
+            for (int32_t p = 0; p < n_part; p++) {
+                if (!grant_one(p)) continue;
+                int32_t best = -1;
+                uint64_t bkey = ~0ull;
+                for (int32_t k = 0; k < n_ful; k++) {
+                    const FV& f = S.fv[k];
+                    if (f._pad || f.er > S.lim || f.gain < S.resid) continue;
+                    uint64_t key = ((uint64_t)f.er << 32) | (uint64_t)(uint32_t)f.idrank;
+                    if (key < bkey) { bkey = key; best = k; }
                 }
-            } else if (g > 0) {
-                push_act(d, S, A_GROW, i, g);
-                S.free -= cost_of(d, i, g);
-                if (returned_of(d, i) && eff + g >= (int64_t)d.used[i] + 1) push_mem(d, S, i, 1);
-            }
-            if (!skip && g < need) {
-                // scheduler.py:710 rebinds `runway`; the extras gate below sees it
-                S.runway = eff + g - d.used[i];
-                S.lim = S.runway > 0 ? S.runway : 0;
-                S.resid = need - g;
-                S.cur = i;
-                S.search = 1;
+                if (best >= 0) {
+                    d.cl_w[S.n_cl] = S.cur; d.cl_p[S.n_cl] = S.fv[best].i; S.n_cl++;
+                    S.fv[best]._pad = 1;
+                }
             }
         }
         __syncthreads();
-        if (S.search) {
-            // pair_release (scheduler.py:253-266): soonest finisher, ties by id
-            const int64_t lim = S.lim, resid = S.resid;
-            uint64_t best = ~0ull;
-            for (int32_t k = tid; k < n_ful; k += NT) {
-                int32_t q = d.l_ful[k];
-                if (d.st_claimed[q] == sid) continue;
-                int64_t er = est_rem(d, q);
-                if (er > lim || gain_of(d, q) < resid) continue;
-                uint64_t key = ((uint64_t)er << 32) | (uint64_t)(uint32_t)d.idrank[q];
-                best = key < best ? key : best;
-            }
-            best = blk_min(best, S.b);
-            if (tid == 0 && best != ~0ull) {
-                int32_t q = d.rank_to_idx[(uint32_t)best];
-                d.cl_w[S.n_cl] = S.cur; d.cl_p[S.n_cl] = q; S.n_cl++;
-                d.st_claimed[q] = sid;
-            }
+    } else {
+        for (int32_t p = 0; p < n_part; p++) {
+            if (tid == 0) S.search = grant_one(p) ? 1 : 0;
             __syncthreads();
+            if (S.search) {
+                const int64_t lim = S.lim, resid = S.resid;
+                uint64_t best = ~0ull;
+                for (int32_t k = tid; k < n_ful; k += NT) {
+                    int32_t q = d.l_ful[k];
+                    if (d.st_claimed[q] == sid) continue;
+                    int64_t er = est_rem(d, q);
+                    if (er > lim || gain_of(d, q) < resid) continue;
+                    uint64_t key = ((uint64_t)er << 32) | (uint64_t)(uint32_t)d.idrank[q];
+                    best = key < best ? key : best;
+                }
+                best = blk_min(best, S.b);
+                if (tid == 0 && best != ~0ull) {
+                    int32_t q = d.rank_to_idx[(uint32_t)best];
+                    d.cl_w[S.n_cl] = S.cur; d.cl_p[S.n_cl] = q; S.n_cl++;
+                    d.st_claimed[q] = sid;
+                }
+                __syncthreads();
+            }
         }
     }
     if (tid == 0) {
@@ -577,6 +715,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     }
     __syncthreads();
 
+    prof_mark(d, 14);
     // ---- case 2: extras while sated (scheduler.py:726-748) ----------------
     if (S.sated) {
         uint64_t fl = ~0ull;
@@ -636,6 +775,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         P.sated = S.sated;
         P.k_sel = k_sel;
     }
+    prof_mark(d, 15);
 }
 
 }  // namespace co
