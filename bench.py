@@ -280,14 +280,16 @@ def device_arm(args, rank, world, dist):
         coll = {"op": "ncclAllReduce(sum, int64[2]={free_tokens, reserved_blocks}) per iteration, side stream",
                 "calls": calls, "global_free_tokens": gfree, "global_reserved_blocks": grsv}
     live = s1.n_live
-    # e2e: the public per-step API (step() + event drain into host dicts),
-    # on the steps that follow the timed window
+    # e2e: the public per-step API, each step returning its iteration result
+    # (the members that ran) to the host, on the steps after the window
     eng.events
+    eng.step_result()  # first call captures the single-step graph
     t0 = time.perf_counter()
     dd0 = eng._scalars().decisions
+    d2h = 0
     for _ in range(args.steps):
-        eng.step()
-        eng.events
+        _, members, _ = eng.step_result()
+        d2h += members.size * 4 + 16
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     eng._dirty()
@@ -334,8 +336,10 @@ def device_arm(args, rank, world, dist):
                          "sample": f"oracle port, config-2 steps {WINDOW_START}..{WINDOW_START + cpu_steps - 1} "
                                    f"({cpu_dt:.1f} s, 1 thread)"},
         "e2e": {"value": e2e_dec / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 256 + iter_ev_bytes,
-                "how": "Engine.step() + event drain per step through the public API, K steps after the window"},
+                "d2h_bytes_per_step": 256 + d2h // max(args.steps, 1),
+                "how": "Engine.step_result() per step through the public API (control block + the iteration's "
+                       "members read back every step), K steps after the window; trace uploaded once at "
+                       "construction"},
         "gpu_launches": args.steps * 6,
         "gpu_launches_note": "6 own kernels per step (begin, admit, classify, plan, apply, check) + CUB onesweep sort kernels",
         "clocks": clocks.summary(),

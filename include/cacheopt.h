@@ -182,6 +182,14 @@ int co_destroy(co_engine* eng);
  * *result receives step()'s boolean. */
 int co_step(co_engine* eng, int32_t* result);
 
+/* step() with the iteration's result in the same call and one device sync:
+ * *result = step()'s bool, members = the (idx, tokens) pairs that ran this
+ * iteration (engine.py:630-633 `members`), *iter_end_us its end time (-1 when
+ * the step idled).  The members are written by the device straight into
+ * mapped pinned host memory. */
+int co_step_result(co_engine* eng, int32_t* result, int32_t* members, int64_t max_members,
+                   int64_t* n_members, int64_t* iter_end_us);
+
 /* engine.py:643-661 Engine.run() loop including the no-progress guard,
  * executed as CUDA-graph launches of `steps_per_launch` device steps.
  * max_steps <= 0 means until done.  *steps_done = step() calls made. */

@@ -223,6 +223,7 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
                 c.now = (int64_t)best;
                 c.last_result = 1;
             }
+            if (d.result) d.result[0] = 0;
         }
         return;
     }
@@ -250,6 +251,17 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
         for (int32_t k = tid; k < ns; k += NT) {
             d.members[2 * (off + k)] = d.l_surv_idx[k];
             d.members[2 * (off + k) + 1] = d.l_surv_tok[k];
+        }
+    }
+    if (d.result) {  // the iteration's result straight into mapped host memory
+        const int32_t nr = ns < d.result_cap ? ns : (int32_t)d.result_cap;
+        for (int32_t k = tid; k < nr; k += NT) {
+            d.result[4 + 2 * k] = d.l_surv_idx[k];
+            d.result[4 + 2 * k + 1] = d.l_surv_tok[k];
+        }
+        if (tid == 0) {
+            d.result[0] = nr;
+            *reinterpret_cast<int64_t*>(d.result + 2) = S.end;
         }
     }
 

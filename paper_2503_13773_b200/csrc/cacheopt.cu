@@ -93,6 +93,8 @@ struct co_engine {
     int64_t* red = nullptr;  // [send 2][recv 2]
     int64_t reduce_calls = 0;
     CUtensorMap kvmap;
+    cudaGraphExec_t graph1 = nullptr;  // one step, step() semantics
+    void* result_host = nullptr;
     bool tc_decode = false;
     int64_t page_bytes = 0;
     std::vector<co_event> st_events;   // host staging of drained device events
@@ -236,6 +238,8 @@ const char* co_version(void) { return "cacheopt-b200 0.1 (sm_100a)"; }
 int co_destroy(co_engine* E) {
     if (!E) return CO_OK;
     if (E->graph) cudaGraphExecDestroy(E->graph);
+    if (E->graph1) cudaGraphExecDestroy(E->graph1);
+    if (E->result_host) cudaFreeHost(E->result_host);
     if (E->comm) ncclCommDestroy(E->comm);
     if (E->side) cudaStreamDestroy(E->side);
     if (E->fork) cudaEventDestroy(E->fork);
@@ -555,14 +559,66 @@ static int check_device_error(co_engine* E) {
     return fail(CO_EDEVICE, buf);
 }
 
-int co_step(co_engine* E, int32_t* result) {
-    if (!E || !result) return fail(CO_EINVAL, "null argument");
+static int ensure_step_graph(co_engine* E) {
+    if (E->graph1) return CO_OK;
+    cudaGraph_t g;
+    int r;
+    CK(cudaStreamBeginCapture(E->stream, cudaStreamCaptureModeThreadLocal));
+    if ((r = launch_step(E, 0))) { cudaStreamEndCapture(E->stream, &g); return r; }
+    CK(cudaStreamEndCapture(E->stream, &g));
+    CK(cudaGraphInstantiate(&E->graph1, g, 0));
+    cudaGraphDestroy(g);
+    return CO_OK;
+}
+
+int co_step_result(co_engine* E, int32_t* result, int32_t* members, int64_t max_members, int64_t* n_members,
+                   int64_t* iter_end_us) {
+    if (!E || !result || !n_members) return fail(CO_EINVAL, "null argument");
+    int r;
+    if (!E->result_host) {
+        const int64_t cap = 3 * E->n + 64;
+        CK(cudaHostAlloc(&E->result_host, (4 + 2 * cap) * sizeof(int32_t), cudaHostAllocMapped));
+        void* dev = nullptr;
+        CK(cudaHostGetDevicePointer(&dev, E->result_host, 0));
+        E->d.result = static_cast<int32_t*>(dev);
+        E->d.result_cap = cap;
+        if (E->graph) { cudaGraphExecDestroy(E->graph); E->graph = nullptr; }   // recapture with the result
+        if (E->graph1) { cudaGraphExecDestroy(E->graph1); E->graph1 = nullptr; }
+    }
+    if ((r = ensure_step_graph(E))) return r;
+    const int32_t* res = static_cast<const int32_t*>(E->result_host);
     for (int attempt = 0; attempt < 3; attempt++) {
         CK(cudaEventRecord(E->ev0, E->stream));
-        int r = launch_step(E, 0);
-        if (r) return r;
+        CK(cudaGraphLaunch(E->graph1, E->stream));
         CK(cudaEventRecord(E->ev1, E->stream));
-        CK(cudaGetLastError());
+        if ((r = sync_ctl(E))) return r;
+        float ms = 0;
+        cudaEventElapsedTime(&ms, E->ev0, E->ev1);
+        E->last_ms = ms;
+        if ((r = check_device_error(E))) return r;
+        if (E->h_ctl->paused) {
+            if ((r = drain_device(E))) return r;
+            continue;
+        }
+        *result = E->h_ctl->done ? 0 : E->h_ctl->last_result;
+        int64_t n = res[0] > 0 ? res[0] : 0;
+        if (n > max_members) return fail(CO_EINVAL, "member buffer too small");
+        if (n && members) std::memcpy(members, res + 4, 2 * n * sizeof(int32_t));
+        *n_members = n;
+        if (iter_end_us) *iter_end_us = n ? *reinterpret_cast<const int64_t*>(res + 2) : -1;
+        return CO_OK;
+    }
+    return fail(CO_EDEVICE, "step could not make buffer headroom");
+}
+
+int co_step(co_engine* E, int32_t* result) {
+    if (!E || !result) return fail(CO_EINVAL, "null argument");
+    int r = ensure_step_graph(E);
+    if (r) return r;
+    for (int attempt = 0; attempt < 3; attempt++) {
+        CK(cudaEventRecord(E->ev0, E->stream));
+        CK(cudaGraphLaunch(E->graph1, E->stream));
+        CK(cudaEventRecord(E->ev1, E->stream));
         if ((r = sync_ctl(E))) return r;
         float ms = 0;
         cudaEventElapsedTime(&ms, E->ev0, E->ev1);
@@ -993,6 +1049,7 @@ int co_attach_nccl(co_engine* E, const uint8_t* uid, int32_t nranks, int32_t ran
     E->nranks = nranks;
     E->rank = rank;
     if (E->graph) { cudaGraphExecDestroy(E->graph); E->graph = nullptr; }  // recapture with the collective
+    if (E->graph1) { cudaGraphExecDestroy(E->graph1); E->graph1 = nullptr; }
     return CO_OK;
 }
 
@@ -1012,6 +1069,7 @@ int co_phase_profile(co_engine* E, int32_t enable, int64_t* out /* 64 */) {
         CK(cudaMalloc(&E->d.prof, 64 * sizeof(int64_t)));
         CK(cudaMemset(E->d.prof, 0, 64 * sizeof(int64_t)));
         if (E->graph) { cudaGraphExecDestroy(E->graph); E->graph = nullptr; }
+        if (E->graph1) { cudaGraphExecDestroy(E->graph1); E->graph1 = nullptr; }
     }
     if (out && E->d.prof) {
         CK(cudaMemcpyAsync(out, E->d.prof, 64 * sizeof(int64_t), cudaMemcpyDeviceToHost, E->stream));

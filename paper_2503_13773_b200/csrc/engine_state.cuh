@@ -113,6 +113,11 @@ struct Dev {
     int64_t* samples;   // (footprint, used) pairs
     Ctl* ctl;
     int64_t* prof;   // optional phase timestamps (ns, %globaltimer), 64 slots per kernel
+    // per-step result in mapped pinned host memory (co_step_result):
+    // [0] member count (-1 while the step is idle/ended), [1] unused,
+    // [2..3] iteration end (int64), then (idx, tokens) pairs
+    int32_t* result;
+    int64_t result_cap;
 };
 
 // ---------------------------------------------------------------------------

@@ -15,6 +15,7 @@ __global__ void k_begin(Dev d, int32_t guard) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     Ctl& c = *d.ctl;
     c.active = 0;
+    if (d.result) d.result[0] = -1;
     if (c.done) { c.last_result = 0; return; }
     if (c.paused || c.error) return;
     // append-buffer headroom for the worst case of this step: pause (the host

@@ -315,6 +315,7 @@ class Engine:
         self._sc = None
         self.report: Optional[MetricsReport] = None
         self.pool = PoolView(self)
+        self._resbuf = None
 
     # -- lifecycle -----------------------------------------------------------
 
@@ -359,6 +360,20 @@ class Engine:
         self._dirty()
         N.check(self._lib.co_step(self._h, C.byref(r)), "co_step")
         return bool(r.value)
+
+    def step_result(self):
+        """step() plus this iteration's result in one device round trip:
+        (step()'s bool, int32 array [m, 2] of (req_id, tokens) that ran, end_us)."""
+        if self._resbuf is None:
+            self._resbuf = np.empty(2 * (3 * self._n + 64), dtype=np.int32)
+            self._rid_np = np.array(self._rid, dtype=np.int64)
+        r, n, end = C.c_int32(), C.c_int64(), C.c_int64()
+        self._dirty()
+        N.check(self._lib.co_step_result(self._h, C.byref(r), _ptr(self._resbuf, C.c_int32),
+                                         len(self._resbuf) // 2, C.byref(n), C.byref(end)), "co_step_result")
+        m = self._resbuf[:2 * n.value].reshape(-1, 2)
+        out = np.stack([self._rid_np[m[:, 0]], m[:, 1]], axis=1) if n.value else np.zeros((0, 2), np.int64)
+        return bool(r.value), out, int(end.value)
 
     def run_steps(self, max_steps: int = 0, steps_per_launch: Optional[int] = None) -> int:
         """Device loop with the run() progress guard; returns step() calls."""

@@ -63,3 +63,22 @@ def test_config2_first_60_steps(cuda_ok):
     for _ in range(60):
         orc.step()
     _compare(eng, orc, "config2")
+
+
+@pytest.mark.parametrize("seed", [4, 8])
+def test_step_result_members_match_iter_events(cuda_ok, seed):
+    from paper_2503_13773_b200 import Engine
+    reqs, cfg = build_product(case_params(seed))
+    eng = Engine(reqs, cfg)
+    got = []
+    while True:
+        more, members, end = eng.step_result()
+        if len(members):
+            got.append((end, members.tolist()))
+        if not more:
+            break
+    iters = [(e["end"], e["members"]) for e in eng.events if e["ev"] == "iter"]
+    assert got == iters
+    orc = CacheOptOracle(reqs, cfg)
+    orc.run()
+    assert eng.events == orc.events
