@@ -323,9 +323,10 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     double max_iter_ms = cfg->iter_base_ms + cfg->iter_per_token_ms * (double)tot_tokens;
     double bound = std::max((double)maxD, (double)horizon + max_iter_ms * 1000.0 + 2.0 + (double)max_tbt_slo);
     int timebits = 1;
-    while (timebits < 61 - idbits && std::ldexp(1.0, timebits) <= bound) timebits++;
+    while (timebits < 61 && std::ldexp(1.0, timebits) <= bound) timebits++;
     if (bound >= std::ldexp(1.0, timebits)) return fail(CO_EINVAL, "trace time range exceeds the sort-key budget");
-    const int key_bits = 3 + timebits + idbits;  // class(2) | blown(1) | time | id rank
+    // class(2) | blown(1) | time-or-index; id ties by the stable sort's input order
+    const int key_bits = 3 + std::max(timebits, idbits);
 
     co_engine* E = new co_engine();
     E->n = n;

@@ -91,14 +91,15 @@ __device__ __forceinline__ void admit_one(const Dev& d, int32_t i, int32_t lo, i
     }
 }
 
-// class codes in the top two key bits: [class:2][blown:1][time][id rank]
+// class codes in the top two key bits: [class:2][blown:1][time].  Keys are
+// written at position idrank[i], so the sort's input is in req_id order and
+// the (stable) radix sort breaks every tie by id without id-rank key bits.
 constexpr uint64_t K_NW = 0, K_NWP = 1, K_RUN = 2;
 
 __global__ void k_classify(Dev d) {
     const Ctl& c = *d.ctl;
     if (!c.active) return;
     const int64_t now = c.now, ti = c.t_i, eps = d.eps;
-    const int ib = d.idbits;
     const int cs = d.key_bits - 2, fs = d.key_bits - 3;  // class / blown-flag bit positions
     int32_t cw = 0, cwp = 0, cr = 0;
     const int32_t hi_live = c.next_pending;
@@ -113,15 +114,14 @@ __global__ void k_classify(Dev d) {
                 // every waiting view is ready (engine.py:311-312); rt = D - now
                 int64_t D = d.first_tok[i] < 0 ? d.arr[i] + d.slo_ttft[i] : d.last_tok[i] + d.slo_tbt[i];
                 int64_t rt = D - now;
-                uint64_t id = (uint64_t)d.idrank[i];
                 if (rt >= -eps && rt - ti < eps) {
-                    key = (K_NW << cs) | ((uint64_t)D << ib) | id;
+                    key = (K_NW << cs) | (uint64_t)D;
                     cw++;
                 } else {
                     // queue_key (scheduler.py:151-157): (0, rt, id) / (1, arrival, id)
                     uint64_t flag = rt < 0 ? 1 : 0;
                     uint64_t v = flag ? (uint64_t)d.arr[i] : (uint64_t)D;
-                    key = (K_NWP << cs) | (flag << fs) | (v << ib) | id;
+                    key = (K_NWP << cs) | (flag << fs) | v;
                     cwp++;
                 }
             } else if (s == ST_RUNNING) {
@@ -129,8 +129,9 @@ __global__ void k_classify(Dev d) {
                 cr++;
             }
         }
-        d.keys_in[i] = key;
-        d.vals_in[i] = (uint32_t)i;
+        const int32_t pos = d.idrank[i];
+        d.keys_in[pos] = key;
+        d.vals_in[pos] = (uint32_t)i;
     }
     // warp-aggregated counters
     for (int o = 16; o > 0; o >>= 1) {
