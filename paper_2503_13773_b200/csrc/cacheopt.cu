@@ -401,6 +401,7 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     AL(d.l_part_grant, n3); AL(d.l_mready, n2); AL(d.l_gm_idx, n); AL(d.l_gm_tok, n); AL(d.l_acted, n3);
     AL(d.l_surv_idx, n3); AL(d.l_surv_tok, n3); AL(d.l_done, n3); AL(d.l_coll, n); AL(d.l_grp, 2 * n3);
     AL(d.l_fill_t0, n3); AL(d.l_fill_n, n3); AL(d.l_mflag, n3);
+    AL(d.views, n);
     AL(d.dctl, 1);
     std::memset(&d.dp, 0, sizeof(d.dp));
     if (cfg->kv_layers > 0) {

@@ -112,6 +112,7 @@ struct Dev {
     int32_t* members;   // (idx, tok) pairs
     int64_t* samples;   // (footprint, used) pairs
     Ctl* ctl;
+    struct PV* views;  // per-request planner snapshot (k_classify -> k_plan)
     int64_t* prof;   // optional phase timestamps (ns, %globaltimer), 64 slots per kernel
     // per-step result in mapped pinned host memory (co_step_result):
     // [0] member count (-1 while the step is idle/ended), [1] unused,
@@ -196,5 +197,47 @@ __device__ __forceinline__ double iter_ms(const Dev& d, int64_t tokens) {
 }
 // core.py:21-23 to_us
 __device__ __forceinline__ int64_t to_us_d(double ms) { return (int64_t)floor(__dadd_rn(__dmul_rn(ms, 1000.0), 0.5)); }
+
+// Planner view of one request (engine.py:284-317 fields the planner reads):
+// one 64-byte record per live request written by k_classify, so the
+// latency-bound planner reads one line per request instead of a dozen SoA
+// arrays; hot lists are further staged into shared memory.  The pool is not
+// mutated while planning, so a view stays valid for the whole plan.
+struct __align__(16) PV {
+    int32_t i, eff, target, er, kvn, pre, used, granted, pcount, pg, idrank, flags;
+    int64_t rt, gain;
+};
+enum : int32_t { PV_HOLDS = 1, PV_GUEST = 2, PV_RETURNED = 4, PV_RUNNING = 8, PV_WAITING = 16, PV_READY = 32 };
+
+__device__ __forceinline__ PV make_pv(const Dev& d, int32_t i, int64_t now) {
+    PV v;
+    v.i = i;
+    v.eff = eff_of(d, i);
+    v.er = est_rem(d, i);
+    v.kvn = d.kv_need[i];
+    v.pre = d.prefill[i];
+    v.used = d.used[i];
+    v.target = (v.used > v.kvn ? v.used : v.kvn) + v.er;
+    v.granted = d.holds[i] ? d.granted[i] : 0;
+    v.pcount = d.pcount[i];
+    v.pg = d.pred[i] - d.gen[i];
+    v.idrank = d.idrank[i];
+    const int8_t st = d.state[i];
+    v.flags = (d.holds[i] ? PV_HOLDS : 0) | (guest_of(d, i) ? PV_GUEST : 0) |
+              (st == ST_RUNNING ? PV_RUNNING : 0) | (st == ST_WAITING ? PV_WAITING : 0) |
+              ((st == ST_RUNNING && v.eff < v.used + 1) ? PV_RETURNED : 0);
+    v.flags |= (st != ST_RUNNING || now >= d.ready_at[i]) ? PV_READY : 0;
+    v.rt = rt_of(d, i, now);
+    v.gain = (d.holds[i] && d.host[i] < 0) ? gain_of(d, i) : 0;
+    return v;
+}
+// the step's snapshot view, written by k_classify for every live request
+__device__ __forceinline__ PV view_of(const Dev& d, int32_t i) {
+    const uint4* src = reinterpret_cast<const uint4*>(d.views + i);
+    PV v;
+    uint4* dst = reinterpret_cast<uint4*>(&v);
+    dst[0] = src[0]; dst[1] = src[1]; dst[2] = src[2]; dst[3] = src[3];
+    return v;
+}
 
 }  // namespace co

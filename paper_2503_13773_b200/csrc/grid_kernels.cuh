@@ -110,6 +110,12 @@ __global__ void k_classify(Dev d) {
         if (i >= alo && i < ahi) admit_one(d, i, alo, ev0);
         if (i < hi_live) {
             int8_t s = d.state[i];
+            if (s >= ST_WAITING && s <= ST_PREEMPTED) {
+                const PV v = make_pv(d, i, now);  // the planner's snapshot view
+                uint4* dst = reinterpret_cast<uint4*>(d.views + i);
+                const uint4* src = reinterpret_cast<const uint4*>(&v);
+                dst[0] = src[0]; dst[1] = src[1]; dst[2] = src[2]; dst[3] = src[3];
+            }
             if (s == ST_WAITING || s == ST_PREEMPTED) {
                 // every waiting view is ready (engine.py:311-312); rt = D - now
                 int64_t D = d.first_tok[i] < 0 ? d.arr[i] + d.slo_ttft[i] : d.last_tok[i] + d.slo_tbt[i];

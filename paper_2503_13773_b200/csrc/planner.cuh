@@ -11,46 +11,17 @@
 
 namespace co {
 
-// Planner view of one request (engine.py:284-317 fields the planner reads),
-// computed in parallel into shared memory so thread 0's ordered loops read
-// shared memory instead of chasing HBM.  The pool is not mutated while
-// planning, so a view stays valid for the whole plan.
-struct PV {
-    int32_t i, eff, target, er, kvn, pre, used, granted, pcount, pg, idrank, flags;
-    int64_t rt;
-};
-enum : int32_t { PV_HOLDS = 1, PV_GUEST = 2, PV_RETURNED = 4, PV_RUNNING = 8, PV_WAITING = 16 };
+__device__ __forceinline__ int64_t pv_cost(const PV& v, int64_t grant, int bs) {  // scheduler.py:350-354
+    if (v.flags & PV_GUEST) return 0;
+    return fp_tokens(v.granted + grant, bs) - fp_tokens(v.granted, bs);
+}
+
 constexpr int PV_CAP = 1024;
 struct FV {  // fulfilled provider candidate (scheduler.py:685-689, 711-716)
     int64_t gain;
     int32_t er, idrank, i, _pad;
 };
 constexpr int FV_CAP = 1024;
-
-__device__ __forceinline__ PV make_pv(const Dev& d, int32_t i, int64_t now) {
-    PV v;
-    v.i = i;
-    v.eff = eff_of(d, i);
-    v.er = est_rem(d, i);
-    v.kvn = d.kv_need[i];
-    v.pre = d.prefill[i];
-    v.used = d.used[i];
-    v.target = (v.used > v.kvn ? v.used : v.kvn) + v.er;
-    v.granted = d.holds[i] ? d.granted[i] : 0;
-    v.pcount = d.pcount[i];
-    v.pg = d.pred[i] - d.gen[i];
-    v.idrank = d.idrank[i];
-    const int8_t st = d.state[i];
-    v.flags = (d.holds[i] ? PV_HOLDS : 0) | (guest_of(d, i) ? PV_GUEST : 0) |
-              (st == ST_RUNNING ? PV_RUNNING : 0) | (st == ST_WAITING ? PV_WAITING : 0) |
-              ((st == ST_RUNNING && v.eff < v.used + 1) ? PV_RETURNED : 0);
-    v.rt = rt_of(d, i, now);
-    return v;
-}
-__device__ __forceinline__ int64_t pv_cost(const PV& v, int64_t grant, int bs) {  // scheduler.py:350-354
-    if (v.flags & PV_GUEST) return 0;
-    return fp_tokens(v.granted + grant, bs) - fp_tokens(v.granted, bs);
-}
 
 struct PlanSh {
     BlkShared b;
@@ -116,7 +87,7 @@ __device__ __forceinline__ int64_t nw_need(const Dev& d, int32_t i) {  // schedu
 
 // participant view by position: cached for p < PV_CAP, recomputed beyond
 __device__ __forceinline__ PV part_pv(const Dev& d, const PlanSh& S, int32_t p, int64_t now) {
-    return p < PV_CAP ? S.pv[p] : make_pv(d, d.l_part[p], now);
+    return p < PV_CAP ? S.pv[p] : view_of(d, d.l_part[p]);
 }
 __device__ __forceinline__ uint64_t amort_weight(const PV& v) {
     int64_t rt = v.rt < 1 ? 1 : v.rt;  // scheduler.py:645: max(1, rt_us), max(1, kv_need)
@@ -259,10 +230,12 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     // ---- returned running (scheduler.py:142-150, 161-162) ------------------
     auto crit_rt = [&](int64_t r) { return r >= -eps && r - ti < eps; };
     const int32_t n_nr = blk_compact(RUN, n_run, d.l_nr, [&](int32_t i) {
-        return ready_of(d, i, now) && returned_of(d, i) && crit_rt(rt_of(d, i, now));
+        const PV v = view_of(d, i);
+        return (v.flags & PV_READY) && (v.flags & PV_RETURNED) && crit_rt(v.rt);
     }, S.b);
     const int32_t n_nrp = blk_compact(RUN, n_run, d.l_nrp, [&](int32_t i) {
-        return ready_of(d, i, now) && returned_of(d, i) && !crit_rt(rt_of(d, i, now));
+        const PV v = view_of(d, i);
+        return (v.flags & PV_READY) && (v.flags & PV_RETURNED) && !crit_rt(v.rt);
     }, S.b);
     blk_sort(d.l_nr, n_nr, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
         k0 = (uint64_t)(rt_of(d, i, now) + (1ll << 62)); k1 = (uint64_t)d.idrank[i]; k2 = 0;
@@ -276,10 +249,12 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     prof_mark(d, 1);
     // ---- embedding hosts (scheduler.py:425-430) sorted by (a_j - u_j, id) --
     const int32_t n_tri = blk_compact(RUN, n_run, d.l_tri, [&](int32_t i) {
-        return !guest_of(d, i) && d.holds[i] && d.prefill[i] >= d.kv_need[i];
+        const PV v = view_of(d, i);
+        return !(v.flags & PV_GUEST) && (v.flags & PV_HOLDS) && v.pre >= v.kvn;
     }, S.b);
     blk_sort(d.l_tri, n_tri, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
-        k0 = (uint64_t)((int64_t)d.granted[i] - d.used[i] + (1ll << 40)); k1 = (uint64_t)d.idrank[i]; k2 = 0;
+        const PV v = view_of(d, i);
+        k0 = (uint64_t)((int64_t)v.granted - v.used + (1ll << 40)); k1 = (uint64_t)v.idrank; k2 = 0;
     }, d, S.b);
     const bool tri_cached = n_tri <= PV_CAP;
     for (int32_t k = tid; k < n_tri; k += NT) {
@@ -300,7 +275,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     if (tid == 0) {
         for (int32_t k = 0; k < n_nw; k++) {
             int32_t i = NW[k];
-            if (try_embed(d, S, make_pv(d, i, now), n_tri, sid)) {
+            if (try_embed(d, S, view_of(d, i), n_tri, sid)) {
                 int32_t ch = d.kv_need[i] - d.prefill[i];
                 d.l_gm_idx[S.n_gm] = i; d.l_gm_tok[S.n_gm] = ch; S.n_gm++;
                 S.gm_tokens += ch;
@@ -315,8 +290,15 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     prof_mark(d, 3);
     // ---- exact-consumption demand and reserve (scheduler.py:459-472) ------
     int64_t dem = 0;
-    for (int32_t k = tid; k < n_pend0; k += NT) { int32_t i = d.l_pend[k]; dem += cost_of(d, i, nw_need(d, i)); }
-    for (int32_t k = tid; k < n_nr; k += NT) { int32_t i = d.l_nr[k]; if (!guest_of(d, i)) dem += cost_of(d, i, B); }
+    for (int32_t k = tid; k < n_pend0; k += NT) {
+        const PV v = view_of(d, d.l_pend[k]);
+        int64_t need = (int64_t)v.kvn + B - v.eff;
+        dem += pv_cost(v, need > 0 ? need : 0, bs);
+    }
+    for (int32_t k = tid; k < n_nr; k += NT) {
+        const PV v = view_of(d, d.l_nr[k]);
+        if (!(v.flags & PV_GUEST)) dem += pv_cost(v, B, bs);
+    }
     dem = blk_sum(dem, S.b);
     if (tid == 0) {
         int64_t sf = dem - S.free;
@@ -454,8 +436,9 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     prof_mark(d, 6);
     // ---- decode members in running order (scheduler.py:576-593) -----------
     const int32_t n_dec_mem = blk_compact(RUN, n_run, d.mem_idx, [&](int32_t i) {
-        if (d.st_removed[i] == sid || !ready_of(d, i, now) || d.prefill[i] < d.kv_need[i]) return false;
-        if (returned_of(d, i)) {
+        const PV v = view_of(d, i);
+        if (d.st_removed[i] == sid || !(v.flags & PV_READY) || v.pre < v.kvn) return false;
+        if (v.flags & PV_RETURNED) {
             if (d.st_stalled[i] == sid) return false;
             if (d.st_nr[i] != sid && d.st_resumed[i] != sid) return false;
         }
@@ -484,7 +467,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         for (int32_t base = 0; base < n_nwp; base += NT) {
             int32_t k = base + tid;
             int32_t ch = 0;
-            if (k < n_nwp) { int32_t i = NWP[k]; ch = d.kv_need[i] - d.prefill[i]; }
+            if (k < n_nwp) { const PV v = view_of(d, NWP[k]); ch = v.kvn - v.pre; }
             int32_t tot;
             int32_t ex = blk_excl_scan(ch, &tot, S.b);
             bool over = k < n_nwp && used_base + ex + ch > budget;
@@ -502,11 +485,11 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
 
     prof_mark(d, 8);
     // ---- participants (scheduler.py:600-638) ------------------------------
-    for (int32_t k = tid; k < k_sel && k < PV_CAP; k += NT) S.pv[k] = make_pv(d, NWP[k], now);
+    for (int32_t k = tid; k < k_sel && k < PV_CAP; k += NT) S.pv[k] = view_of(d, NWP[k]);
     __syncthreads();
     if (tid == 0) {
         for (int32_t k = 0; k < k_sel; k++) {
-            const PV v = k < PV_CAP ? S.pv[k] : make_pv(d, NWP[k], now);
+            const PV v = k < PV_CAP ? S.pv[k] : view_of(d, NWP[k]);
             const int32_t i = v.i;
             if (try_embed(d, S, v, n_tri, sid)) { d.l_mready[S.n_mready++] = i; continue; }
             int64_t t = v.target, f = (int64_t)v.kvn + 1;
@@ -533,11 +516,12 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     // proactive_include (scheduler.py:269-279) over the post-eviction running set
     const int64_t mpre = d.prealloc_m;
     const int32_t n_pro = blk_compact(RUN, n_run, d.l_pro, [&](int32_t i) {
-        return d.st_removed[i] != sid && !returned_of(d, i) && eff_of(d, i) < target_of(d, i) &&
-               est_rem(d, i) <= mpre;
+        const PV v = view_of(d, i);
+        return d.st_removed[i] != sid && !(v.flags & PV_RETURNED) && v.eff < v.target && v.er <= mpre;
     }, S.b);
     blk_sort(d.l_pro, n_pro, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
-        k0 = (uint64_t)est_rem(d, i); k1 = (uint64_t)d.idrank[i]; k2 = 0;
+        const PV v = view_of(d, i);
+        k0 = (uint64_t)v.er; k1 = (uint64_t)v.idrank; k2 = 0;
     }, d, S.b);
     if (tid == 0) {
         for (int32_t k = 0; k < n_pro; k++) {
@@ -553,14 +537,14 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     {
         const int32_t base = S.n_part;
         const int32_t n_top = blk_compact(RUN, n_run, d.l_part + base, [&](int32_t i) {
-            return d.st_removed[i] != sid && !guest_of(d, i) && ready_of(d, i, now) &&
-                   d.prefill[i] >= d.kv_need[i] && !returned_of(d, i) &&
-                   (int64_t)eff_of(d, i) - d.used[i] <= mpre && d.st_parts[i] != sid;
+            const PV v = view_of(d, i);
+            return d.st_removed[i] != sid && !(v.flags & PV_GUEST) && (v.flags & PV_READY) && v.pre >= v.kvn &&
+                   !(v.flags & PV_RETURNED) && (int64_t)v.eff - v.used <= mpre && d.st_parts[i] != sid;
         }, S.b);
         for (int32_t k = tid; k < n_top; k += NT) {
-            int32_t i = d.l_part[base + k];
-            int64_t t = target_of(d, i), f = (int64_t)d.used[i] + 1 + B;
-            d.l_part_need[base + k] = (int32_t)((t > f ? t : f) - eff_of(d, i));
+            const PV v = view_of(d, d.l_part[base + k]);
+            int64_t t = v.target, f = (int64_t)v.used + 1 + B;
+            d.l_part_need[base + k] = (int32_t)((t > f ? t : f) - v.eff);
         }
         __syncthreads();
         if (tid == 0) S.n_part = base + n_top;
@@ -570,7 +554,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     prof_mark(d, 11);
     // participant views, cached
     for (int32_t p = tid; p < n_part && p < PV_CAP; p += NT) {
-        S.pv[p] = make_pv(d, d.l_part[p], now);
+        S.pv[p] = view_of(d, d.l_part[p]);
         S.pneed[p] = d.l_part_need[p];
     }
     __syncthreads();
@@ -580,7 +564,8 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     int64_t ndec = 0;
     for (int32_t k = tid; k < n_run; k += NT) {
         int32_t i = RUN[k];
-        if (d.st_removed[i] != sid && !guest_of(d, i) && d.prefill[i] >= d.kv_need[i]) ndec++;
+        const PV v = view_of(d, i);
+        if (d.st_removed[i] != sid && !(v.flags & PV_GUEST) && v.pre >= v.kvn) ndec++;
     }
     ndec = blk_sum(ndec, S.b);
     auto part_running = [&](int32_t p) { return (part_pv(d, S, p, now).flags & PV_RUNNING) != 0; };
@@ -617,17 +602,18 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     prof_mark(d, 13);
     // ---- grant application + pair-release claims (scheduler.py:684-720) ---
     const int32_t n_ful = blk_compact(RUN, n_run, d.l_ful, [&](int32_t i) {
-        return !guest_of(d, i) && !returned_of(d, i) && eff_of(d, i) >= target_of(d, i) &&
-               d.st_removed[i] != sid;
+        const PV v = view_of(d, i);
+        return !(v.flags & PV_GUEST) && !(v.flags & PV_RETURNED) && v.eff >= v.target && d.st_removed[i] != sid;
     }, S.b);
     const bool ful_cached = n_ful <= FV_CAP;
     if (ful_cached) {
         for (int32_t k = tid; k < n_ful; k += NT) {
             const int32_t q = d.l_ful[k];
+            const PV v = view_of(d, q);
             FV f;
-            f.gain = gain_of(d, q);
-            f.er = est_rem(d, q);
-            f.idrank = d.idrank[q];
+            f.gain = v.gain;
+            f.er = v.er;
+            f.idrank = v.idrank;
             f.i = q;
             f._pad = 0;  // claimed this plan
             S.fv[k] = f;
@@ -736,10 +722,10 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
             int32_t k = base + tid;
             int64_t need = 0, cst = 0;
             if (k < n_nwp) {
-                int32_t i = NWP[k];
-                int64_t t = (int64_t)target_of(d, i) - eff_of(d, i);
+                const PV v = view_of(d, NWP[k]);
+                int64_t t = (int64_t)v.target - v.eff;
                 need = t > 0 ? t : 0;
-                cst = cost_of(d, i, need);
+                cst = pv_cost(v, need, bs);
             }
             while (true) {
                 const int64_t room = S.free - S.runway;
