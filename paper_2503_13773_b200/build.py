@@ -31,7 +31,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     OUT.parent.mkdir(parents=True, exist_ok=True)
     tmp = OUT.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           "-I", str(PKG.parent / "include"), "-o", str(tmp), str(SRC), "-lnccl"]
+           "-I", str(PKG.parent / "include"), "-o", str(tmp), str(SRC), "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.run(cmd, check=True)

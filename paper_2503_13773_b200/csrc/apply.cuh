@@ -16,7 +16,7 @@ namespace co {
 __device__ void check_pool(const Dev& d, BlkShared& sb) {
     Ctl& c = *d.ctl;
     int64_t fp = 0, bad = 0;
-    for (int32_t i = threadIdx.x; i < d.n; i += NT) {
+    for (int32_t i = threadIdx.x; i < d.n; i += (int)blockDim.x) {
         if (!d.holds[i]) continue;
         if (d.host[i] < 0) fp += fp_tokens(d.granted[i], d.bs);
         if (d.used[i] > d.granted[i]) bad |= 1;
@@ -110,10 +110,10 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
     // survivors keep member order through ordered compactions.
     const int32_t nm = P.n_mem;
     const uint64_t stamp = (uint64_t)(uint32_t)sid << 24;
-    for (int32_t m = tid; m < nm; m += NT) atomicMax((unsigned long long*)&d.seen64[d.mem_idx[m]],
+    for (int32_t m = tid; m < nm; m += (int)blockDim.x) atomicMax((unsigned long long*)&d.seen64[d.mem_idx[m]],
                                                       (unsigned long long)(stamp | (0xFFFFFFu - (uint32_t)m)));
     __syncthreads();
-    for (int32_t m = tid; m < nm; m += NT) {
+    for (int32_t m = tid; m < nm; m += (int)blockDim.x) {
         const int32_t i = d.mem_idx[m];
         const int32_t tok = d.mem_tok[m];
         int32_t f = 0;  // bit0 survive, bit1 admit event
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
         d.l_mflag[m] = f;
     }
     __syncthreads();
-    for (int32_t m = tid; m < nm; m += NT) {
+    for (int32_t m = tid; m < nm; m += (int)blockDim.x) {
         const int32_t f = d.l_mflag[m];
         if (f & 4) {
             const int32_t i = d.mem_idx[m];
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
     if (d.record_events) {
         const int64_t ev_base = c.ev_count;
         int32_t base = 0;
-        for (int32_t c0 = 0; c0 < nm; c0 += NT) {
+        for (int32_t c0 = 0; c0 < nm; c0 += (int)blockDim.x) {
             const int32_t m = c0 + tid;
             const int32_t fl = (m < nm && (d.l_mflag[m] & 2)) ? 1 : 0;
             int32_t tot;
@@ -172,14 +172,14 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
     // survivors in member order: positions first, then (idx, tokens)
     const int32_t ns0 = blk_compact(nullptr, nm, d.l_surv_tok, [&](int32_t m) { return (d.l_mflag[m] & 1) != 0; }, S.b);
     int64_t bsum = 0;
-    for (int32_t k = tid; k < ns0; k += NT) bsum += d.mem_tok[d.l_surv_tok[k]];
+    for (int32_t k = tid; k < ns0; k += (int)blockDim.x) bsum += d.mem_tok[d.l_surv_tok[k]];
     bsum = blk_sum(bsum, S.b);
-    for (int32_t k = tid; k < ns0; k += NT) {
+    for (int32_t k = tid; k < ns0; k += (int)blockDim.x) {
         const int32_t m = d.l_surv_tok[k];
         d.l_surv_idx[k] = d.mem_idx[m];
     }
     __syncthreads();
-    for (int32_t k = tid; k < ns0; k += NT) d.l_surv_tok[k] = d.mem_tok[d.l_surv_tok[k]];  // position -> tokens
+    for (int32_t k = tid; k < ns0; k += (int)blockDim.x) d.l_surv_tok[k] = d.mem_tok[d.l_surv_tok[k]];  // position -> tokens
     __syncthreads();
     if (tid == 0) {
         const int32_t ns = ns0;
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
         // barrier; nothing changed state in this step, so the classify-time
         // running set is current
         uint64_t best = ~0ull;
-        for (int32_t k = tid; k < n_run; k += NT) {
+        for (int32_t k = tid; k < n_run; k += (int)blockDim.x) {
             int32_t i = RUN[k];
             if (d.state[i] == ST_RUNNING && d.ready_at[i] > now) {
                 uint64_t v = (uint64_t)d.ready_at[i];
@@ -248,14 +248,14 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
     const int64_t end = S.end;
     if (d.record_events) {
         const int64_t off = S.n_acted;
-        for (int32_t k = tid; k < ns; k += NT) {
+        for (int32_t k = tid; k < ns; k += (int)blockDim.x) {
             d.members[2 * (off + k)] = d.l_surv_idx[k];
             d.members[2 * (off + k) + 1] = d.l_surv_tok[k];
         }
     }
     if (d.result) {  // the iteration's result straight into mapped host memory
         const int32_t nr = ns < d.result_cap ? ns : (int32_t)d.result_cap;
-        for (int32_t k = tid; k < nr; k += NT) {
+        for (int32_t k = tid; k < nr; k += (int)blockDim.x) {
             d.result[4 + 2 * k] = d.l_surv_idx[k];
             d.result[4 + 2 * k + 1] = d.l_surv_tok[k];
         }
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
     prof_mark(d, 35);
     // ---- emission (engine.py:553-571), members are distinct ---------------
     int64_t dused = 0, dgen = 0;
-    for (int32_t k = tid; k < ns; k += NT) {
+    for (int32_t k = tid; k < ns; k += (int)blockDim.x) {
         const int32_t i = d.l_surv_idx[k];
         const int32_t tok = d.l_surv_tok[k];
         bool token = false;

@@ -39,7 +39,7 @@ __device__ int64_t blk_sum(int64_t v, BlkShared& s) {
     if (lane == 0) s.red[w] = v;
     __syncthreads();
     if (w == 0) {
-        int64_t x = s.red[lane];
+        int64_t x = lane < (int)(blockDim.x >> 5) ? s.red[lane] : 0;
         x = warp_sum64(x);
         if (lane == 0) s.red[0] = x;
     }
@@ -55,7 +55,7 @@ __device__ uint64_t blk_min(uint64_t v, BlkShared& s) {
     if (lane == 0) s.ured[w] = v;
     __syncthreads();
     if (w == 0) {
-        uint64_t x = s.ured[lane];
+        uint64_t x = lane < (int)(blockDim.x >> 5) ? s.ured[lane] : ~0ull;
         x = warp_min_u64(x);
         if (lane == 0) s.ured[0] = x;
     }
@@ -77,7 +77,7 @@ __device__ int32_t blk_excl_scan(int32_t v, int32_t* total, BlkShared& s) {
     if (lane == 31) s.scan[w] = x;
     __syncthreads();
     if (w == 0) {
-        int32_t y = s.scan[lane];
+        int32_t y = lane < (int)(blockDim.x >> 5) ? s.scan[lane] : 0;
         int32_t z = y;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -99,13 +99,34 @@ __device__ int32_t blk_excl_scan(int32_t v, int32_t* total, BlkShared& s) {
 template <class Pred>
 __device__ int32_t blk_compact(const int32_t* src, int32_t m, int32_t* dst, Pred pred, BlkShared& s) {
     int32_t base = 0;
-    for (int32_t c = 0; c < m; c += NT) {
+    for (int32_t c = 0; c < m; c += (int)blockDim.x) {
         int32_t k = c + (int32_t)threadIdx.x;
         int32_t item = 0;
         int32_t f = 0;
         if (k < m) {
             item = src ? src[k] : k;
             f = pred(item) ? 1 : 0;
+        }
+        int32_t tot;
+        int32_t p = blk_excl_scan(f, &tot, s);
+        if (f) dst[base + p] = item;
+        base += tot;
+    }
+    __syncthreads();
+    return base;
+}
+
+// Order-preserving compaction over positions k of src[0..m) with a predicate
+// that sees (k, src[k]); writes src[k].
+template <class Pred>
+__device__ int32_t blk_compact_at(const int32_t* src, int32_t m, int32_t* dst, Pred pred, BlkShared& s) {
+    int32_t base = 0;
+    for (int32_t c = 0; c < m; c += (int)blockDim.x) {
+        int32_t k = c + (int32_t)threadIdx.x;
+        int32_t item = 0, f = 0;
+        if (k < m) {
+            item = src[k];
+            f = pred(k, item) ? 1 : 0;
         }
         int32_t tot;
         int32_t p = blk_excl_scan(f, &tot, s);
@@ -123,14 +144,14 @@ __device__ void blk_sort(int32_t* items, int32_t m, KeyFn kf, const Dev& d, BlkS
     if (m <= 1) return;
     if (m <= BlkShared::TILE) {
         // small set: keys and items live in shared memory, one rank per thread
-        for (int32_t k = threadIdx.x; k < m; k += NT) {
+        for (int32_t k = threadIdx.x; k < m; k += (int)blockDim.x) {
             uint64_t a, b, c;
             kf(items[k], a, b, c);
             s.t0[k] = a; s.t1[k] = b; s.t2[k] = c;
             s.it[k] = items[k];
         }
         __syncthreads();
-        for (int32_t k = threadIdx.x; k < m; k += NT) {
+        for (int32_t k = threadIdx.x; k < m; k += (int)blockDim.x) {
             const uint64_t a0 = s.t0[k], b0 = s.t1[k], c0 = s.t2[k];
             int32_t rank = 0;
             for (int32_t j = 0; j < m; j++) {
@@ -142,7 +163,7 @@ __device__ void blk_sort(int32_t* items, int32_t m, KeyFn kf, const Dev& d, BlkS
         __syncthreads();
         return;
     }
-    for (int32_t k = threadIdx.x; k < m; k += NT) {
+    for (int32_t k = threadIdx.x; k < m; k += (int)blockDim.x) {
         uint64_t a, b, c;
         kf(items[k], a, b, c);
         d.sk0[k] = a; d.sk1[k] = b; d.sk2[k] = c;
@@ -150,19 +171,19 @@ __device__ void blk_sort(int32_t* items, int32_t m, KeyFn kf, const Dev& d, BlkS
     }
     __syncthreads();
     constexpr int Q = 4;
-    for (int32_t base = 0; base < m; base += Q * NT) {
+    for (int32_t base = 0; base < m; base += Q * (int)blockDim.x) {
         int32_t rank[Q];
         uint64_t m0[Q], m1[Q], m2[Q];
 #pragma unroll
         for (int q = 0; q < Q; q++) {
-            int32_t k = base + q * NT + threadIdx.x;
+            int32_t k = base + q * (int)blockDim.x + threadIdx.x;
             rank[q] = 0;
             if (k < m) { m0[q] = d.sk0[k]; m1[q] = d.sk1[k]; m2[q] = d.sk2[k]; }
             else { m0[q] = m1[q] = m2[q] = 0; }
         }
         for (int32_t t = 0; t < m; t += BlkShared::TILE) {
             int32_t tn = m - t < BlkShared::TILE ? m - t : BlkShared::TILE;
-            for (int32_t j = threadIdx.x; j < tn; j += NT) {
+            for (int32_t j = threadIdx.x; j < tn; j += (int)blockDim.x) {
                 s.t0[j] = d.sk0[t + j]; s.t1[j] = d.sk1[t + j]; s.t2[j] = d.sk2[t + j];
             }
             __syncthreads();
@@ -178,7 +199,7 @@ __device__ void blk_sort(int32_t* items, int32_t m, KeyFn kf, const Dev& d, BlkS
         }
 #pragma unroll
         for (int q = 0; q < Q; q++) {
-            int32_t k = base + q * NT + threadIdx.x;
+            int32_t k = base + q * (int)blockDim.x + threadIdx.x;
             if (k < m) items[rank[q]] = d.sk_item[k];
         }
     }

@@ -11,10 +11,12 @@
 // needed inside a launch.
 #include <cub/device/device_radix_sort.cuh>
 #include <nccl.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -33,6 +35,34 @@
 using namespace co;
 
 static thread_local std::string g_err;
+
+// NCCL is resolved at first use (N4 only), never at load time: a process that
+// loads this library before torch must still get torch's own libnccl
+// (dlopen of the soname returns an already-loaded copy).
+struct NcclApi {
+    decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+    decltype(&ncclCommInitRank) commInitRank = nullptr;
+    decltype(&ncclAllReduce) allReduce = nullptr;
+    decltype(&ncclCommDestroy) commDestroy = nullptr;
+    decltype(&ncclGetErrorString) errorString = nullptr;
+    bool ok = false;
+};
+static NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return a;
+        a.getUniqueId = reinterpret_cast<decltype(a.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+        a.commInitRank = reinterpret_cast<decltype(a.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+        a.allReduce = reinterpret_cast<decltype(a.allReduce)>(dlsym(h, "ncclAllReduce"));
+        a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+        a.errorString = reinterpret_cast<decltype(a.errorString)>(dlsym(h, "ncclGetErrorString"));
+        a.ok = a.getUniqueId && a.commInitRank && a.allReduce && a.commDestroy && a.errorString;
+        return a;
+    }();
+    return api;
+}
 
 static int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -85,6 +115,7 @@ struct co_engine {
     std::vector<int64_t> tok_off_host;
     int64_t n_chunks = 0;
     int sms = 148;
+    int plan_threads = NT;  // CTA size of the single-CTA planner / apply kernels
     void* host_pool = nullptr;
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0;
@@ -146,9 +177,9 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
                                                     d.vals_out, (int)E->n, 0, d.key_bits, s);
     if (e != cudaSuccess) return fail(CO_ECUDA, std::string("radix sort: ") + cudaGetErrorString(e));
     if (ev) mark(ev[3], s);
-    k_plan<<<1, NT, sizeof(PlanSh), s>>>(d);
+    k_plan<<<1, E->plan_threads, sizeof(PlanSh), s>>>(d);
     if (ev) mark(ev[4], s);
-    k_apply<<<1, NT, 0, s>>>(d);
+    k_apply<<<1, E->plan_threads, 0, s>>>(d);
     if (ev) mark(ev[5], s);
     if (ev) mark(ev[6], s);  // (the validate_every check runs inside k_apply)
     if (E->comm) {
@@ -156,8 +187,8 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
         cudaEventRecord(E->fork, s);
         cudaStreamWaitEvent(E->side, E->fork, 0);
         k_reserve_pack<<<1, 32, 0, E->side>>>(d, E->red);
-        ncclResult_t nr = ncclAllReduce(E->red, E->red + 2, 2, ncclInt64, ncclSum, E->comm, E->side);
-        if (nr != ncclSuccess) return fail(CO_ECUDA, std::string("ncclAllReduce: ") + ncclGetErrorString(nr));
+        ncclResult_t nr = nccl().allReduce(E->red, E->red + 2, 2, ncclInt64, ncclSum, E->comm, E->side);
+        if (nr != ncclSuccess) return fail(CO_ECUDA, std::string("ncclAllReduce: ") + nccl().errorString(nr));
         cudaEventRecord(E->join, E->side);
         E->reduce_calls++;
     }
@@ -240,7 +271,7 @@ int co_destroy(co_engine* E) {
     if (E->graph) cudaGraphExecDestroy(E->graph);
     if (E->graph1) cudaGraphExecDestroy(E->graph1);
     if (E->result_host) cudaFreeHost(E->result_host);
-    if (E->comm) ncclCommDestroy(E->comm);
+    if (E->comm) nccl().commDestroy(E->comm);
     if (E->side) cudaStreamDestroy(E->side);
     if (E->fork) cudaEventDestroy(E->fork);
     if (E->join) cudaEventDestroy(E->join);
@@ -349,6 +380,10 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, E->device);
     E->grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8));
     E->sms = sms;
+    if (const char* pt = std::getenv("CACHEOPT_PLAN_THREADS")) {
+        int v = std::atoi(pt);
+        if (v >= 64 && v <= NT && v % 32 == 0) E->plan_threads = v;
+    }
 
     Dev& d = E->d;
     d.n = (int32_t)n; d.bs = cfg->block_size; d.B = cfg->block_size; d.buffer_b = cfg->buffer_b;
@@ -1028,9 +1063,10 @@ int co_swap_bench(co_engine* E, int64_t ntok, int32_t iters, double* out_ms, dou
 
 int co_nccl_unique_id(uint8_t* out) {
     if (!out) return fail(CO_EINVAL, "null argument");
+    if (!nccl().ok) return fail(CO_ECUDA, "libnccl.so.2 not loadable");
     ncclUniqueId id;
-    ncclResult_t r = ncclGetUniqueId(&id);
-    if (r != ncclSuccess) return fail(CO_ECUDA, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    ncclResult_t r = nccl().getUniqueId(&id);
+    if (r != ncclSuccess) return fail(CO_ECUDA, std::string("ncclGetUniqueId: ") + nccl().errorString(r));
     std::memcpy(out, id.internal, NCCL_UNIQUE_ID_BYTES);
     return CO_OK;
 }
@@ -1038,11 +1074,15 @@ int co_nccl_unique_id(uint8_t* out) {
 int co_attach_nccl(co_engine* E, const uint8_t* uid, int32_t nranks, int32_t rank) {
     if (!E || !uid || nranks < 1 || rank < 0 || rank >= nranks) return fail(CO_EINVAL, "bad arguments");
     if (E->comm) return fail(CO_EINVAL, "already attached");
+    if (!nccl().ok) return fail(CO_ECUDA, "libnccl.so.2 not loadable");
     ncclUniqueId id;
     std::memcpy(id.internal, uid, NCCL_UNIQUE_ID_BYTES);
     cudaSetDevice(E->device);
-    ncclResult_t r = ncclCommInitRank(&E->comm, nranks, id, rank);
-    if (r != ncclSuccess) { E->comm = nullptr; return fail(CO_ECUDA, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)); }
+    ncclResult_t r = nccl().commInitRank(&E->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+        E->comm = nullptr;
+        return fail(CO_ECUDA, std::string("ncclCommInitRank: ") + nccl().errorString(r));
+    }
     CK(cudaStreamCreateWithFlags(&E->side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&E->fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&E->join, cudaEventDisableTiming));

@@ -22,6 +22,7 @@ struct FV {  // fulfilled provider candidate (scheduler.py:685-689, 711-716)
     int32_t er, idrank, i, _pad;
 };
 constexpr int FV_CAP = 1024;
+constexpr int RV_CAP = 1024;
 
 struct PlanSh {
     BlkShared b;
@@ -31,6 +32,7 @@ struct PlanSh {
     int64_t tri_key[PV_CAP];     // host triples (a_j - u_j), cached when n_tri <= PV_CAP
     int32_t tri_idx[PV_CAP], tri_taken[PV_CAP];
     int32_t n_tri_cached;
+    PV rv[RV_CAP];               // the running set's views, staged once per plan
     unsigned __int128 wsum;
     int64_t free, shortfall, runway, batch_now, gm_tokens;
     int64_t f_total, a_total, f_supply, a_supply, tbt_floor, lim, resid;
@@ -104,7 +106,7 @@ __device__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64
                          int64_t* total_out) {
     const int tid = threadIdx.x;
     int64_t tot = 0, live_tot = 0, nlive = 0;
-    for (int32_t k = tid; k < m; k += NT) {
+    for (int32_t k = tid; k < m; k += (int)blockDim.x) {
         int32_t p = grp[k];
         int64_t need = d.l_part_need[p];
         tot += need;
@@ -122,7 +124,7 @@ __device__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64
         return;
     }
     if (live_tot <= supply) {
-        for (int32_t k = tid; k < m; k += NT) {
+        for (int32_t k = tid; k < m; k += (int)blockDim.x) {
             int32_t p = grp[k];
             int64_t need = d.l_part_need[p];
             if (need > 0) d.l_part_grant[p] = (int32_t)need;
@@ -132,13 +134,13 @@ __device__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64
     }
     // live demands only, order-preserving (the ranking below is total)
     const int32_t w = blk_compact(grp, m, d.sk_item, [&](int32_t p) { return d.l_part_need[p] > 0; }, S.b);
-    for (int32_t k = tid; k < w; k += NT) grp[k] = d.sk_item[k];
+    for (int32_t k = tid; k < w; k += (int)blockDim.x) grp[k] = d.sk_item[k];
     if (tid == 0) S.wsum = 0;
     __syncthreads();
     // W = sum of weights (u128): per-thread partial sums, then one atomic-free
     // serial fold of the 32 warp totals
     unsigned __int128 part = 0;
-    for (int32_t k = tid; k < w; k += NT) part += (unsigned __int128)amort_weight(part_pv(d, S, grp[k], now));
+    for (int32_t k = tid; k < w; k += (int)blockDim.x) part += (unsigned __int128)amort_weight(part_pv(d, S, grp[k], now));
     {
         uint64_t lo = (uint64_t)part, hi = (uint64_t)(part >> 64);
 #pragma unroll
@@ -153,14 +155,14 @@ __device__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64
     __syncthreads();
     if (tid == 0) {
         unsigned __int128 W = 0;
-        for (int k = 0; k < NT / 32; k++)
+        for (int k = 0; k < (int)(blockDim.x >> 5); k++)
             W += ((unsigned __int128)(uint64_t)S.b.red[k] << 64) | (unsigned __int128)S.b.ured[k];
         S.wsum = W;
     }
     __syncthreads();
     const unsigned __int128 W = S.wsum;
     int64_t sq = 0;
-    for (int32_t k = tid; k < w; k += NT) {
+    for (int32_t k = tid; k < w; k += (int)blockDim.x) {
         const int32_t p = grp[k];
         const unsigned __int128 x = (unsigned __int128)(uint64_t)supply * amort_weight(part_pv(d, S, p, now));
         const unsigned __int128 q = x / W, r = x % W;
@@ -177,12 +179,12 @@ __device__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64
         k1 = ~d.am_rlo[p];
         k2 = (uint64_t)d.idrank[d.l_part[p]];
     }, d, S.b);
-    for (int32_t k = tid; k < left && k < w; k += NT) d.l_part_grant[grp[k]] += 1;
+    for (int32_t k = tid; k < left && k < w; k += (int)blockDim.x) d.l_part_grant[grp[k]] += 1;
     __syncthreads();
     if (tot > supply) {
         const int bs = d.bs;
         int64_t fsum = 0;
-        for (int32_t k = tid; k < w; k += NT) {
+        for (int32_t k = tid; k < w; k += (int)blockDim.x) {
             int64_t g = d.l_part_grant[grp[k]];
             fsum += (g / bs) * bs;
         }
@@ -194,7 +196,7 @@ __device__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64
             k1 = (uint64_t)d.idrank[d.l_part[p]];
             k2 = 0;
         }, d, S.b);
-        for (int32_t k = tid; k < w; k += NT) {
+        for (int32_t k = tid; k < w; k += (int)blockDim.x) {
             int32_t p = grp[k];
             int64_t g = d.l_part_grant[p];
             g = (g / bs) * bs;
@@ -227,14 +229,20 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     __syncthreads();
 
     prof_mark(d, 0);
+    const bool rcached = n_run <= RV_CAP;
+    if (rcached)
+        for (int32_t k = tid; k < n_run; k += (int)blockDim.x) S.rv[k] = view_of(d, RUN[k]);
+    __syncthreads();
+    auto RV = [&](int32_t k) -> PV { return rcached ? S.rv[k] : view_of(d, RUN[k]); };
+
     // ---- returned running (scheduler.py:142-150, 161-162) ------------------
     auto crit_rt = [&](int64_t r) { return r >= -eps && r - ti < eps; };
-    const int32_t n_nr = blk_compact(RUN, n_run, d.l_nr, [&](int32_t i) {
-        const PV v = view_of(d, i);
+    const int32_t n_nr = blk_compact_at(RUN, n_run, d.l_nr, [&](int32_t k, int32_t i) {
+        const PV v = RV(k);
         return (v.flags & PV_READY) && (v.flags & PV_RETURNED) && crit_rt(v.rt);
     }, S.b);
-    const int32_t n_nrp = blk_compact(RUN, n_run, d.l_nrp, [&](int32_t i) {
-        const PV v = view_of(d, i);
+    const int32_t n_nrp = blk_compact_at(RUN, n_run, d.l_nrp, [&](int32_t k, int32_t i) {
+        const PV v = RV(k);
         return (v.flags & PV_READY) && (v.flags & PV_RETURNED) && !crit_rt(v.rt);
     }, S.b);
     blk_sort(d.l_nr, n_nr, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
@@ -244,12 +252,12 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         int64_t r = rt_of(d, i, now);
         k0 = r < 0 ? 1 : 0; k1 = r < 0 ? (uint64_t)d.arr[i] : (uint64_t)r; k2 = (uint64_t)d.idrank[i];
     }, d, S.b);
-    for (int32_t k = tid; k < n_nr; k += NT) d.st_nr[d.l_nr[k]] = sid;
+    for (int32_t k = tid; k < n_nr; k += (int)blockDim.x) d.st_nr[d.l_nr[k]] = sid;
 
     prof_mark(d, 1);
     // ---- embedding hosts (scheduler.py:425-430) sorted by (a_j - u_j, id) --
-    const int32_t n_tri = blk_compact(RUN, n_run, d.l_tri, [&](int32_t i) {
-        const PV v = view_of(d, i);
+    const int32_t n_tri = blk_compact_at(RUN, n_run, d.l_tri, [&](int32_t k, int32_t i) {
+        const PV v = RV(k);
         return !(v.flags & PV_GUEST) && (v.flags & PV_HOLDS) && v.pre >= v.kvn;
     }, S.b);
     blk_sort(d.l_tri, n_tri, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
@@ -257,7 +265,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         k0 = (uint64_t)((int64_t)v.granted - v.used + (1ll << 40)); k1 = (uint64_t)v.idrank; k2 = 0;
     }, d, S.b);
     const bool tri_cached = n_tri <= PV_CAP;
-    for (int32_t k = tid; k < n_tri; k += NT) {
+    for (int32_t k = tid; k < n_tri; k += (int)blockDim.x) {
         int32_t h = d.l_tri[k];
         const int64_t key = (int64_t)d.granted[h] - d.used[h];
         const int32_t taken = d.guest[h] >= 0 ? 1 : 0;  // already hosting: skipped without stacking
@@ -290,12 +298,12 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     prof_mark(d, 3);
     // ---- exact-consumption demand and reserve (scheduler.py:459-472) ------
     int64_t dem = 0;
-    for (int32_t k = tid; k < n_pend0; k += NT) {
+    for (int32_t k = tid; k < n_pend0; k += (int)blockDim.x) {
         const PV v = view_of(d, d.l_pend[k]);
         int64_t need = (int64_t)v.kvn + B - v.eff;
         dem += pv_cost(v, need > 0 ? need : 0, bs);
     }
-    for (int32_t k = tid; k < n_nr; k += NT) {
+    for (int32_t k = tid; k < n_nr; k += (int)blockDim.x) {
         const PV v = view_of(d, d.l_nr[k]);
         if (!(v.flags & PV_GUEST)) dem += pv_cost(v, B, bs);
     }
@@ -311,8 +319,8 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     prof_mark(d, 4);
     // ---- victims and deferral (scheduler.py:474-507) ----------------------
     if (S.shortfall > 0) {
-        for (int32_t k = tid; k < n_pend0; k += NT) d.st_crit[d.l_pend[k]] = sid;
-        for (int32_t k = tid; k < n_nr; k += NT) d.st_crit[d.l_nr[k]] = sid;
+        for (int32_t k = tid; k < n_pend0; k += (int)blockDim.x) d.st_crit[d.l_pend[k]] = sid;
+        for (int32_t k = tid; k < n_nr; k += (int)blockDim.x) d.st_crit[d.l_nr[k]] = sid;
         __syncthreads();
         const bool fcfs = d.fcfs;
         const int32_t n_v = blk_compact(RUN, n_run, d.l_vict, [&](int32_t i) {
@@ -351,7 +359,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         }
         __syncthreads();
         if (S.shortfall > 0) {
-            for (int32_t k = tid; k < n_pend0; k += NT) d.l_defer[k] = d.l_pend[k];
+            for (int32_t k = tid; k < n_pend0; k += (int)blockDim.x) d.l_defer[k] = d.l_pend[k];
             __syncthreads();
             blk_sort(d.l_defer, n_pend0, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
                 k0 = (uint64_t)((1ll << 62) - rt_of(d, i, now)); k1 = (uint64_t)d.idrank[i]; k2 = 0;
@@ -435,8 +443,8 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
 
     prof_mark(d, 6);
     // ---- decode members in running order (scheduler.py:576-593) -----------
-    const int32_t n_dec_mem = blk_compact(RUN, n_run, d.mem_idx, [&](int32_t i) {
-        const PV v = view_of(d, i);
+    const int32_t n_dec_mem = blk_compact_at(RUN, n_run, d.mem_idx, [&](int32_t k, int32_t i) {
+        const PV v = RV(k);
         if (d.st_removed[i] == sid || !(v.flags & PV_READY) || v.pre < v.kvn) return false;
         if (v.flags & PV_RETURNED) {
             if (d.st_stalled[i] == sid) return false;
@@ -444,9 +452,9 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         }
         return true;
     }, S.b);
-    for (int32_t k = tid; k < n_dec_mem; k += NT) d.mem_tok[k] = 1;
+    for (int32_t k = tid; k < n_dec_mem; k += (int)blockDim.x) d.mem_tok[k] = 1;
     const int32_t n_gm = S.n_gm;
-    for (int32_t k = tid; k < n_gm; k += NT) {
+    for (int32_t k = tid; k < n_gm; k += (int)blockDim.x) {
         d.mem_idx[n_dec_mem + k] = d.l_gm_idx[k];
         d.mem_tok[n_dec_mem + k] = d.l_gm_tok[k];
     }
@@ -464,7 +472,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         const int64_t budget = d.token_budget;
         int64_t used_base = consumed;
         int32_t ksel = n_nwp;
-        for (int32_t base = 0; base < n_nwp; base += NT) {
+        for (int32_t base = 0; base < n_nwp; base += (int)blockDim.x) {
             int32_t k = base + tid;
             int32_t ch = 0;
             if (k < n_nwp) { const PV v = view_of(d, NWP[k]); ch = v.kvn - v.pre; }
@@ -485,7 +493,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
 
     prof_mark(d, 8);
     // ---- participants (scheduler.py:600-638) ------------------------------
-    for (int32_t k = tid; k < k_sel && k < PV_CAP; k += NT) S.pv[k] = view_of(d, NWP[k]);
+    for (int32_t k = tid; k < k_sel && k < PV_CAP; k += (int)blockDim.x) S.pv[k] = view_of(d, NWP[k]);
     __syncthreads();
     if (tid == 0) {
         for (int32_t k = 0; k < k_sel; k++) {
@@ -515,8 +523,8 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     prof_mark(d, 9);
     // proactive_include (scheduler.py:269-279) over the post-eviction running set
     const int64_t mpre = d.prealloc_m;
-    const int32_t n_pro = blk_compact(RUN, n_run, d.l_pro, [&](int32_t i) {
-        const PV v = view_of(d, i);
+    const int32_t n_pro = blk_compact_at(RUN, n_run, d.l_pro, [&](int32_t k, int32_t i) {
+        const PV v = RV(k);
         return d.st_removed[i] != sid && !(v.flags & PV_RETURNED) && v.eff < v.target && v.er <= mpre;
     }, S.b);
     blk_sort(d.l_pro, n_pro, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
@@ -536,12 +544,12 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     // pre-exhaust top-up, running order (scheduler.py:625-638)
     {
         const int32_t base = S.n_part;
-        const int32_t n_top = blk_compact(RUN, n_run, d.l_part + base, [&](int32_t i) {
-            const PV v = view_of(d, i);
+        const int32_t n_top = blk_compact_at(RUN, n_run, d.l_part + base, [&](int32_t k, int32_t i) {
+            const PV v = RV(k);
             return d.st_removed[i] != sid && !(v.flags & PV_GUEST) && (v.flags & PV_READY) && v.pre >= v.kvn &&
                    !(v.flags & PV_RETURNED) && (int64_t)v.eff - v.used <= mpre && d.st_parts[i] != sid;
         }, S.b);
-        for (int32_t k = tid; k < n_top; k += NT) {
+        for (int32_t k = tid; k < n_top; k += (int)blockDim.x) {
             const PV v = view_of(d, d.l_part[base + k]);
             int64_t t = v.target, f = (int64_t)v.used + 1 + B;
             d.l_part_need[base + k] = (int32_t)((t > f ? t : f) - v.eff);
@@ -553,7 +561,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     const int32_t n_part = S.n_part;
     prof_mark(d, 11);
     // participant views, cached
-    for (int32_t p = tid; p < n_part && p < PV_CAP; p += NT) {
+    for (int32_t p = tid; p < n_part && p < PV_CAP; p += (int)blockDim.x) {
         S.pv[p] = view_of(d, d.l_part[p]);
         S.pneed[p] = d.l_part_need[p];
     }
@@ -562,9 +570,9 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     prof_mark(d, 12);
     // ---- amortized round (scheduler.py:662-682) ---------------------------
     int64_t ndec = 0;
-    for (int32_t k = tid; k < n_run; k += NT) {
+    for (int32_t k = tid; k < n_run; k += (int)blockDim.x) {
         int32_t i = RUN[k];
-        const PV v = view_of(d, i);
+        const PV v = RV(k);
         if (d.st_removed[i] != sid && !(v.flags & PV_GUEST) && v.pre >= v.kvn) ndec++;
     }
     ndec = blk_sum(ndec, S.b);
@@ -580,7 +588,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     int64_t ftot;
     amortize(d, S, d.l_grp, n_fl, S.f_supply, now, &ftot);
     int64_t spent = 0;  // sum of the in-flight grants (amortize compacts grp in place)
-    for (int32_t p = tid; p < n_part; p += NT)
+    for (int32_t p = tid; p < n_part; p += (int)blockDim.x)
         if (part_running(p)) spent += d.l_part_grant[p];
     spent = blk_sum(spent, S.b);
     if (tid == 0) {
@@ -596,18 +604,18 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         S.a_total = atot;
         S.sated = (S.f_total <= S.f_supply && S.a_total <= S.a_supply) ? 1 : 0;
     }
-    for (int32_t p = tid; p < n_part && p < PV_CAP; p += NT) S.pgrant[p] = d.l_part_grant[p];
+    for (int32_t p = tid; p < n_part && p < PV_CAP; p += (int)blockDim.x) S.pgrant[p] = d.l_part_grant[p];
     __syncthreads();
 
     prof_mark(d, 13);
     // ---- grant application + pair-release claims (scheduler.py:684-720) ---
-    const int32_t n_ful = blk_compact(RUN, n_run, d.l_ful, [&](int32_t i) {
-        const PV v = view_of(d, i);
+    const int32_t n_ful = blk_compact_at(RUN, n_run, d.l_ful, [&](int32_t k, int32_t i) {
+        const PV v = RV(k);
         return !(v.flags & PV_GUEST) && !(v.flags & PV_RETURNED) && v.eff >= v.target && d.st_removed[i] != sid;
     }, S.b);
     const bool ful_cached = n_ful <= FV_CAP;
     if (ful_cached) {
-        for (int32_t k = tid; k < n_ful; k += NT) {
+        for (int32_t k = tid; k < n_ful; k += (int)blockDim.x) {
             const int32_t q = d.l_ful[k];
             const PV v = view_of(d, q);
             FV f;
@@ -675,7 +683,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
             if (S.search) {
                 const int64_t lim = S.lim, resid = S.resid;
                 uint64_t best = ~0ull;
-                for (int32_t k = tid; k < n_ful; k += NT) {
+                for (int32_t k = tid; k < n_ful; k += (int)blockDim.x) {
                     int32_t q = d.l_ful[k];
                     if (d.st_claimed[q] == sid) continue;
                     int64_t er = est_rem(d, q);
@@ -705,7 +713,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     // ---- case 2: extras while sated (scheduler.py:726-748) ----------------
     if (S.sated) {
         uint64_t fl = ~0ull;
-        for (int32_t k = tid; k < n_run; k += NT) {
+        for (int32_t k = tid; k < n_run; k += (int)blockDim.x) {
             int32_t x = RUN[k];
             if (d.st_removed[x] == sid || d.last_tok[x] < 0 || returned_of(d, x)) continue;
             if (d.max_tbt[x] > d.slo_tbt[x]) continue;
@@ -718,7 +726,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         __syncthreads();
         const int64_t batch_now = S.batch_now;
         const bool has_floor = fl != ~0ull;
-        for (int32_t base = k_sel; base < n_nwp && !S.stop; base += NT) {
+        for (int32_t base = k_sel; base < n_nwp && !S.stop; base += (int)blockDim.x) {
             int32_t k = base + tid;
             int64_t need = 0, cst = 0;
             if (k < n_nwp) {

@@ -33,6 +33,7 @@ def broadcast_uid(uid: bytes, group=None) -> bytes:
 
 def new_uid() -> bytes:
     import ctypes as C
+    import torch  # noqa: F401  (load torch's libnccl first; libcacheopt reuses it)
     from . import _native as N
     lib = N.load()
     buf = (C.c_uint8 * UID_BYTES)()

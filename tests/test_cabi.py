@@ -71,3 +71,17 @@ def test_unsupported_modes_are_rejected_not_emulated():
         P.Engine(reqs, P.EngineConfig(sched=P.SchedulerConfig(policy="vllm_block")))
     with pytest.raises(ValueError):
         P.Engine(reqs, P.EngineConfig(allow_stacking=True))
+
+
+def test_loading_the_library_before_torch_keeps_torch_importable():
+    # libcacheopt must not pin an NCCL older than torch's (N4 resolves NCCL lazily)
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_2503_13773_b200 import _native as N; N.load()\n"
+            "import torch; print('ok')\n") % ROOT
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_no_link_time_nccl_dependency():
+    out = subprocess.run(["ldd", str(N.LIB_PATH)], capture_output=True, text=True)
+    assert "nccl" not in out.stdout

@@ -20,7 +20,14 @@ buf = np.zeros(64, dtype=np.int64)
 N.check(eng._lib.co_phase_profile(eng._h, 1, buf.ctypes.data_as(C.POINTER(C.c_int64))), "prof")
 acc = np.zeros(64)
 K = 10
+flush = os.environ.get("FLUSH_L2") == "1"
+if flush:
+    import torch
+    scratch = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(K):
+    if flush:
+        scratch.fill_(1)
+        torch.cuda.synchronize()
     eng.step()
     N.check(eng._lib.co_phase_profile(eng._h, 0, buf.ctypes.data_as(C.POINTER(C.c_int64))), "prof")
     acc += np.diff(np.concatenate([buf[:16], buf[32:38]]).astype(np.float64), prepend=np.nan).tolist() + [0] * 42
