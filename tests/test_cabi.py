@@ -4,6 +4,7 @@ No compute calls (this runs without a GPU)."""
 import os
 import re
 import subprocess
+import sys
 import tempfile
 
 import pytest
