@@ -49,6 +49,23 @@ __device__ int64_t blk_sum(int64_t v, BlkShared& s) {
     return r;
 }
 
+// three sums in one reduction (same barrier count as one)
+__device__ void blk_sum3(int64_t& a, int64_t& b, int64_t& c, BlkShared& s) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+    a = warp_sum64(a); b = warp_sum64(b); c = warp_sum64(c);
+    if (lane == 0) { s.red[w] = a; s.ured[w] = (uint64_t)b; s.t0[w] = (uint64_t)c; }
+    __syncthreads();
+    if (w == 0) {
+        int64_t x = lane < nw ? s.red[lane] : 0, y = lane < nw ? (int64_t)s.ured[lane] : 0,
+                z = lane < nw ? (int64_t)s.t0[lane] : 0;
+        x = warp_sum64(x); y = warp_sum64(y); z = warp_sum64(z);
+        if (lane == 0) { s.red[0] = x; s.ured[0] = (uint64_t)y; s.t0[0] = (uint64_t)z; }
+    }
+    __syncthreads();
+    a = s.red[0]; b = (int64_t)s.ured[0]; c = (int64_t)s.t0[0];
+    __syncthreads();
+}
+
 __device__ uint64_t blk_min(uint64_t v, BlkShared& s) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     v = warp_min_u64(v);

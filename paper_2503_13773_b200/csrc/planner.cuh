@@ -91,6 +91,19 @@ __device__ __forceinline__ int64_t nw_need(const Dev& d, int32_t i) {  // schedu
 __device__ __forceinline__ PV part_pv(const Dev& d, const PlanSh& S, int32_t p, int64_t now) {
     return p < PV_CAP ? S.pv[p] : view_of(d, d.l_part[p]);
 }
+// exact floor(x / W) and x mod W for x = supply * w with supply < 2^31 (so
+// the quotient is < 2^31): double-precision estimate, then exact u128
+// multiply corrections (no software 128-bit division)
+__device__ __forceinline__ void divmod_small_q(unsigned __int128 x, unsigned __int128 W, uint64_t& q,
+                                               unsigned __int128& r) {
+    double est = (double)x / (double)W;
+    uint64_t qe = est < 0 ? 0 : (uint64_t)est;
+    unsigned __int128 prod = (unsigned __int128)qe * W;
+    while (prod > x) { qe--; prod -= W; }
+    while (prod + W <= x) { qe++; prod += W; }
+    q = qe;
+    r = x - prod;
+}
 __device__ __forceinline__ uint64_t amort_weight(const PV& v) {
     int64_t rt = v.rt < 1 ? 1 : v.rt;  // scheduler.py:645: max(1, rt_us), max(1, kv_need)
     int64_t pr = v.kvn < 1 ? 1 : v.kvn;
@@ -102,20 +115,99 @@ __device__ __forceinline__ uint64_t amort_weight(const PV& v) {
 // integer restatement of the Fraction arithmetic: every share has the common
 // denominator W, so floor(share_i) = q_i and the fractional order is the
 // order of r_i = supply*w_i mod W (unsigned 128-bit).
+__device__ __forceinline__ int32_t& part_need(const Dev& d, PlanSh& S, int32_t p) {
+    return p < PV_CAP ? S.pneed[p] : d.l_part_need[p];
+}
+__device__ __forceinline__ int32_t& part_grant(const Dev& d, PlanSh& S, int32_t p) {
+    return p < PV_CAP ? S.pgrant[p] : d.l_part_grant[p];
+}
+
+// amortize() for groups of at most 32 demands, entirely in warp 0 (lane =
+// demand): same exact integer arithmetic, ranks by pairwise shuffles, one
+// block barrier at the end.
+__device__ void amortize_warp(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64_t supply, int64_t now,
+                              int64_t* total_out) {
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 32) {
+        const bool in = lane < m;
+        const int32_t p = in ? grp[lane] : 0;
+        const int64_t need = in ? part_need(d, S, p) : 0;
+        const bool live = in && need > 0;
+        int64_t tot = need, live_tot = live ? need : 0, nlive = live ? 1 : 0;
+        tot = warp_sum64(tot); live_tot = warp_sum64(live_tot); nlive = warp_sum64(nlive);
+        int64_t g = 0;
+        if (nlive > 0 && supply > 0) {
+            if (live_tot <= supply) {
+                g = live ? need : 0;
+            } else {
+                const PV v = live ? part_pv(d, S, p, now) : PV{};
+                const uint64_t w = live ? amort_weight(v) : 0;
+                // W = sum w (u128)
+                uint64_t lo = w, hi = 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    uint64_t lo2 = __shfl_xor_sync(0xffffffffu, lo, o), hi2 = __shfl_xor_sync(0xffffffffu, hi, o);
+                    uint64_t nl = lo + lo2;
+                    hi = hi + hi2 + (nl < lo ? 1 : 0);
+                    lo = nl;
+                }
+                const unsigned __int128 W = ((unsigned __int128)hi << 64) | lo;
+                uint64_t q = 0;
+                unsigned __int128 r = 0;
+                if (live) divmod_small_q((unsigned __int128)(uint64_t)supply * w, W, q, r);
+                g = (int64_t)q;
+                const int64_t left = supply - warp_sum64(g);
+                const uint64_t rhi = (uint64_t)(r >> 64), rlo = (uint64_t)r;
+                const uint32_t id = live ? (uint32_t)v.idrank : 0xffffffffu;
+                // rank by (-r, id) among live lanes
+                int32_t rank = 0;
+                for (int j = 0; j < 32; j++) {
+                    const uint64_t jhi = __shfl_sync(0xffffffffu, rhi, j), jlo = __shfl_sync(0xffffffffu, rlo, j);
+                    const uint32_t jid = __shfl_sync(0xffffffffu, id, j);
+                    const bool jlive = __shfl_sync(0xffffffffu, live ? 1 : 0, j);
+                    const bool before = jhi > rhi || (jhi == rhi && (jlo > rlo || (jlo == rlo && jid < id)));
+                    rank += (jlive && before) ? 1 : 0;
+                }
+                if (live && rank < left) g += 1;
+                if (tot > supply) {
+                    const int bs = d.bs;
+                    const int64_t fl = (g / bs) * bs;
+                    const int64_t left_blocks = (supply - warp_sum64(live ? fl : 0)) / bs;
+                    const uint64_t rem = (uint64_t)(g - fl);
+                    int32_t rk = 0;
+                    for (int j = 0; j < 32; j++) {
+                        const uint64_t jr = __shfl_sync(0xffffffffu, rem, j);
+                        const uint32_t jid = __shfl_sync(0xffffffffu, id, j);
+                        const bool jlive = __shfl_sync(0xffffffffu, live ? 1 : 0, j);
+                        rk += (jlive && (jr > rem || (jr == rem && jid < id))) ? 1 : 0;
+                    }
+                    g = fl + ((live && rk < left_blocks) ? bs : 0);
+                }
+                if (!live) g = 0;
+            }
+        }
+        if (in) part_grant(d, S, p) = (int32_t)g;
+        if (lane == 0) S.b.red[0] = tot;
+    }
+    __syncthreads();
+    *total_out = S.b.red[0];
+    __syncthreads();
+}
+
 __device__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64_t supply, int64_t now,
                          int64_t* total_out) {
     const int tid = threadIdx.x;
+    if (m == 0) { *total_out = 0; return; }  // block-uniform: nothing to split
+    if (m <= 32) { amortize_warp(d, S, grp, m, supply, now, total_out); return; }
     int64_t tot = 0, live_tot = 0, nlive = 0;
     for (int32_t k = tid; k < m; k += (int)blockDim.x) {
         int32_t p = grp[k];
-        int64_t need = d.l_part_need[p];
+        int64_t need = part_need(d, S, p);
         tot += need;
         if (need > 0) { live_tot += need; nlive += 1; }
-        d.l_part_grant[p] = 0;
+        part_grant(d, S, p) = 0;
     }
-    tot = blk_sum(tot, S.b);
-    live_tot = blk_sum(live_tot, S.b);
-    nlive = blk_sum(nlive, S.b);
+    blk_sum3(tot, live_tot, nlive, S.b);
     *total_out = tot;
     if (nlive == 0) return;
     if (supply == 0) {
@@ -126,14 +218,14 @@ __device__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64
     if (live_tot <= supply) {
         for (int32_t k = tid; k < m; k += (int)blockDim.x) {
             int32_t p = grp[k];
-            int64_t need = d.l_part_need[p];
-            if (need > 0) d.l_part_grant[p] = (int32_t)need;
+            int64_t need = part_need(d, S, p);
+            if (need > 0) part_grant(d, S, p) = (int32_t)need;
         }
         __syncthreads();
         return;
     }
     // live demands only, order-preserving (the ranking below is total)
-    const int32_t w = blk_compact(grp, m, d.sk_item, [&](int32_t p) { return d.l_part_need[p] > 0; }, S.b);
+    const int32_t w = blk_compact(grp, m, d.sk_item, [&](int32_t p) { return part_need(d, S, p) > 0; }, S.b);
     for (int32_t k = tid; k < w; k += (int)blockDim.x) grp[k] = d.sk_item[k];
     if (tid == 0) S.wsum = 0;
     __syncthreads();
@@ -164,10 +256,11 @@ __device__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64
     int64_t sq = 0;
     for (int32_t k = tid; k < w; k += (int)blockDim.x) {
         const int32_t p = grp[k];
-        const unsigned __int128 x = (unsigned __int128)(uint64_t)supply * amort_weight(part_pv(d, S, p, now));
-        const unsigned __int128 q = x / W, r = x % W;
-        d.l_part_grant[p] = (int32_t)(uint64_t)q;
-        sq += (int64_t)(uint64_t)q;
+        uint64_t q;
+        unsigned __int128 r;
+        divmod_small_q((unsigned __int128)(uint64_t)supply * amort_weight(part_pv(d, S, p, now)), W, q, r);
+        part_grant(d, S, p) = (int32_t)q;
+        sq += (int64_t)q;
         d.am_rhi[p] = (uint64_t)(r >> 64);
         d.am_rlo[p] = (uint64_t)r;
     }
@@ -179,29 +272,29 @@ __device__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64
         k1 = ~d.am_rlo[p];
         k2 = (uint64_t)d.idrank[d.l_part[p]];
     }, d, S.b);
-    for (int32_t k = tid; k < left && k < w; k += (int)blockDim.x) d.l_part_grant[grp[k]] += 1;
+    for (int32_t k = tid; k < left && k < w; k += (int)blockDim.x) part_grant(d, S, grp[k]) += 1;
     __syncthreads();
     if (tot > supply) {
         const int bs = d.bs;
         int64_t fsum = 0;
         for (int32_t k = tid; k < w; k += (int)blockDim.x) {
-            int64_t g = d.l_part_grant[grp[k]];
+            int64_t g = part_grant(d, S, grp[k]);
             fsum += (g / bs) * bs;
         }
         fsum = blk_sum(fsum, S.b);
         const int64_t left_blocks = (supply - fsum) / bs;
         blk_sort(grp, w, [&](int32_t p, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
-            int64_t g = d.l_part_grant[p];
+            int64_t g = part_grant(d, S, p);
             k0 = 0x7fffffffull - (uint64_t)(g - (g / bs) * bs);
             k1 = (uint64_t)d.idrank[d.l_part[p]];
             k2 = 0;
         }, d, S.b);
         for (int32_t k = tid; k < w; k += (int)blockDim.x) {
             int32_t p = grp[k];
-            int64_t g = d.l_part_grant[p];
+            int64_t g = part_grant(d, S, p);
             g = (g / bs) * bs;
             if (k < left_blocks) g += bs;
-            d.l_part_grant[p] = (int32_t)g;
+            part_grant(d, S, p) = (int32_t)g;
         }
         __syncthreads();
     }
@@ -576,6 +669,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         if (d.st_removed[i] != sid && !(v.flags & PV_GUEST) && v.pre >= v.kvn) ndec++;
     }
     ndec = blk_sum(ndec, S.b);
+    prof_mark(d, 16);
     auto part_running = [&](int32_t p) { return (part_pv(d, S, p, now).flags & PV_RUNNING) != 0; };
     const int32_t n_fl = blk_compact(nullptr, n_part, d.l_grp, [&](int32_t p) { return part_running(p); }, S.b);
     const int32_t n_ad = blk_compact(nullptr, n_part, d.l_grp + n_part, [&](int32_t p) { return !part_running(p); },
@@ -585,11 +679,13 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         S.f_supply = (S.free / bs) * bs;  // free >= 0 throughout planning
     }
     __syncthreads();
+    prof_mark(d, 17);
     int64_t ftot;
     amortize(d, S, d.l_grp, n_fl, S.f_supply, now, &ftot);
+    prof_mark(d, 18);
     int64_t spent = 0;  // sum of the in-flight grants (amortize compacts grp in place)
     for (int32_t p = tid; p < n_part; p += (int)blockDim.x)
-        if (part_running(p)) spent += d.l_part_grant[p];
+        if (part_running(p)) spent += part_grant(d, S, p);
     spent = blk_sum(spent, S.b);
     if (tid == 0) {
         int64_t a = S.free - spent - S.runway;
@@ -598,13 +694,14 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         S.f_total = ftot;
     }
     __syncthreads();
+    prof_mark(d, 19);
     int64_t atot;
     amortize(d, S, d.l_grp + n_part, n_ad, S.a_supply, now, &atot);
+    prof_mark(d, 20);
     if (tid == 0) {
         S.a_total = atot;
         S.sated = (S.f_total <= S.f_supply && S.a_total <= S.a_supply) ? 1 : 0;
     }
-    for (int32_t p = tid; p < n_part && p < PV_CAP; p += (int)blockDim.x) S.pgrant[p] = d.l_part_grant[p];
     __syncthreads();
 
     prof_mark(d, 13);
@@ -633,7 +730,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         const PV v = part_pv(d, S, p, now);
         const int32_t i = v.i;
         const int64_t need = p < PV_CAP ? S.pneed[p] : d.l_part_need[p];
-        const int64_t g = p < PV_CAP ? S.pgrant[p] : d.l_part_grant[p];
+        const int64_t g = part_grant(d, S, p);
         const int64_t eff = v.eff;
         if (!(v.flags & PV_RUNNING)) {
             if (eff + g < (int64_t)v.kvn + 1) return false;  // a partial grant that cannot start prefill
