@@ -11,8 +11,8 @@
 
 namespace co {
 
-constexpr int NT = 1024;
-constexpr int TCHUNK = 64;        // pages per block-table chunk           // threads of the single-CTA planner / apply kernels
+constexpr int NT = 256;   // threads of the single-CTA planner / apply kernels (max; 256 measured best)
+constexpr int TCHUNK = 64;  // pages per block-table chunk
 constexpr int ST_PENDING = CO_PENDING, ST_WAITING = CO_WAITING, ST_RUNNING = CO_RUNNING,
               ST_PREEMPTED = CO_PREEMPTED, ST_COMPLETED = CO_COMPLETED;
 
