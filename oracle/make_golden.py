@@ -112,17 +112,30 @@ def run_and_store(name, params, reqs, cfg, steps=None, keep_events=True, store_t
 def main():
     sys.path.insert(0, REF)
     from tests.cases import case_params
+    only = set(sys.argv[1:])
     for s in SEEDS:
+        if only and f"case{s:02d}" not in only:
+            continue
         p = case_params(s)
         reqs, cfg = ref_build(p)
         run_and_store(f"case{s:02d}", p, reqs, cfg)
     # config 2 window: 65,536 requests, first 60 steps (digest + final state only)
+    if only and not only & {"config2_60", "config1", "config3"}:
+        return
     p = {"seed": 0, "trace": {"kind": "preset", "preset": "sharegpt", "num_requests": 65536,
                                "arrival_rate": 1e6},
          "slo": [2_000_000, 200_000], "capacity": 166_400, "reserved": 8, "truth": None, "pred": {},
          "sched": {"small_block_b": 16}, "fixed_confidence": None, "validate_every": 0}
     reqs, cfg = ref_build(p)
     run_and_store("config2_60", p, reqs, cfg, steps=60, keep_events=False, store_trace=False)
+    # BASELINE configs 1 and 3, full runs, with the reference's own calibrated SLO baselines
+    from tests.cases import CONFIG1_SLO, CONFIG3_SLO
+    for name, rate, cap, bs, slo in (("config1", 4.0, 53_696, 8, CONFIG1_SLO), ("config3", 8.0, 8_192, 16, CONFIG3_SLO)):
+        p = {"seed": 0, "trace": {"kind": "preset", "preset": "sharegpt", "num_requests": 1000, "arrival_rate": rate},
+             "slo": list(slo), "capacity": cap, "reserved": 8, "truth": None, "pred": {},
+             "sched": {"small_block_b": bs}, "fixed_confidence": None, "validate_every": 0}
+        reqs, cfg = ref_build(p)
+        run_and_store(name, p, reqs, cfg, keep_events=False, store_trace=False)
 
 
 if __name__ == "__main__":

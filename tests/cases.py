@@ -99,3 +99,34 @@ def final_arrays(eng) -> dict:
         predicted=f("PREDICTED"), estimated=f("ESTIMATED"), holds=f("HOLDS"),
         granted=np.where(f("HOLDS") == 1, f("GRANTED"), 0),
     )
+
+
+# SLO baselines of BASELINE configs 1 and 3 from the reference's own
+# calibrate_slo_baselines (engine.py:675-699, a vllm_block run), computed in
+# the development container (tests/test_oracle_vs_reference_live.py re-derives them)
+CONFIG1_SLO = (9141, 5070)
+CONFIG3_SLO = (9674, 5140)
+
+
+def config1(seed: int = 0, error: bool = False):
+    """BASELINE config 1: ShareGPT 1K requests @4 req/s, OPT-13B-sized pool
+    53,696 tokens, B = 8, reserve 8 blocks, CacheOPT; optionally the uniform
+    +-24 predictor error used to exercise under-prediction."""
+    import paper_2503_13773_b200 as P
+    reqs = P.generate(P.PRESETS["sharegpt"].sized(1000, 4.0), seed)
+    P.assign_slos(reqs, CONFIG1_SLO[0], CONFIG1_SLO[1], P.SloPolicy(), seed)
+    pred = P.PredictorConfig(error_dist="uniform", error_scale=24) if error else P.PredictorConfig()
+    cfg = P.EngineConfig(capacity_tokens=53_696, reserved_blocks=8, sched=P.SchedulerConfig(small_block_b=8),
+                         predictor=pred, seed=seed)
+    return reqs, cfg
+
+
+def config3(seed: int = 0):
+    """BASELINE config 3: the 2x-rate heavy-preemption regime (ShareGPT 1K @8
+    req/s, 8,192-token pool, 16-token blocks)."""
+    import paper_2503_13773_b200 as P
+    reqs = P.generate(P.PRESETS["sharegpt"].sized(1000, 8.0), seed)
+    P.assign_slos(reqs, CONFIG3_SLO[0], CONFIG3_SLO[1], P.SloPolicy(), seed)
+    cfg = P.EngineConfig(capacity_tokens=8_192, reserved_blocks=8, sched=P.SchedulerConfig(small_block_b=16),
+                         seed=seed)
+    return reqs, cfg

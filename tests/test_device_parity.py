@@ -82,3 +82,17 @@ def test_step_result_members_match_iter_events(cuda_ok, seed):
     orc = CacheOptOracle(reqs, cfg)
     orc.run()
     assert eng.events == orc.events
+
+
+@pytest.mark.parametrize("which", ["config1", "config1_err", "config3"])
+def test_baseline_configs_full_run(cuda_ok, which):
+    """BASELINE.json configs 1 and 3 end to end (tens of thousands of steps)."""
+    from paper_2503_13773_b200 import Engine
+    from tests.cases import config1, config3
+    reqs, cfg = {"config1": lambda: config1(), "config1_err": lambda: config1(error=True),
+                 "config3": lambda: config3()}[which]()
+    eng = Engine(reqs, cfg, steps_per_launch=64)
+    eng.run_steps(0)
+    orc = CacheOptOracle(reqs, cfg)
+    orc.run()
+    _compare(eng, orc, which)

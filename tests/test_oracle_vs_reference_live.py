@@ -26,3 +26,15 @@ def test_oracle_matches_live_reference(seed):
     assert orc.events == eng.events
     for k, rid in enumerate(orc.rid):
         assert orc.token_times[k] == eng.runtimes[rid].token_times_us
+
+
+def test_config_slo_baselines_match_reference_calibration():
+    import copy
+    sys.path.insert(0, REFERENCE_SRC)
+    from kvcsim.engine import EngineConfig, calibrate_slo_baselines
+    from kvcsim.scheduler import SchedulerConfig
+    from kvcsim.workload import PRESETS, generate
+    from tests.cases import CONFIG1_SLO
+    reqs = generate(PRESETS["sharegpt"].sized(1000, 4.0), 0)
+    cfg = EngineConfig(capacity_tokens=53_696, reserved_blocks=8, sched=SchedulerConfig(small_block_b=8), seed=0)
+    assert calibrate_slo_baselines(copy.deepcopy(reqs), cfg) == CONFIG1_SLO
