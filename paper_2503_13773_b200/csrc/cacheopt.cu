@@ -190,7 +190,6 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
         ncclResult_t nr = nccl().allReduce(E->red, E->red + 2, 2, ncclInt64, ncclSum, E->comm, E->side);
         if (nr != ncclSuccess) return fail(CO_ECUDA, std::string("ncclAllReduce: ") + nccl().errorString(nr));
         cudaEventRecord(E->join, E->side);
-        E->reduce_calls++;
     }
     if (d.dp.on) {
         k_data<<<E->sms, 512, 0, s>>>(d, d.dp, d.dctl, 0);
@@ -596,6 +595,18 @@ static int check_device_error(co_engine* E) {
     return fail(CO_EDEVICE, buf);
 }
 
+// Drain the append buffers before a single step when its worst case could
+// overflow them, so the step never pauses (a paused-and-retried step would
+// enqueue one extra all-reduce on this rank only when a communicator is attached).
+static int predrain(co_engine* E) {
+    const Ctl& c = *E->h_ctl;
+    const int64_t need_ev = 5 * E->n + 16, need_mem = E->n + 16;
+    if (c.ev_count + need_ev > E->d.ev_cap || c.mem_count + need_mem > E->d.mem_cap ||
+        c.sample_count + 1 > E->d.sample_cap)
+        return drain_device(E);
+    return CO_OK;
+}
+
 static int ensure_step_graph(co_engine* E) {
     if (E->graph1) return CO_OK;
     cudaGraph_t g;
@@ -623,10 +634,12 @@ int co_step_result(co_engine* E, int32_t* result, int32_t* members, int64_t max_
         if (E->graph1) { cudaGraphExecDestroy(E->graph1); E->graph1 = nullptr; }
     }
     if ((r = ensure_step_graph(E))) return r;
+    if ((r = predrain(E))) return r;
     const int32_t* res = static_cast<const int32_t*>(E->result_host);
     for (int attempt = 0; attempt < 3; attempt++) {
         CK(cudaEventRecord(E->ev0, E->stream));
         CK(cudaGraphLaunch(E->graph1, E->stream));
+        if (E->comm) E->reduce_calls += 1;
         CK(cudaEventRecord(E->ev1, E->stream));
         if ((r = sync_ctl(E))) return r;
         float ms = 0;
@@ -634,6 +647,7 @@ int co_step_result(co_engine* E, int32_t* result, int32_t* members, int64_t max_
         E->last_ms = ms;
         if ((r = check_device_error(E))) return r;
         if (E->h_ctl->paused) {
+            if (E->comm) return fail(CO_EDEVICE, "step paused with a communicator attached");
             if ((r = drain_device(E))) return r;
             continue;
         }
@@ -652,9 +666,11 @@ int co_step(co_engine* E, int32_t* result) {
     if (!E || !result) return fail(CO_EINVAL, "null argument");
     int r = ensure_step_graph(E);
     if (r) return r;
+    if ((r = predrain(E))) return r;
     for (int attempt = 0; attempt < 3; attempt++) {
         CK(cudaEventRecord(E->ev0, E->stream));
         CK(cudaGraphLaunch(E->graph1, E->stream));
+        if (E->comm) E->reduce_calls += 1;
         CK(cudaEventRecord(E->ev1, E->stream));
         if ((r = sync_ctl(E))) return r;
         float ms = 0;
@@ -662,6 +678,7 @@ int co_step(co_engine* E, int32_t* result) {
         E->last_ms = ms;
         if ((r = check_device_error(E))) return r;
         if (E->h_ctl->paused) {
+            if (E->comm) return fail(CO_EDEVICE, "step paused with a communicator attached");
             if ((r = drain_device(E))) return r;
             continue;
         }
@@ -692,16 +709,23 @@ int co_run(co_engine* E, int64_t max_steps, int32_t K, int64_t* steps_done) {
         E->graph_k = K;
     }
     double total_ms = 0;
+    // With a communicator every rank must enqueue the same number of steps
+    // (each carries one all-reduce), so progress is counted in launched steps
+    // there, and in executed steps otherwise.
+    int64_t launched = 0;
     while (true) {
-        int64_t done_steps = E->h_ctl->steps - steps0;
+        const int64_t done_steps = E->comm ? launched : E->h_ctl->steps - steps0;
         if (max_steps > 0 && done_steps >= max_steps) break;
-        bool single = max_steps > 0 && max_steps - done_steps < K;
+        const bool single = max_steps > 0 && max_steps - done_steps < K;
         CK(cudaEventRecord(E->ev0, E->stream));
         if (single) {
             if ((r = launch_step(E, 1))) return r;
+            launched += 1;
         } else {
             CK(cudaGraphLaunch(E->graph, E->stream));
+            launched += K;
         }
+        if (E->comm) E->reduce_calls += single ? 1 : K;
         CK(cudaEventRecord(E->ev1, E->stream));
         if ((r = sync_ctl(E))) return r;
         float ms = 0;
@@ -712,7 +736,7 @@ int co_run(co_engine* E, int64_t max_steps, int32_t K, int64_t* steps_done) {
             if ((r = drain_device(E))) return r;
             continue;
         }
-        if (E->h_ctl->done && !(E->comm && max_steps > 0)) break;
+        if (E->h_ctl->done && !E->comm) break;
     }
     E->last_ms = total_ms;
     if (steps_done) *steps_done = E->h_ctl->steps - steps0;
@@ -868,6 +892,7 @@ int co_time_steps(co_engine* E, int32_t k, int64_t flush_bytes, double* step_ms,
     if (!r) {
         CK(cudaGraphInstantiate(&ge, g, 0));
         CK(cudaGraphLaunch(ge, E->stream));
+        if (E->comm) E->reduce_calls += k;
         CK(cudaStreamSynchronize(E->stream));
         for (int q = 0; q < CO_NSTAGES; q++) stage_ms[q] = 0;
         for (int32_t j = 0; j < k; j++) {

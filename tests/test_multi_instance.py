@@ -82,3 +82,22 @@ def test_one_rank_nccl_reserve_matches_instance(cuda_ok):
         orc.step()
     assert eng.events == orc.events  # telemetry never changes a decision
     assert eng.global_reserve()[2] > 0
+
+
+@pytest.mark.gpu
+def test_collective_mode_runs_fixed_step_counts_past_the_end(cuda_ok):
+    # with a communicator every rank must enqueue the same number of steps even
+    # after its own shard finished (an early-finishing rank must not hang others)
+    from paper_2503_13773_b200 import Engine
+    from paper_2503_13773_b200.multi import attach_global_reserve
+    from tests.cases import build_product, case_params
+    reqs, cfg = build_product(case_params(2))
+    eng = Engine(reqs, cfg, steps_per_launch=16)
+    orc = CacheOptOracle(reqs, cfg)
+    total = orc.run()
+    attach_global_reserve(eng, 0, 1)
+    eng.run_steps(total + 100)
+    free, rsv, calls = eng.global_reserve()
+    assert calls >= total + 100
+    assert eng.events == orc.events
+    assert eng.step_result()[0] is False  # finished, and still enqueues its collective
