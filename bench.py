@@ -117,8 +117,10 @@ def stage_bytes(n: int, live: int, stage: str, running: int = 0) -> int:
         # every slot: state (1 B) read + key (8 B) and value (4 B) written;
         # every live request: deadline inputs (3 x 8 B) + id rank (4 B) read
         return n * 13 + live * 28
-    if stage == "sort":
-        return n * 24  # one read and one write of (u64 key, u32 value)
+    if stage == "bucket":
+        # k_bins: bin tag (4 B) per slot read, key (8 B) read + tag written per
+        # waiting request; k_scatter: tag per slot read, bucket slot written
+        return n * 8 + live * 16
     return 0
 
 
@@ -344,7 +346,7 @@ def device_arm(args, rank, world, dist):
                      "frac": ach / peak if peak else None, "traffic": None,
                      "peak_kind": peak_kind, "algorithmic_bytes_per_launch": algo,
                      "note": "the step's dominant stages are single-CTA ordered greedy phases (scheduler.py "
-                             "loops) and a 65,536-key sort: latency-bound, so the HBM fraction is ~0 by "
+                             "loops) and deadline bucketing: latency-bound, so the HBM fraction is ~0 by "
                              "construction; classify (grid) and the decode leg carry the bandwidth rooflines"},
         "cpu_baseline": {"value": cpu_val, "unit": UNIT, "cores": 1, "kind": "port",
                          "sample": f"oracle port, config-2 steps {WINDOW_START}..{WINDOW_START + cpu_steps - 1} "
@@ -355,7 +357,7 @@ def device_arm(args, rank, world, dist):
                        "members read back every step), K steps after the window; trace uploaded once at "
                        "construction"},
         "gpu_launches": args.steps * 6,
-        "gpu_launches_note": "6 own kernels per step (begin, admit, classify, plan, apply, check) + CUB onesweep sort kernels",
+        "gpu_launches_note": "6 own kernels per step (begin+admit, classify, bins, scatter, plan, apply+check); no library kernels",
         "clocks": clocks.summary(),
         "collective": coll,
         **extra,

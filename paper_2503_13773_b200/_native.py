@@ -14,7 +14,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libcacheopt.so"
 CO_OK, CO_EINVAL, CO_ECUDA, CO_EDEVICE = 0, 1, 2, 3
 MAX_SLO_EDGES = 8
 NSTAGES = 8
-STAGES = ("begin+admit", "classify", "sort", "plan", "apply", "check", "data", "decode")
+STAGES = ("begin+admit", "classify", "bucket", "plan", "apply", "check", "data", "decode")
 
 EV_ARRIVE, EV_ADMIT, EV_ITER, EV_PREEMPT, EV_READMIT, EV_COMPLETE = range(6)
 CAUSES = ("plan", "squeeze", "collision")

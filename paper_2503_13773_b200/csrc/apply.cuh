@@ -56,8 +56,8 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
     const int64_t now = c.now;
     const int32_t sid = c.sid;
     const PlanHdr& P = *d.plan;
-    const int32_t n_nw = c.cnt_nw, n_nwp = c.cnt_nwp, n_run = c.cnt_run;
-    const int32_t* RUN = reinterpret_cast<const int32_t*>(d.vals_out) + n_nw + n_nwp;
+    const int32_t n_run = c.cnt_run;
+    const int32_t* RUN = d.l_run;  // running set in arrival order (built by k_plan)
 
     prof_mark(d, 32);
     if (tid == 0) {

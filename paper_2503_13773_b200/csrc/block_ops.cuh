@@ -111,6 +111,20 @@ __device__ int32_t blk_excl_scan(int32_t v, int32_t* total, BlkShared& s) {
     return r;
 }
 
+// In-place exclusive prefix sum of a[0..n) in shared memory (any n); returns
+// the total to every thread.
+__device__ int32_t blk_scan_smem(int32_t* a, int32_t n, BlkShared& s) {
+    const int32_t bd = (int32_t)blockDim.x, per = (n + bd - 1) / bd;
+    const int32_t lo = threadIdx.x * per, hi = min(n, lo + per);
+    int32_t t = 0;
+    for (int32_t k = lo; k < hi; k++) t += a[k];
+    int32_t total;
+    int32_t run = blk_excl_scan(t, &total, s);
+    for (int32_t k = lo; k < hi; k++) { const int32_t v = a[k]; a[k] = run; run += v; }
+    __syncthreads();
+    return total;
+}
+
 // Order-preserving compaction of src[0..m) (or of 0..m when src == nullptr)
 // by predicate pred(item) into dst, returning the count (all threads).
 template <class Pred>
@@ -219,6 +233,31 @@ __device__ void blk_sort(int32_t* items, int32_t m, KeyFn kf, const Dev& d, BlkS
             int32_t k = base + q * (int)blockDim.x + threadIdx.x;
             if (k < m) items[rank[q]] = d.sk_item[k];
         }
+    }
+    __syncthreads();
+}
+
+// blk_sort for a unique 64-bit key; the small case compares one word
+template <class KeyFn>
+__device__ void blk_sort_u64(int32_t* items, int32_t m, KeyFn kf, const Dev& d, BlkShared& s) {
+    if (m <= 1) return;
+    if (m > BlkShared::TILE) {
+        blk_sort(items, m, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
+            k0 = kf(i); k1 = 0; k2 = 0;
+        }, d, s);
+        return;
+    }
+    for (int32_t k = threadIdx.x; k < m; k += (int)blockDim.x) {
+        const int32_t it = items[k];
+        s.t0[k] = kf(it);
+        s.it[k] = it;
+    }
+    __syncthreads();
+    for (int32_t k = threadIdx.x; k < m; k += (int)blockDim.x) {
+        const uint64_t a0 = s.t0[k];
+        int32_t rank = 0;
+        for (int32_t j = 0; j < m; j++) rank += s.t0[j] < a0 ? 1 : 0;
+        items[rank] = s.it[k];
     }
     __syncthreads();
 }

@@ -2,14 +2,15 @@
 // include/cacheopt.h.  One translation unit so every device helper inlines.
 //
 // Per engine step the stream runs:
-//   k_begin (1 thread)  -> k_admit (grid) -> k_classify (grid)
-//   -> cub::DeviceRadixSort (one 64-bit composite key per request)
-//   -> k_plan (1 CTA x 1024) -> k_apply (1 CTA x 1024) -> k_check (1 CTA, gated)
+//   k_begin (guards + admission window) -> k_classify (grid: views, classes,
+//   block-ordered running/blown lists, N'_w keys) -> k_bins + k_scatter (grid:
+//   range-adaptive deadline buckets) -> k_plan (1 CTA x 256) -> k_apply
+//   (1 CTA x 256, gated invariant check inside) [-> NCCL reserve all-reduce
+//   on a side stream] [-> k_data -> k_decode_tc + k_decode_reduce]
 // co_run captures `steps_per_launch` steps into one CUDA graph and relaunches
 // it; every kernel early-exits once the device control block says the run is
 // done or paused (an append buffer needs draining), so no host round trip is
 // needed inside a launch.
-#include <cub/device/device_radix_sort.cuh>
 #include <nccl.h>
 #include <dlfcn.h>
 
@@ -101,8 +102,6 @@ struct co_engine {
     int device = 0;
     cudaStream_t stream = nullptr;
     std::vector<void*> allocs;
-    void* cub_tmp = nullptr;
-    size_t cub_bytes = 0;
     Ctl* h_ctl = nullptr;  // pinned mirror
     cudaGraphExec_t graph = nullptr;
     int32_t graph_k = 0;
@@ -170,12 +169,10 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
     if (ev) mark(ev[0], s);
     k_begin<<<1, 32, 0, s>>>(d, guard);
     if (ev) mark(ev[1], s);
-    k_classify<<<E->grid, 256, 0, s>>>(d);
+    k_classify<<<d.nblk, 256, 0, s>>>(d);
     if (ev) mark(ev[2], s);
-    size_t bytes = E->cub_bytes;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(E->cub_tmp, bytes, d.keys_in, d.keys_out, d.vals_in,
-                                                    d.vals_out, (int)E->n, 0, d.key_bits, s);
-    if (e != cudaSuccess) return fail(CO_ECUDA, std::string("radix sort: ") + cudaGetErrorString(e));
+    k_bins<<<E->grid, 256, 0, s>>>(d);
+    k_scatter<<<E->grid, 256, 0, s>>>(d);
     if (ev) mark(ev[3], s);
     k_plan<<<1, E->plan_threads, sizeof(PlanSh), s>>>(d);
     if (ev) mark(ev[4], s);
@@ -277,7 +274,6 @@ int co_destroy(co_engine* E) {
     if (E->red) cudaFree(E->red);
     if (E->d.prof) cudaFree(E->d.prof);
     for (void* p : E->allocs) cudaFree(p);
-    if (E->cub_tmp) cudaFree(E->cub_tmp);
     if (E->host_pool) cudaFreeHost(E->host_pool);
     if (E->h_ctl) cudaFreeHost(E->h_ctl);
     if (E->ev0) cudaEventDestroy(E->ev0);
@@ -352,11 +348,9 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     while ((1ll << idbits) < n) idbits++;
     double max_iter_ms = cfg->iter_base_ms + cfg->iter_per_token_ms * (double)tot_tokens;
     double bound = std::max((double)maxD, (double)horizon + max_iter_ms * 1000.0 + 2.0 + (double)max_tbt_slo);
-    int timebits = 1;
-    while (timebits < 61 && std::ldexp(1.0, timebits) <= bound) timebits++;
-    if (bound >= std::ldexp(1.0, timebits)) return fail(CO_EINVAL, "trace time range exceeds the sort-key budget");
-    // class(2) | blown(1) | time-or-index; id ties by the stable sort's input order
-    const int key_bits = 3 + std::max(timebits, idbits);
+    // non-blown N'_w key = deadline << idbits | id rank (unique u64)
+    if (bound >= std::ldexp(1.0, 62 - idbits)) return fail(CO_EINVAL, "trace time range exceeds the key budget");
+    const int key_bits = 64;
 
     co_engine* E = new co_engine();
     E->n = n;
@@ -425,7 +419,17 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     AL(d.st_nr, n); AL(d.st_crit, n); AL(d.st_removed, n); AL(d.st_embedded, n); AL(d.st_resumed, n);
     AL(d.st_stalled, n); AL(d.st_parts, n); AL(d.st_claimed, n); AL(d.st_failed, n); AL(d.seen64, n);
     AL(d.st_acted, n); AL(d.st_deferred, n);
-    AL(d.keys_in, n); AL(d.keys_out, n); AL(d.vals_in, n); AL(d.vals_out, n);
+    {
+        int64_t nb = std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8));
+        int64_t chunk = ((n + nb - 1) / nb + 255) / 256 * 256;
+        if (chunk < 256) chunk = 256;
+        nb = std::max<int64_t>(1, (n + chunk - 1) / chunk);
+        d.nblk = (int32_t)nb;
+        d.chunk = (int32_t)chunk;
+    }
+    AL(d.run_tmp, n); AL(d.blown_tmp, n); AL(d.blk_cnt, 2 * d.nblk + 2); AL(d.crit_idx, n); AL(d.key0, n);
+    AL(d.f0_bin, n); AL(d.hist, NBIN); AL(d.fill, NBIN); AL(d.bin_off, NBIN + 1); AL(d.bucket, n); AL(d.grp_end, n / GRP + 2);
+    AL(d.l_run, n); AL(d.l_blown, n); AL(d.l_nw, n); AL(d.l_nwp, n);
     AL(d.plan, 1);
     AL(d.mem_idx, n3); AL(d.mem_tok, n3);
     AL(d.act_kind, n3); AL(d.act_idx, n3); AL(d.act_tok, n3); AL(d.act_nb, n3); AL(d.act_host, n3); AL(d.act_start, n3);
@@ -531,6 +535,8 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     for (int64_t* p : {d.max_tbt, d.ready_at, d.pstart, d.swap_done, d.ptime, d.rec_seq}) memset_all(p, 0, n8);
     for (int64_t* p : {d.first_tok, d.last_tok, d.first_start, d.completion}) memset_all(p, 0xff, n8);
     memset_all(d.holds, 0, n);
+    memset_all(d.hist, 0, NBIN * 4);
+    memset_all(d.fill, 0, NBIN * 4);
     memset_all(d.seen64, 0, n8);
     memset_all(d.dctl, 0, sizeof(DataCtl));
     if (d.dp.on) {
@@ -544,7 +550,10 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
         std::memset(&dc0, 0, sizeof(dc0));
         dc0.htop = d.dp.h_pages;
         dc0.decode_enabled = d.dp.decode_on;
-        CK(cudaMemcpy(d.dctl, &dc0, sizeof(dc0), cudaMemcpyHostToDevice));
+        // on the engine stream, after the memset above (a legacy-stream copy
+        // is not ordered with the non-blocking stream's async memset)
+        CK(cudaMemcpyAsync(d.dctl, &dc0, sizeof(dc0), cudaMemcpyHostToDevice, E->stream));
+        CK(cudaStreamSynchronize(E->stream));
     }
     memset_all(d.tab_len, 0, n4);
     {
@@ -567,11 +576,6 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
         co_destroy(E);
         return fail(CO_ECUDA, "ctl upload");
     }
-    size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, d.keys_in, d.keys_out, d.vals_in, d.vals_out, (int)n, 0,
-                                    key_bits, E->stream);
-    E->cub_bytes = std::max<size_t>(bytes, 256);
-    if (cudaMalloc(&E->cub_tmp, E->cub_bytes) != cudaSuccess) { co_destroy(E); return fail(CO_ECUDA, "cub temp"); }
     cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PlanSh));
     cudaError_t e = cudaStreamSynchronize(E->stream);
     if (e != cudaSuccess) { co_destroy(E); return fail(CO_ECUDA, cudaGetErrorString(e)); }

@@ -13,6 +13,8 @@ namespace co {
 
 constexpr int NT = 256;   // threads of the single-CTA planner / apply kernels (max; 256 measured best)
 constexpr int TCHUNK = 64;  // pages per block-table chunk
+constexpr int NBIN = 4096;  // N'_w deadline buckets
+constexpr int GRP = 256;    // N'_w materialization group (items)
 constexpr int ST_PENDING = CO_PENDING, ST_WAITING = CO_WAITING, ST_RUNNING = CO_RUNNING,
               ST_PREEMPTED = CO_PREEMPTED, ST_COMPLETED = CO_COMPLETED;
 
@@ -31,7 +33,9 @@ struct Ctl {
     int32_t done, stalled, error, paused;
     int32_t active;                                   // this step proceeds past begin
     int32_t last_result;                              // step() return value
-    int32_t cnt_nw, cnt_nwp, cnt_run;                 // classify counts
+    int32_t cnt_nw, cnt_nwp, cnt_run;                 // classify counts (N_w, non-blown N'_w, running)
+    int32_t cnt_blown;                                // blown N'_w (arrival order)
+    uint64_t kmin, kmax;                              // range of the non-blown N'_w keys
     int32_t sid;                                      // stamp id of the current step
     int32_t check_due;
     int32_t free_top;                                 // N1: pages on the free stack
@@ -88,9 +92,16 @@ struct Dev {
     int32_t *st_nr, *st_crit, *st_removed, *st_embedded, *st_resumed, *st_stalled, *st_parts,
         *st_claimed, *st_failed, *st_acted, *st_deferred;
     uint64_t* seen64;            // member-filter first occurrence: (sid << 24) | (2^24-1-pos)
-    // classify + sort
-    uint64_t *keys_in, *keys_out;
-    uint32_t *vals_in, *vals_out;
+    // classify + bucketed ordering (no full sort): classify block b owns the
+    // index range [b*chunk, (b+1)*chunk) and compacts its running / blown
+    // requests in index order; non-blown N'_w requests get the unique key
+    // (D << idbits | idrank) and are bucketed by a range-adaptive histogram
+    int32_t nblk, chunk;
+    int32_t *run_tmp, *blown_tmp, *blk_cnt;
+    int32_t* crit_idx;
+    uint64_t* key0;
+    int32_t *f0_bin, *hist, *fill, *bin_off, *bucket, *grp_end;
+    int32_t *l_run, *l_blown, *l_nw, *l_nwp;
     // plan buffers
     PlanHdr* plan;
     int32_t *mem_idx, *mem_tok, *act_kind, *act_idx, *act_tok, *act_nb, *act_host, *act_start;

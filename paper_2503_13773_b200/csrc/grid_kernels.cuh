@@ -38,7 +38,9 @@ __global__ void k_begin(Dev d, int32_t guard) {
     c.last_result = 0;
     c.sid += 1;
     if (d.dp.on) { d.dctl->n_dec = 0; d.dctl->dec_items = 0; }
-    c.cnt_nw = c.cnt_nwp = c.cnt_run = 0;
+    c.cnt_nw = c.cnt_nwp = c.cnt_run = c.cnt_blown = 0;
+    c.kmin = ~0ull;
+    c.kmax = 0;
     if (guard) {
         // engine.py:644-659 no-progress guard, evaluated before each step()
         int64_t m[5] = {c.now, c.gen_total, c.n_live, (int64_t)(d.n - c.next_pending), c.fp_sum};
@@ -91,65 +93,190 @@ __device__ __forceinline__ void admit_one(const Dev& d, int32_t i, int32_t lo, i
     }
 }
 
-// class codes in the top two key bits: [class:2][blown:1][time].  Keys are
-// written at position idrank[i], so the sort's input is in req_id order and
-// the (stable) radix sort breaks every tie by id without id-rank key bits.
-constexpr uint64_t K_NW = 0, K_NWP = 1, K_RUN = 2;
-
-__global__ void k_classify(Dev d) {
+// k_classify (contiguous index chunk per block): admission, the planner's
+// 64-byte views, and the classification of scheduler.py:129-163 into
+//   running (index order)              -> run_tmp   (block-ordered)
+//   critical N_w                       -> crit_idx  (unordered; sorted by the planner)
+//   N'_w blown, rt < 0 (arrival order) -> blown_tmp (block-ordered; SoA order IS (arrival, id))
+//   N'_w rt >= 0 ordered by (D, id)    -> key0 = D << idbits | idrank, range kmin..kmax
+__global__ void __launch_bounds__(256) k_classify(Dev d) {
+    __shared__ int32_t sc[32];
+    __shared__ int32_t tot_s[2];
+    __shared__ uint64_t kr[2][8];
     const Ctl& c = *d.ctl;
     if (!c.active) return;
     const int64_t now = c.now, ti = c.t_i, eps = d.eps;
-    const int cs = d.key_bits - 2, fs = d.key_bits - 3;  // class / blown-flag bit positions
-    int32_t cw = 0, cwp = 0, cr = 0;
+    const int ib = d.idbits;
     const int32_t hi_live = c.next_pending;
     const int32_t alo = c.adm_lo, ahi = c.adm_hi;
     const int64_t ev0 = c.ev_count - (ahi - alo);
-    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < d.n; i += gridDim.x * blockDim.x) {
-        uint64_t key = ~0ull;
-        if (i >= alo && i < ahi) admit_one(d, i, alo, ev0);
-        if (i < hi_live) {
-            int8_t s = d.state[i];
-            if (s >= ST_WAITING && s <= ST_PREEMPTED) {
-                const PV v = make_pv(d, i, now);  // the planner's snapshot view
-                uint4* dst = reinterpret_cast<uint4*>(d.views + i);
-                const uint4* src = reinterpret_cast<const uint4*>(&v);
-                dst[0] = src[0]; dst[1] = src[1]; dst[2] = src[2]; dst[3] = src[3];
-            }
-            if (s == ST_WAITING || s == ST_PREEMPTED) {
-                // every waiting view is ready (engine.py:311-312); rt = D - now
-                int64_t D = d.first_tok[i] < 0 ? d.arr[i] + d.slo_ttft[i] : d.last_tok[i] + d.slo_tbt[i];
-                int64_t rt = D - now;
-                if (rt >= -eps && rt - ti < eps) {
-                    key = (K_NW << cs) | (uint64_t)D;
-                    cw++;
-                } else {
-                    // queue_key (scheduler.py:151-157): (0, rt, id) / (1, arrival, id)
-                    uint64_t flag = rt < 0 ? 1 : 0;
-                    uint64_t v = flag ? (uint64_t)d.arr[i] : (uint64_t)D;
-                    key = (K_NWP << cs) | (flag << fs) | v;
-                    cwp++;
+    const int32_t lo = blockIdx.x * d.chunk, hi = min(d.n, lo + d.chunk);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int32_t run_base = 0, blown_base = 0, ncrit = 0, nf0 = 0;
+    uint64_t kmin = ~0ull, kmax = 0;
+    for (int32_t c0 = lo; c0 < hi; c0 += 256) {
+        const int32_t i = c0 + (int32_t)threadIdx.x;
+        int32_t is_run = 0, is_blown = 0;
+        if (i < hi) {
+            if (i >= alo && i < ahi) admit_one(d, i, alo, ev0);
+            int32_t f0 = -1;
+            if (i < hi_live) {
+                const int8_t s = d.state[i];
+                if (s >= ST_WAITING && s <= ST_PREEMPTED) {
+                    const PV v = make_pv(d, i, now);  // the planner's snapshot view
+                    uint4* dst = reinterpret_cast<uint4*>(d.views + i);
+                    const uint4* src = reinterpret_cast<const uint4*>(&v);
+                    dst[0] = src[0]; dst[1] = src[1]; dst[2] = src[2]; dst[3] = src[3];
                 }
-            } else if (s == ST_RUNNING) {
-                key = (K_RUN << cs) | (uint64_t)i;
-                cr++;
+                if (s == ST_WAITING || s == ST_PREEMPTED) {
+                    // every waiting view is ready (engine.py:311-312); rt = D - now
+                    const int64_t D = d.first_tok[i] < 0 ? d.arr[i] + d.slo_ttft[i] : d.last_tok[i] + d.slo_tbt[i];
+                    const int64_t rt = D - now;
+                    if (rt >= -eps && rt - ti < eps) {
+                        d.crit_idx[atomicAdd(&d.ctl->cnt_nw, 1)] = i;
+                        ncrit++;
+                    } else if (rt < 0) {
+                        is_blown = 1;  // queue key (1, arrival, id)
+                    } else {
+                        const uint64_t k = ((uint64_t)D << ib) | (uint64_t)d.idrank[i];  // (0, rt, id)
+                        d.key0[i] = k;
+                        f0 = -2;
+                        nf0++;
+                        kmin = k < kmin ? k : kmin;
+                        kmax = k > kmax ? k : kmax;
+                    }
+                } else if (s == ST_RUNNING) {
+                    is_run = 1;
+                }
             }
+            d.f0_bin[i] = f0;
         }
-        const int32_t pos = d.idrank[i];
-        d.keys_in[pos] = key;
-        d.vals_in[pos] = (uint32_t)i;
+        // order-preserving block compaction of the running and blown flags
+        int32_t packed = is_run | (is_blown << 16), x = packed;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) sc[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            int32_t y = lane < 8 ? sc[lane] : 0, z = y;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int32_t q = __shfl_up_sync(0xffffffffu, z, o);
+                if (lane >= o) z += q;
+            }
+            if (lane < 8) sc[lane] = z - y;
+            if (lane == 7) { tot_s[0] = z & 0xffff; tot_s[1] = z >> 16; }
+        }
+        __syncthreads();
+        const int32_t ex = sc[w] + x - packed;
+        if (is_run) d.run_tmp[lo + run_base + (ex & 0xffff)] = i;
+        if (is_blown) d.blown_tmp[lo + blown_base + (ex >> 16)] = i;
+        run_base += tot_s[0];
+        blown_base += tot_s[1];
+        __syncthreads();
     }
-    // warp-aggregated counters
+    // block totals: counts, key range
     for (int o = 16; o > 0; o >>= 1) {
-        cw += __shfl_xor_sync(0xffffffffu, cw, o);
-        cwp += __shfl_xor_sync(0xffffffffu, cwp, o);
-        cr += __shfl_xor_sync(0xffffffffu, cr, o);
+        ncrit += __shfl_xor_sync(0xffffffffu, ncrit, o);
+        nf0 += __shfl_xor_sync(0xffffffffu, nf0, o);
+        uint64_t a = __shfl_xor_sync(0xffffffffu, kmin, o), b = __shfl_xor_sync(0xffffffffu, kmax, o);
+        kmin = a < kmin ? a : kmin;
+        kmax = b > kmax ? b : kmax;
     }
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) { kr[0][w] = kmin; kr[1][w] = kmax; sc[w] = nf0; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t mn = ~0ull, mx = 0;
+        int32_t f = 0;
+        for (int k = 0; k < 8; k++) {
+            mn = kr[0][k] < mn ? kr[0][k] : mn;
+            mx = kr[1][k] > mx ? kr[1][k] : mx;
+            f += sc[k];
+        }
         Ctl* cm = d.ctl;
-        if (cw) atomicAdd(&cm->cnt_nw, cw);
-        if (cwp) atomicAdd(&cm->cnt_nwp, cwp);
-        if (cr) atomicAdd(&cm->cnt_run, cr);
+        if (f) {
+            atomicAdd(&cm->cnt_nwp, f);
+            atomicMin((unsigned long long*)&cm->kmin, (unsigned long long)mn);
+            atomicMax((unsigned long long*)&cm->kmax, (unsigned long long)mx);
+        }
+        if (run_base) atomicAdd(&cm->cnt_run, run_base);
+        if (blown_base) atomicAdd(&cm->cnt_blown, blown_base);
+        d.blk_cnt[2 * blockIdx.x] = run_base;
+        d.blk_cnt[2 * blockIdx.x + 1] = blown_base;
+    }
+}
+
+__device__ __forceinline__ int bin_shift(uint64_t range) {
+    const int bits = range ? 64 - __clzll((long long)range) : 0;
+    return bits > 12 ? bits - 12 : 0;  // (key - kmin) >> shift < NBIN
+}
+
+// histogram of the non-blown N'_w keys over NBIN range-adaptive buckets
+__global__ void __launch_bounds__(256) k_bins(Dev d) {
+    __shared__ int32_t h[NBIN];
+    const Ctl& c = *d.ctl;
+    if (!c.active || c.cnt_nwp == 0) return;
+    const uint64_t kmin = c.kmin;
+    const int sh = bin_shift(c.kmax - kmin);
+    for (int k = threadIdx.x; k < NBIN; k += blockDim.x) h[k] = 0;
+    __syncthreads();
+    const int32_t n = c.next_pending;
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        if (d.f0_bin[i] == -2) {
+            const int32_t b = (int32_t)((d.key0[i] - kmin) >> sh);
+            d.f0_bin[i] = b;
+            atomicAdd(&h[b], 1);
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < NBIN; k += blockDim.x)
+        if (h[k]) atomicAdd(&d.hist[k], h[k]);
+}
+
+// scatter into bucket order (unordered within a bucket; the planner sorts
+// each bucket group by key when it first needs it)
+__global__ void __launch_bounds__(256) k_scatter(Dev d) {
+    __shared__ int32_t off[NBIN];
+    __shared__ int32_t wsum[8];
+    const Ctl& c = *d.ctl;
+    if (!c.active || c.cnt_nwp == 0) return;
+    // exclusive prefix of the histogram (16 bins per thread)
+    constexpr int PER = NBIN / 256;
+    int32_t loc[PER], t = 0;
+    for (int q = 0; q < PER; q++) { loc[q] = d.hist[threadIdx.x * PER + q]; t += loc[q]; }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int32_t x = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    int32_t wbase = 0;
+    for (int k = 0; k < w; k++) wbase += wsum[k];
+    int32_t run = wbase + x - t;
+    for (int q = 0; q < PER; q++) { off[threadIdx.x * PER + q] = run; run += loc[q]; }
+    __syncthreads();
+    if (blockIdx.x == 0) {
+        for (int k = threadIdx.x; k < NBIN; k += blockDim.x) d.bin_off[k] = off[k];
+        if (threadIdx.x == 0) d.bin_off[NBIN] = c.cnt_nwp;
+        // group ends for the planner's lazy materialization: grp_end[j] is the
+        // first bucket boundary at or after (j+1)*GRP (capped at the total)
+        const int32_t tot = c.cnt_nwp;
+        for (int k = threadIdx.x; k < NBIN; k += blockDim.x) {
+            const int32_t lo = off[k], hi = k + 1 < NBIN ? off[k + 1] : tot;
+            for (int32_t j = lo / GRP; j < hi / GRP; j++) d.grp_end[j] = hi;
+        }
+        if (threadIdx.x == 0 && tot % GRP) d.grp_end[tot / GRP] = tot;
+    }
+    const int32_t n = c.next_pending;
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int32_t b = d.f0_bin[i];
+        if (b >= 0) d.bucket[off[b] + atomicAdd(&d.fill[b], 1)] = i;
     }
 }
 

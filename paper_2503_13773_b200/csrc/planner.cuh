@@ -33,6 +33,8 @@ struct PlanSh {
     int32_t tri_idx[PV_CAP], tri_taken[PV_CAP];
     int32_t n_tri_cached;
     PV rv[RV_CAP];               // the running set's views, staged once per plan
+    int32_t blkoff[2][1288];     // prefix of the classify blocks' running / blown counts
+    int32_t mat, any_feasible;
     unsigned __int128 wsum;
     int64_t free, shortfall, runway, batch_now, gm_tokens;
     int64_t f_total, a_total, f_supply, a_supply, tbt_floor, lim, resid;
@@ -308,10 +310,11 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     const int tid = threadIdx.x;
     const int64_t now = c.now, ti = c.t_i, eps = d.eps;
     const int32_t sid = c.sid;
-    const int32_t n_nw = c.cnt_nw, n_nwp = c.cnt_nwp, n_run = c.cnt_run;
-    const int32_t* NW = reinterpret_cast<const int32_t*>(d.vals_out);
-    const int32_t* NWP = NW + n_nw;
-    const int32_t* RUN = NWP + n_nwp;
+    const int32_t n_nw = c.cnt_nw, n_f0 = c.cnt_nwp, n_blown = c.cnt_blown, n_run = c.cnt_run;
+    const int32_t n_nwp = n_f0 + n_blown;
+    const int32_t* NW = d.crit_idx;   // sorted below by (rt, id)
+    const int32_t* NWP = d.l_nwp;     // N'_w queue order, materialized on demand
+    const int32_t* RUN = d.l_run;     // running set in arrival order
     const int B = d.B, bs = d.bs;
     if (tid == 0) {
         S.free = free_tokens(d);
@@ -322,6 +325,55 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     __syncthreads();
 
     prof_mark(d, 0);
+    // running set and the blown N'_w tail: concatenate the classify blocks'
+    // ordered lists (block b owns indices [b*chunk, (b+1)*chunk))
+    for (int32_t b = tid; b < d.nblk; b += (int)blockDim.x) {
+        S.blkoff[0][b] = d.blk_cnt[2 * b];
+        S.blkoff[1][b] = d.blk_cnt[2 * b + 1];
+    }
+    if (tid == 0) {
+        S.mat = 0;
+        S.blkoff[0][d.nblk] = 0; S.blkoff[1][d.nblk] = 0;
+    }
+    __syncthreads();
+    blk_scan_smem(S.blkoff[0], d.nblk + 1, S.b);
+    blk_scan_smem(S.blkoff[1], d.nblk + 1, S.b);
+    {
+        const int nw = (int)(blockDim.x >> 5), lane = tid & 31;
+        for (int32_t b = tid >> 5; b < d.nblk; b += nw) {
+            const int32_t r0 = S.blkoff[0][b], nr = S.blkoff[0][b + 1] - r0;
+            const int32_t b0 = S.blkoff[1][b], nb = S.blkoff[1][b + 1] - b0, src = b * d.chunk;
+            for (int32_t k = lane; k < nr; k += 32) d.l_run[r0 + k] = d.run_tmp[src + k];
+            for (int32_t k = lane; k < nb; k += 32) d.l_blown[b0 + k] = d.blown_tmp[src + k];
+        }
+    }
+    __syncthreads();
+    // N_w by (rt, id) (scheduler.py:159); D = rt + now, unique with the id rank
+    blk_sort(d.crit_idx, n_nw, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
+        k0 = (uint64_t)(view_of(d, i).rt + (1ll << 62)); k1 = (uint64_t)d.idrank[i]; k2 = 0;
+    }, d, S.b);
+    // N'_w (scheduler.py:151-160): rt >= 0 by (D, id) from the buckets, whole
+    // buckets at a time (k_scatter's group ends), then the blown requests in
+    // arrival order.  S.mat is always a bucket boundary below n_f0.
+    auto ensure = [&](int32_t target) {
+        if (target > n_nwp) target = n_nwp;
+        while (S.mat < target) {
+            const int32_t m0 = S.mat;
+            if (m0 < n_f0) {
+                const int32_t want = target < n_f0 ? target : n_f0;
+                const int32_t end = d.grp_end[(want - 1) / GRP], g = end - m0;
+                for (int32_t k = tid; k < g; k += (int)blockDim.x) d.l_nwp[m0 + k] = d.bucket[m0 + k];
+                __syncthreads();
+                blk_sort_u64(d.l_nwp + m0, g, [&](int32_t i) { return d.key0[i]; }, d, S.b);
+                if (tid == 0) S.mat = end;
+            } else {
+                for (int32_t k = tid; k < n_blown; k += (int)blockDim.x) d.l_nwp[m0 + k] = d.l_blown[k];
+                if (tid == 0) S.mat = m0 + n_blown;
+            }
+            __syncthreads();
+        }
+    };
+
     const bool rcached = n_run <= RV_CAP;
     if (rcached)
         for (int32_t k = tid; k < n_run; k += (int)blockDim.x) S.rv[k] = view_of(d, RUN[k]);
@@ -566,6 +618,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         int64_t used_base = consumed;
         int32_t ksel = n_nwp;
         for (int32_t base = 0; base < n_nwp; base += (int)blockDim.x) {
+            ensure(base + (int)blockDim.x);
             int32_t k = base + tid;
             int32_t ch = 0;
             if (k < n_nwp) { const PV v = view_of(d, NWP[k]); ch = v.kvn - v.pre; }
@@ -821,9 +874,28 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         fl = blk_min(fl, S.b);
         if (tid == 0) { S.tbt_floor = (int64_t)fl; S.stop = 0; S.pos = k_sel; }
         __syncthreads();
+        // exact early exit: the loop only ever takes items with need > 0 and
+        // cost <= free - runway, and free only decreases, so if no remaining
+        // N'_w item qualifies now the walk cannot act (scheduler.py:737-741)
+        {
+            const int64_t room0 = S.free - S.runway;
+            auto feas = [&](int32_t i) {
+                const PV v = view_of(d, i);
+                const int64_t t = (int64_t)v.target - v.eff;
+                return t > 0 && pv_cost(v, t, bs) <= room0;
+            };
+            int f = 0;
+            for (int32_t k = k_sel + tid; k < S.mat; k += (int)blockDim.x) f |= feas(NWP[k]);
+            for (int32_t k = S.mat + tid; k < n_f0; k += (int)blockDim.x) f |= feas(d.bucket[k]);
+            if (S.mat <= n_f0)
+                for (int32_t k = tid; k < n_blown; k += (int)blockDim.x) f |= feas(d.l_blown[k]);
+            if (!__syncthreads_or(f) && tid == 0) S.stop = 1;
+            __syncthreads();
+        }
         const int64_t batch_now = S.batch_now;
         const bool has_floor = fl != ~0ull;
         for (int32_t base = k_sel; base < n_nwp && !S.stop; base += (int)blockDim.x) {
+            ensure(base + (int)blockDim.x);
             int32_t k = base + tid;
             int64_t need = 0, cst = 0;
             if (k < n_nwp) {
@@ -866,6 +938,7 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         P.sated = S.sated;
         P.k_sel = k_sel;
     }
+    for (int32_t k = tid; k < NBIN; k += (int)blockDim.x) { d.hist[k] = 0; d.fill[k] = 0; }
     prof_mark(d, 15);
 }
 
