@@ -61,26 +61,43 @@ def make_trace(rank: int, world: int):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled while the GPU is busy."""
+    """SM clock and throttle reasons sampled through NVML (the library behind
+    nvidia-smi) every ~0.5 ms while the timed region runs, so even a few-ms
+    region gets samples; falls back to nvidia-smi polling without NVML."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, reasons bitmask)
+        self.how = "nvml"
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((float(sm), float(mx), int(rs)))
+                self._stop.wait(0.0005)
+            pynvml.nvmlShutdown()
+            return
+        except Exception:
+            self.how = "nvidia-smi"
+        q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                a, b, r = [x.strip() for x in out.split(",")]
+                self.rows.append((float(a), float(b), int(r, 16)))
             except Exception:
                 pass
             self._stop.wait(0.05)
@@ -96,13 +113,11 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k].lower() == "active"})
-        loaded = [x for x in sm if x > 0.5 * (max(mx) if mx else 1)] or sm
-        return {"sm_mhz": statistics.median(loaded) if loaded else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        mx = max(r[1] for r in self.rows)
+        reasons = sorted({n for r in self.rows for n, bit in self.REASONS.items() if r[2] & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows), "how": f"{self.how}, sampled only while the K timed steps run"}
 
 
 def stage_bytes(n: int, live: int, stage: str, running: int = 0) -> int:
@@ -262,24 +277,27 @@ def device_arm(args, rank, world, dist):
         from paper_2503_13773_b200.multi import attach_global_reserve
         attach_global_reserve(eng, rank, world)
     pre = max(0, WINDOW_START - args.warmup)
+    eng.run_steps(pre)
+    eng.run_steps(args.warmup)
+    eng.events  # drain the arrival burst outside the timed region
+    s0 = eng._scalars()
+    d0, it0 = s0.decisions, s0.iterations
+    step_ms = (C.c_double * args.steps)()
+    stage_ms = (C.c_double * N.NSTAGES)()
     with ClockSampler(dev) as clocks:
-        eng.run_steps(pre)
-        eng.run_steps(args.warmup)
-        eng.events  # drain the arrival burst outside the timed region
-        s0 = eng._scalars()
-        d0, it0 = s0.decisions, s0.iterations
+        t_wait = time.perf_counter()
+        while not clocks.rows and time.perf_counter() - t_wait < 2.0:
+            time.sleep(0.001)
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
-        step_ms = (C.c_double * args.steps)()
-        stage_ms = (C.c_double * N.NSTAGES)()
         eng._dirty()
         N.check(eng._lib.co_time_steps(eng._h, args.steps, L2_FLUSH_BYTES, step_ms, stage_ms), "co_time_steps")
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
-        eng._dirty()
-        s1 = eng._scalars()
+    eng._dirty()
+    s1 = eng._scalars()
     dev_ms = float(sum(step_ms))
     decisions = s1.decisions - d0
     coll = None

@@ -31,6 +31,7 @@
 #include "apply.cuh"
 #include "data_plane.cuh"
 #include "decode_tc.cuh"
+#include "decode_tc05.cuh"
 #include <cudaTypedefs.h>
 
 using namespace co;
@@ -125,7 +126,7 @@ struct co_engine {
     CUtensorMap kvmap;
     cudaGraphExec_t graph1 = nullptr;  // one step, step() semantics
     void* result_host = nullptr;
-    bool tc_decode = false;
+    int tc_decode = 0;  // 2 = tcgen05 (k_decode_tc05), 1 = mma.sync (k_decode_tc), 0 = CUDA cores
     int64_t page_bytes = 0;
     std::vector<co_event> st_events;   // host staging of drained device events
     std::vector<int32_t> st_members;
@@ -192,7 +193,9 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
         k_data<<<E->sms, 512, 0, s>>>(d, d.dp, d.dctl, 0);
         if (ev) mark(ev[7], s);
         if (d.dp.decode_on) {
-            if (E->tc_decode)
+            if (E->tc_decode == 2)
+                k_decode_tc05<<<E->sms, T5_THREADS, T5_SMEM, s>>>(d, d.dp, d.dctl, E->kvmap);
+            else if (E->tc_decode == 1)
                 k_decode_tc<<<E->sms, TC_WARPS * 32, TC_SMEM, s>>>(d, d.dp, d.dctl, E->kvmap);
             else
                 k_decode<<<E->sms * 8, DEC_T, 0, s>>>(d, d.dp, d.dctl);
@@ -499,7 +502,9 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (cr != CUDA_SUCCESS) { co_destroy(E); return fail(CO_ECUDA, "tensor map encode failed"); }
             cudaFuncSetAttribute(k_decode_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
-            E->tc_decode = true;
+            cudaFuncSetAttribute(k_decode_tc05, cudaFuncAttributeMaxDynamicSharedMemorySize, T5_SMEM);
+            const char* dk = getenv("CO_DECODE_KERNEL");
+            E->tc_decode = (dk && std::string(dk) == "mma_sync") ? 1 : 2;
         }
     }
     AL(d.l_tri_key, n); AL(d.am_rhi, n3); AL(d.am_rlo, n3); AL(d.rank_to_idx, n);
