@@ -194,7 +194,10 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
         if (ev) mark(ev[7], s);
         if (d.dp.decode_on) {
             if (E->tc_decode == 2)
-                k_decode_tc05<<<E->sms, T5_THREADS, T5_SMEM, s>>>(d, d.dp, d.dctl, E->kvmap);
+                if (d.dp.Hq / d.dp.Hkv <= 8)
+                    k_decode_tc05<8><<<E->sms, T5_THREADS, T5_SMEM, s>>>(d, d.dp, d.dctl, E->kvmap);
+                else
+                    k_decode_tc05<16><<<E->sms, T5_THREADS, T5_SMEM, s>>>(d, d.dp, d.dctl, E->kvmap);
             else if (E->tc_decode == 1)
                 k_decode_tc<<<E->sms, TC_WARPS * 32, TC_SMEM, s>>>(d, d.dp, d.dctl, E->kvmap);
             else
@@ -502,7 +505,8 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (cr != CUDA_SUCCESS) { co_destroy(E); return fail(CO_ECUDA, "tensor map encode failed"); }
             cudaFuncSetAttribute(k_decode_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
-            cudaFuncSetAttribute(k_decode_tc05, cudaFuncAttributeMaxDynamicSharedMemorySize, T5_SMEM);
+            cudaFuncSetAttribute(k_decode_tc05<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, T5_SMEM);
+            cudaFuncSetAttribute(k_decode_tc05<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, T5_SMEM);
             const char* dk = getenv("CO_DECODE_KERNEL");
             E->tc_decode = (dk && std::string(dk) == "mma_sync") ? 1 : 2;
         }

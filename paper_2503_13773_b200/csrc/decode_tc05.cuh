@@ -100,6 +100,42 @@ __device__ __forceinline__ void t5_ld16(uint32_t taddr, float* v) {
 #pragma unroll
     for (int k = 0; k < 16; k++) v[k] = __uint_as_float(r[k]);
 }
+template <int N>
+__device__ __forceinline__ void t5_ld(uint32_t taddr, float* v) {  // N = 8 or 16 columns of this lane
+    if constexpr (N == 16) {
+        t5_ld16(taddr, v);
+    } else {
+        uint32_t r[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                     : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int k = 0; k < 8; k++) v[k] = __uint_as_float(r[k]);
+    }
+}
+// max of each of N values over the 32 lanes of a warp: halving exchanges at
+// lane offsets 16, 8, ... leave lane l with head (l >> (5 - log2 N)) & (N - 1),
+// reduced over the remaining low lane bits
+template <int N>
+__device__ __forceinline__ float t5_butterfly_max(const float* v, int lane) {
+    float a[N];
+#pragma unroll
+    for (int k = 0; k < N; k++) a[k] = v[k];
+    int off = 16;
+#pragma unroll
+    for (int cnt = N; cnt > 1; cnt >>= 1, off >>= 1) {
+        const bool hi = lane & off;
+#pragma unroll
+        for (int k = 0; k < cnt / 2; k++) {
+            const float keep = hi ? a[k + cnt / 2] : a[k], send = hi ? a[k] : a[k + cnt / 2];
+            a[k] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, off));
+        }
+    }
+#pragma unroll
+    for (; off > 0; off >>= 1) a[0] = fmaxf(a[0], __shfl_xor_sync(0xffffffffu, a[0], off));
+    return a[0];
+}
 __device__ __forceinline__ float t5_ex2(float v) {  // 2^v, MUFU.EX2 (ex2(-inf) = +0)
     float r;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
@@ -163,6 +199,10 @@ struct T5Cursor {
     }
 };
 
+// NHR = query heads per KV head the softmax handles (G rounded up to 8 or
+// 16): the MMA N stays 16 (its minimum at M = 128, padded rows are zero) but
+// the softmax, its reductions and the TMEM loads skip the padding.
+template <int NHR>
 __global__ void __launch_bounds__(T5_THREADS, 1)
     k_decode_tc05(Dev d, DataCfg x, DataCtl* dc, const __grid_constant__ CUtensorMap kvmap) {
     const Ctl& c = *d.ctl;
@@ -241,11 +281,7 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
                 off = lane * box;
                 const int32_t pos = P0 + off;
                 const int32_t pi = pos / bs;
-#ifdef T5_FAKE_PAGES
-                const int32_t page = pi % 1000;
-#else
                 const int32_t page = pi < d.tab_len[w.owner] ? page_of(d, w.owner, pi) : 0;
-#endif
                 rr = (page * x.rows + row) * bs + pos % bs;
             }
             if (lane == 0) {
@@ -273,12 +309,8 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
             uint32_t ptg1 = 0, pst1 = 0, ptg2 = 0, pst2 = 0;
             auto issue_o = [&](int og, uint32_t tg, uint32_t st, uint32_t tv) {
                 const int ob = (int)(tg & 1);
-#ifndef T5_EXP_NOSOFTMAX
                 mbar_wait(PF(og, ob), (tg >> 1) & 1);
-#endif
-#ifndef T5_EXP_NOSOFTMAX
                 mbar_wait(OE(og, ob), ((tg >> 1) & 1) ^ 1);
-#endif
                 mbar_wait(FULL(1, (int)st), (tv / T5_STAGES) & 1);
                 t5_fence_after();
                 const uint32_t vb = sb + st * T5_STAGE_BYTES + T5_KV_BYTES;
@@ -300,13 +332,9 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
                 const uint32_t tg = g ? Tg1 : Tg0, ig = g ? Ig1 : Ig0;
                 const int sbuf = (int)(tg & 1), qb = (int)(ig & 1);
                 const bool first = cur.t() == 0, last = cur.t() == cur.nt() - 1;
-#ifndef T5_EXP_NOSOFTMAX
                 if (first) mbar_wait(QF(g, qb), (ig >> 1) & 1);
-#endif
                 mbar_wait(FULL(0, s), (T / T5_STAGES) & 1);
-#ifndef T5_EXP_NOSOFTMAX
                 mbar_wait(SE(g, sbuf), ((tg >> 1) & 1) ^ 1);
-#endif
                 t5_fence_after();
                 const uint32_t kb = sb + (uint32_t)s * T5_STAGE_BYTES;
                 const uint32_t qbase = sb + QBUF(g, qb);
@@ -347,9 +375,7 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
                 const uint32_t rid = (uint32_t)d.rid[w.i];
                 const uint32_t ig = g ? Ig1++ : Ig0++;
                 const int qb = (int)(ig & 1);
-#ifndef T5_EXP_NOSOFTMAX
                 if (lane == 0) mbar_wait(QE(g, qb), ((ig >> 1) & 1) ^ 1);
-#endif
                 __syncwarp();
                 uint8_t* qs = base + QBUF(g, qb);
                 // lane owns dims [4*lane, 4*lane+4) of every head; rows >= G are zero
@@ -371,76 +397,43 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
         }
     } else if (warp >= 4) {
         // ---------------- softmax + output (group g) ----------------
-#ifdef T5_EXP_NOSOFTMAX
-        if (true) {} else
-#endif
-        {
         const int g = (warp - 4) >> 2, q4 = warp & 3;
         const int r = q4 * 32 + lane;  // TMEM lane: tile position (S) / head dim (O)
         const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
         float* red = reinterpret_cast<float*>(base + T5_OFF_RED) + g * T5_RED_FLOATS;
-        const int hme = (lane >> 1) & 15;  // the head this lane reduces in the butterfly
+        constexpr int LSH = NHR == 16 ? 1 : 2;  // lanes per head after the butterfly = 1 << LSH
+        const int hme = (lane >> LSH) & (NHR - 1);  // the head this lane reduces in the butterfly
         uint32_t T = 0;
         for (int32_t it = (int32_t)(blockIdx.x + g * gridDim.x); it < nitems; it += T5_GROUPS * (int32_t)gridDim.x) {
             DecItem w;
             dec_item(d, x, dc, it, w);
             const int32_t nt = (w.pos_hi - w.nt0 + T5_TILE - 1) / T5_TILE;
-            float mrun[T5_NH], lpart[T5_NH], oacc[T5_NH], cprev[T5_NH];
+            float mrun[NHR], lpart[NHR], oacc[NHR], cprev[NHR];
 #pragma unroll
-            for (int h = 0; h < T5_NH; h++) { mrun[h] = -INFINITY; lpart[h] = 0.f; oacc[h] = 0.f; cprev[h] = 1.f; }
+            for (int h = 0; h < NHR; h++) { mrun[h] = -INFINITY; lpart[h] = 0.f; oacc[h] = 0.f; cprev[h] = 1.f; }
             for (int32_t t = 0; t < nt; t++, T++) {
                 const int b = (int)(T & 1);
                 mbar_wait(SF(g, b), (T >> 1) & 1);
                 t5_fence_after();
-                float sv[T5_NH];
-                t5_ld16(tl + 32 * g + 16 * b, sv);
+                float sv[NHR];
+                t5_ld<NHR>(tl + 32 * g + 16 * b, sv);
                 t5_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(SE(g, b));
                 const int32_t pos = w.nt0 + t * T5_TILE + r;
                 const bool valid = pos >= w.pos_lo && pos < w.pos_hi;
 #pragma unroll
-                for (int h = 0; h < T5_NH; h++) sv[h] = valid ? sv[h] : -INFINITY;
-                // butterfly max: 16 heads over 32 lanes in 16 shuffles; lane
-                // ends with head (lane >> 1) & 15
-                float m8[8], m4[4], m2[2], m1;
-                {
-                    const bool hi = lane & 16;
-#pragma unroll
-                    for (int k = 0; k < 8; k++) {
-                        const float keep = hi ? sv[k + 8] : sv[k], send = hi ? sv[k] : sv[k + 8];
-                        m8[k] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 16));
-                    }
-                }
-                {
-                    const bool hi = lane & 8;
-#pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        const float keep = hi ? m8[k + 4] : m8[k], send = hi ? m8[k] : m8[k + 4];
-                        m4[k] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 8));
-                    }
-                }
-                {
-                    const bool hi = lane & 4;
-#pragma unroll
-                    for (int k = 0; k < 2; k++) {
-                        const float keep = hi ? m4[k + 2] : m4[k], send = hi ? m4[k] : m4[k + 2];
-                        m2[k] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 4));
-                    }
-                }
-                {
-                    const bool hi = lane & 2;
-                    const float keep = hi ? m2[1] : m2[0], send = hi ? m2[0] : m2[1];
-                    m1 = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 2));
-                    m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 1));
-                }
+                for (int h = 0; h < NHR; h++) sv[h] = valid ? sv[h] : -INFINITY;
+                // butterfly max: NHR heads over 32 lanes (NHR shuffles); lane
+                // ends with head hme
+                const float m1 = t5_butterfly_max<NHR>(sv, lane);
                 float* rb = red + b * T5_NH * 4;  // [head][warp]
-                if (!(lane & 1)) rb[hme * 4 + q4] = m1;
+                if (!(lane & ((1 << LSH) - 1))) rb[hme * 4 + q4] = m1;
                 t5_named_sync(1 + g, 128);
-                float corr[T5_NH];
+                float corr[NHR];
                 uint8_t* pbuf = base + PBUF(g, b);
 #pragma unroll
-                for (int h = 0; h < T5_NH; h++) {
+                for (int h = 0; h < NHR; h++) {
                     const float4 q = *reinterpret_cast<const float4*>(rb + h * 4);
                     const float m = fmaxf(mrun[h], fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
                     corr[h] = t5_ex2(mrun[h] - m);  // mrun = -inf -> 0
@@ -459,25 +452,25 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
                     const int ob = (int)(To & 1);
                     mbar_wait(OF(g, ob), (To >> 1) & 1);
                     t5_fence_after();
-                    float ov[T5_NH];
-                    t5_ld16(tl + 64 + 32 * g + 16 * ob, ov);
+                    float ov[NHR];
+                    t5_ld<NHR>(tl + 64 + 32 * g + 16 * ob, ov);
                     t5_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(OE(g, ob));
 #pragma unroll
-                    for (int h = 0; h < T5_NH; h++) oacc[h] = oacc[h] * (f ? corr[h] : cprev[h]) + ov[h];
+                    for (int h = 0; h < NHR; h++) oacc[h] = oacc[h] * (f ? corr[h] : cprev[h]) + ov[h];
                 }
 #pragma unroll
-                for (int h = 0; h < T5_NH; h++) cprev[h] = corr[h];
+                for (int h = 0; h < NHR; h++) cprev[h] = corr[h];
             }
             // item result: O (lane = dim), m (exp2 domain -> natural log), l
             float* out = x.dec_part + (int64_t)it * G * (x.D + 2);
 #pragma unroll
-            for (int h = 0; h < T5_NH; h++)  // unrolled: the accumulators stay in registers
+            for (int h = 0; h < NHR; h++)  // unrolled: the accumulators stay in registers
                 if (h < G) out[h * (x.D + 2) + r] = oacc[h];
             float* lb = red + 2 * T5_NH * 4;  // [4 warps][16 heads]
 #pragma unroll
-            for (int h = 0; h < T5_NH; h++) {
+            for (int h = 0; h < NHR; h++) {
                 if (h >= G) break;
                 float l = lpart[h];
 #pragma unroll
@@ -489,11 +482,10 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
                 const float l = lb[r] + lb[T5_NH + r] + lb[2 * T5_NH + r] + lb[3 * T5_NH + r];
                 float m = 0.f;
 #pragma unroll
-                for (int h = 0; h < T5_NH; h++) m = h == r ? mrun[h] : m;
+                for (int h = 0; h < NHR; h++) m = h == r ? mrun[h] : m;
                 out[r * (x.D + 2) + x.D] = m * 0.6931471805599453f;  // exp2 domain -> natural log
                 out[r * (x.D + 2) + x.D + 1] = l;
             }
-        }
         }
     }
     t5_fence_before();
