@@ -6,7 +6,7 @@
 //   block-ordered running/blown lists, N'_w keys) -> k_bins + k_scatter (grid:
 //   range-adaptive deadline buckets) -> k_plan (1 CTA x 256) -> k_apply
 //   (1 CTA x 256, gated invariant check inside) [-> NCCL reserve all-reduce
-//   on a side stream] [-> k_data -> k_decode_tc + k_decode_reduce]
+//   on a side stream] [-> k_data -> k_decode_tc05 + k_decode_reduce]
 // co_run captures `steps_per_launch` steps into one CUDA graph and relaunches
 // it; every kernel early-exits once the device control block says the run is
 // done or paused (an append buffer needs draining), so no host round trip is
@@ -30,7 +30,6 @@
 #include "planner.cuh"
 #include "apply.cuh"
 #include "data_plane.cuh"
-#include "decode_tc.cuh"
 #include "decode_tc05.cuh"
 #include <cudaTypedefs.h>
 
@@ -126,7 +125,7 @@ struct co_engine {
     CUtensorMap kvmap;
     cudaGraphExec_t graph1 = nullptr;  // one step, step() semantics
     void* result_host = nullptr;
-    int tc_decode = 0;  // 2 = tcgen05 (k_decode_tc05), 1 = mma.sync (k_decode_tc), 0 = CUDA cores
+    bool tc_decode = false;  // tcgen05 (k_decode_tc05) when the block size tiles by 16; else CUDA cores
     int64_t page_bytes = 0;
     std::vector<co_event> st_events;   // host staging of drained device events
     std::vector<int32_t> st_members;
@@ -193,15 +192,14 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
         k_data<<<E->sms, 512, 0, s>>>(d, d.dp, d.dctl, 0);
         if (ev) mark(ev[7], s);
         if (d.dp.decode_on) {
-            if (E->tc_decode == 2)
+            if (E->tc_decode) {
                 if (d.dp.Hq / d.dp.Hkv <= 8)
                     k_decode_tc05<8><<<E->sms, T5_THREADS, T5_SMEM, s>>>(d, d.dp, d.dctl, E->kvmap);
                 else
                     k_decode_tc05<16><<<E->sms, T5_THREADS, T5_SMEM, s>>>(d, d.dp, d.dctl, E->kvmap);
-            else if (E->tc_decode == 1)
-                k_decode_tc<<<E->sms, TC_WARPS * 32, TC_SMEM, s>>>(d, d.dp, d.dctl, E->kvmap);
-            else
+            } else {
                 k_decode<<<E->sms * 8, DEC_T, 0, s>>>(d, d.dp, d.dctl);
+            }
             k_decode_reduce<<<E->sms * 8, 128, 0, s>>>(d, d.dp, d.dctl);
         }
         if (ev) mark(ev[8], s);
@@ -504,11 +502,9 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (cr != CUDA_SUCCESS) { co_destroy(E); return fail(CO_ECUDA, "tensor map encode failed"); }
-            cudaFuncSetAttribute(k_decode_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
             cudaFuncSetAttribute(k_decode_tc05<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, T5_SMEM);
             cudaFuncSetAttribute(k_decode_tc05<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, T5_SMEM);
-            const char* dk = getenv("CO_DECODE_KERNEL");
-            E->tc_decode = (dk && std::string(dk) == "mma_sync") ? 1 : 2;
+            E->tc_decode = true;
         }
     }
     AL(d.l_tri_key, n); AL(d.am_rhi, n3); AL(d.am_rlo, n3); AL(d.rank_to_idx, n);

@@ -31,7 +31,7 @@
 // group 1.
 #pragma once
 #include <cuda.h>
-#include "decode_tc.cuh"
+#include "decode_common.cuh"
 
 namespace co {
 

@@ -15,11 +15,11 @@ pytestmark = pytest.mark.gpu
 SMALL = dict(layers=2, kv_heads=2, q_heads=4)
 
 
-def _engine(seed, decode=True):
+def _engine(seed, decode=True, layout=SMALL, split=64):
     import paper_2503_13773_b200 as P
     reqs, cfg = build_product(case_params(seed))
     pages = cfg.capacity_tokens // cfg.sched.small_block_b
-    kv = P.KVLayout(**SMALL, host_swap_pages=16 * pages + 64, decode=decode, decode_split=64)
+    kv = P.KVLayout(**layout, host_swap_pages=16 * pages + 64, decode=decode, decode_split=split)
     return P.Engine(reqs, cfg, kv=kv), reqs, cfg
 
 
@@ -55,17 +55,24 @@ def test_swaps_really_move_bytes(cuda_ok):
     assert moved > 0
 
 
-@pytest.mark.parametrize("seed", [1, 5])
-def test_decode_matches_fp32_reference(cuda_ok, seed):
-    eng, _, _ = _engine(seed, decode=True)
+# (seed, layout, split): G = 2 and G = 16 query heads per KV head (the
+# tcgen05 kernel's 8- and 16-head softmax variants), splits shorter and
+# longer than its 128-position tile
+DECODE_CASES = [(1, SMALL, 64), (5, SMALL, 64), (2, dict(layers=1, kv_heads=1, q_heads=16), 300),
+                (6, dict(layers=2, kv_heads=2, q_heads=16), 512)]
+
+
+@pytest.mark.parametrize("seed,layout,split", DECODE_CASES)
+def test_decode_matches_fp32_reference(cuda_ok, seed, layout, split):
+    eng, _, _ = _engine(seed, decode=True, layout=layout, split=split)
     checked = 0
     for _ in range(400):
         if not eng.step():
             break
         rids, ctx, out, step_id = eng.last_decode()
         for k in range(0, len(rids), max(1, len(rids) // 3)):
-            ref = decode_reference(rids[k], int(ctx[k]), step_id, SMALL["layers"], SMALL["q_heads"],
-                                   SMALL["kv_heads"])
+            ref = decode_reference(rids[k], int(ctx[k]), step_id, layout["layers"], layout["q_heads"],
+                                   layout["kv_heads"])
             err = np.abs(out[k] - ref).max() / max(np.abs(ref).max(), 1e-6)
             assert err <= 1e-2, f"member {rids[k]} ctx {ctx[k]}: rel err {err}"
             checked += 1

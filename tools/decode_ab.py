@@ -1,5 +1,5 @@
 """Development aid: the bench decode leg (config 5) with the kernel chosen by
-CO_DECODE_KERNEL (unset = tcgen05, mma_sync = the mma.sync kernel)."""
+the engine's decode kernel."""
 import json
 import os
 import sys
@@ -8,6 +8,6 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 
 r = bench.decode_leg(0, warm_steps=int(os.environ.get("WARM", "6000")))
-print(json.dumps({"kernel": os.environ.get("CO_DECODE_KERNEL", "tcgen05"), "tok_s": r["value"],
+print(json.dumps({"tok_s": r["value"],
                   "frac": r["roofline"]["frac"], "gbs": r["roofline"]["achieved"],
                   "ms": r["decode_ms_per_step"], "integrity": r["kv_integrity"]}))
