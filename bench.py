@@ -398,11 +398,13 @@ def main():
     if args.impl == "reference":
         reference_arm(args, rank, world)
         return
-    if world > 1:
+    if world > 1 or "LOCAL_RANK" in os.environ:
+        # under torchrun (any N, so the 1-GPU box exercises the same path):
+        # NCCL process group + the per-iteration global-reserve all-reduce
         import torch
         import torch.distributed as td
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
-        td.init_process_group("nccl")
+        td.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
         dist = td
     device_arm(args, rank, world, dist)
     if dist:
