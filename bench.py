@@ -257,6 +257,46 @@ def decode_leg(dev, warm_steps=6000, k=10):
                       f"{warm_steps} warm steps"}
 
 
+def costmodel_leg(dev):
+    """swap and recompute latencies measured on this B200
+    (Llama-2-70B layout; swap = the engine's k_data round trip, recompute = a
+    bf16 prefill proxy), fitted with the reference's estimators; then BASELINE
+    config 3 (2x-rate heavy preemption) runs with those hardware-true costs and
+    the Llama-2-70B KV data plane, so its preemptions move real bytes."""
+    import dataclasses
+    import paper_2503_13773_b200 as P
+    from paper_2503_13773_b200 import costprofile as cp
+    from tests.cases import config3
+    t0 = time.perf_counter()
+    res = cp.hardware_truth(kv_layout=P.KVLayout.llama2_70b(decode=False), dims=cp.ModelDims.llama2_70b(),
+                            device=dev)
+    t_prof = time.perf_counter() - t0
+    reqs, cfg = config3()
+    cfg = dataclasses.replace(cfg, truth=res["truth"])
+    kv = P.KVLayout.llama2_70b(host_swap_pages=2048, decode=False)
+    eng = P.Engine(reqs, cfg, device=dev, kv=kv)
+    t0 = time.perf_counter()
+    eng.run_steps(0)
+    wall = time.perf_counter() - t0
+    evs = eng.events
+    st = eng.data_stats()
+    iters = sum(1 for e in evs if e["ev"] == "iter")
+    pre = [e for e in evs if e["ev"] == "preempt"]
+    n_swap = sum(1 for e in pre if e["strategy"] == "swap")
+    bad, checked = eng.kv_verify()
+    eng.close()
+    return {"metric": "B200-fitted swap/recompute cost models",
+            "model": "Llama-2-70B KV (327,680 B/token)",
+            "swap_ms": res["swap"], "recompute_ms": res["recompute"], "sweet_spot_tokens": res["sweet_spot"],
+            "crossover": res["crossover_note"] or "crossover inside the range",
+            "profile_s": t_prof,
+            "config3_with_fitted_costs": {
+                "iterations": iters, "preemptions": len(pre), "swaps": n_swap, "recomputes": len(pre) - n_swap,
+                "swap_out_gb": st["swap_out_bytes"] / 1e9, "swap_in_gb": st["swap_in_bytes"] / 1e9,
+                "wall_s": wall, "iterations_per_s": iters / wall,
+                "kv_integrity": {"mismatches": bad, "checked": checked}}}
+
+
 def peak_kind_label(kind):
     return f"{kind} (MEASURED_PEAKS.json hbm_gbs)" if kind == "measured" else kind
 
@@ -354,6 +394,10 @@ def device_arm(args, rank, world, dist):
             extra["decode"] = decode_leg(dev)
         except Exception as exc:
             extra["decode"] = {"error": repr(exc)}
+        try:
+            extra["costmodel"] = costmodel_leg(dev)
+        except Exception as exc:
+            extra["costmodel"] = {"error": repr(exc)}
     line = {
         "metric": METRIC, "value": decisions / (dev_ms * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,

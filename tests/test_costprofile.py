@@ -1,0 +1,86 @@
+"""Row (f).4: hardware-true swap / recompute cost models.  The restated
+estimators are pinned to the unmodified reference's fits on its own profile
+samples (tests/golden/fit_golden.json, oracle/make_fit_golden.py); on the GPU
+the models are fitted from latencies measured on the B200 and drive an engine
+run that stays bit-identical to the CPU oracle."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2503_13773_b200 import costprofile as cp
+from paper_2503_13773_b200.config import RecomputeModel, SwapModel
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "fit_golden.json")
+
+
+def _cases():
+    with open(GOLDEN) as fh:
+        return json.load(fh)
+
+
+@pytest.mark.parametrize("case", _cases(), ids=lambda c: c["name"])
+def test_fits_match_reference(case):
+    sm = cp.fit_swap([tuple(p) for p in case["swap_samples"]])
+    rm = cp.fit_recompute([tuple(p) for p in case["recompute_samples"]])
+    for k, v in case["swap"].items():
+        assert getattr(sm, k) == pytest.approx(v, rel=1e-12, abs=1e-15), k
+    assert rm.beta_r == case["recompute"]["beta_r"]
+    for k in ("alpha_r", "kappa_r", "eps_r"):
+        assert getattr(rm, k) == pytest.approx(case["recompute"][k], rel=1e-9, abs=1e-15), k
+    if case["error"] is None:
+        assert cp.sweet_spot(rm, sm) == case["sweet_spot"]
+    else:
+        with pytest.raises(ValueError, match=case["error"].split(":")[0]):
+            cp.sweet_spot(rm, sm)
+
+
+def test_decision_spot_encodings():
+    swap_cheap = SwapModel(gamma_s=0.001, delta_s=0.0)
+    rec_dear = RecomputeModel(alpha_r=0.0, beta_r=2.0, kappa_r=0.01, eps_r=1.0)
+    assert cp.decision_spot(rec_dear, swap_cheap) == 0  # swap dominates -> always swap
+    rec_cheap = RecomputeModel(alpha_r=0.0, beta_r=2.0, kappa_r=1e-6, eps_r=1e-6)
+    assert cp.decision_spot(rec_cheap, SwapModel(gamma_s=0.01, delta_s=1.0)) == 1 << 62
+    assert cp.decision_spot(RecomputeModel(1e-6, 2.0, 0.0, 0.0), SwapModel(0.002, 8.0)) == 4000
+
+
+def test_fit_validation_matches_reference_errors():
+    with pytest.raises(ValueError, match="at least 2"):
+        cp.fit_swap([(1.0, 1.0)])
+    with pytest.raises(ValueError, match="degenerate"):
+        cp.fit_swap([(5.0, 1.0), (5.0, 2.0)])
+    with pytest.raises(ValueError, match="at least 8"):
+        cp.fit_recompute([(float(s), 1.0) for s in range(1, 5)])
+    with pytest.raises(ValueError, match="positive"):
+        cp.fit_recompute([(float(s), -1.0) for s in range(1, 10)])
+
+
+def test_default_lengths_follow_profile_command():
+    ls = cp.default_lengths(16, 8192, 12)
+    assert ls == sorted(set(ls)) and ls[0] == 16 and ls[-1] == 8192
+
+
+@pytest.mark.gpu
+def test_hardware_truth_drives_a_parity_run(cuda_ok):
+    from oracle.cacheopt_oracle import CacheOptOracle
+    import dataclasses
+    import paper_2503_13773_b200 as P
+    from tests.cases import build_product, case_params
+
+    res = cp.hardware_truth(lengths=[64, 256, 1024, 2048, 4096, 6144, 8192, 12288],
+                            dims=cp.ModelDims.llama2_13b())
+    swap = res["samples"]["swap"]
+    rec = res["samples"]["recompute"]
+    assert all(ms > 0 for _, ms in swap + rec)
+    assert swap[-1][1] > swap[0][1] and rec[-1][1] > rec[0][1]  # latency grows with S
+    assert res["swap"]["gamma_s"] > 0
+    truth = res["truth"]
+    reqs, cfg = build_product(case_params(5))
+    cfg = dataclasses.replace(cfg, truth=truth)
+    eng = P.Engine(reqs, cfg)
+    eng.run_steps(0)
+    orc = CacheOptOracle(reqs, cfg)
+    orc.run()
+    assert eng.events == orc.events
+    eng.close()
