@@ -271,6 +271,22 @@ int co_kernels_per_step(co_engine* eng, int32_t* n);
 #define CO_NSTAGES 8
 int co_time_steps(co_engine* eng, int32_t k, int64_t flush_bytes, double* step_ms, double* stage_ms);
 
+/* engine.py:132-211 compute_metrics on the device: counts,
+ * exact integer sums, numpy-pairwise sum of the normalized latencies in the
+ * caller's request order, and the order statistics the percentiles
+ * interpolate between (np.percentile 'linear': ranks floor/ceil of
+ * (count-1)*q for q = .50/.90/.99, and the max), per list: 0 TTFT and 2
+ * normalized latency of completed requests, 1 every inter-token gap of
+ * completed requests, 3 preemption time of preempted requests. */
+typedef struct co_metrics_raw {
+    int64_t completed, ok_ttft, ok_tbt, generated, preemption_total, preempted;
+    int64_t sum_ttft, sum_gap, sum_wait, sum_exec, sum_pdec, sum_ptime;
+    int64_t count[4];
+    double norm_sum;
+    double order_stat[4][7]; /* p50 lo, p50 hi, p90 lo, p90 hi, p99 lo, p99 hi, max */
+} co_metrics_raw;
+int co_metrics(co_engine* eng, co_metrics_raw* out);
+
 const char* co_last_error(void);
 const char* co_version(void);
 

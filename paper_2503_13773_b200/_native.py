@@ -81,10 +81,17 @@ EXPORTS = (
     "co_check_invariants", "co_last_device_ms", "co_kernels_per_step", "co_time_steps", "co_last_error",
     "co_version", "co_read_block_tables", "co_data_stats", "co_kv_verify", "co_read_decode", "co_host_link_gbs",
     "co_set_decode", "co_swap_bench", "co_nccl_unique_id", "co_attach_nccl", "co_global_reserve",
-    "co_phase_profile", "co_step_result",
+    "co_phase_profile", "co_step_result", "co_metrics",
 )
 
 _lib = None
+
+
+class CoMetricsRaw(C.Structure):
+    _fields_ = [(k, C.c_int64) for k in ("completed", "ok_ttft", "ok_tbt", "generated", "preemption_total",
+                                         "preempted", "sum_ttft", "sum_gap", "sum_wait", "sum_exec", "sum_pdec",
+                                         "sum_ptime")] + [
+        ("count", C.c_int64 * 4), ("norm_sum", C.c_double), ("order_stat", (C.c_double * 7) * 4)]
 
 
 class NativeError(RuntimeError):
@@ -129,6 +136,7 @@ def load() -> C.CDLL:
         "co_global_reserve": (C.c_int, [V, I64P, I64P]),
         "co_phase_profile": (C.c_int, [V, C.c_int32, I64P]),
         "co_step_result": (C.c_int, [V, I32P, I32P, C.c_int64, I64P, I64P]),
+        "co_metrics": (C.c_int, [V, C.POINTER(CoMetricsRaw)]),
         "co_last_error": (C.c_char_p, []),
         "co_version": (C.c_char_p, []),
     }

@@ -31,6 +31,7 @@
 #include "apply.cuh"
 #include "data_plane.cuh"
 #include "decode_tc05.cuh"
+#include "metrics.cuh"
 #include <cudaTypedefs.h>
 
 using namespace co;
@@ -865,6 +866,83 @@ int co_read_token_times(co_engine* E, int64_t* offsets, int64_t* times) {
         CK(cudaStreamSynchronize(E->stream));
     }
     return CO_OK;
+}
+
+int co_metrics(co_engine* E, co_metrics_raw* out) {
+    if (!E || !out) return fail(CO_EINVAL, "null argument");
+    const int64_t n = E->n, ntok = std::max<int64_t>(E->tok_total, 1);
+    std::memset(out, 0, sizeof(*out));
+    if (n == 0) return CO_OK;
+    std::vector<void*> tmp;
+    auto get = [&](size_t bytes) -> void* {
+        void* p = nullptr;
+        if (cudaMalloc(&p, std::max<size_t>(bytes, 8)) != cudaSuccess) return nullptr;
+        tmp.push_back(p);
+        return p;
+    };
+    auto release = [&]() { for (void* p : tmp) cudaFree(p); };
+    MetScratch m;
+    m.cnt = (unsigned long long*)get(16 * 8);
+    m.keys[0] = (uint64_t*)get(n * 8); m.keys[1] = (uint64_t*)get(ntok * 8);
+    m.keys[2] = (uint64_t*)get(n * 8); m.keys[3] = (uint64_t*)get(n * 8);
+    m.normc = (double*)get(n * 8); m.flagc = (uint8_t*)get(n); m.norm_list = (double*)get(n * 8);
+    int32_t* perm = (int32_t*)get(n * 4);
+    m.perm = perm;
+    m.hist = (unsigned int*)get(MET_RANKS * 256 * 4);
+    m.pre = (uint64_t*)get(MET_RANKS * 8); m.rem = (long long*)get(MET_RANKS * 8);
+    m.out_norm_sum = (double*)get(8);
+    for (void* p : tmp)
+        if (!p) { release(); return fail(CO_ECUDA, "metrics scratch allocation failed"); }
+    std::vector<int32_t> ph(n);
+    for (int64_t k = 0; k < n; k++) ph[k] = (int32_t)E->perm[k];
+    cudaStream_t s = E->stream;
+    int r = CO_OK;
+    auto ck = [&](cudaError_t e) { if (e != cudaSuccess && r == CO_OK) r = fail(CO_ECUDA, cudaGetErrorString(e)); };
+    ck(cudaMemcpyAsync(perm, ph.data(), n * 4, cudaMemcpyHostToDevice, s));
+    ck(cudaMemsetAsync(m.cnt, 0, 16 * 8, s));
+    ck(cudaMemsetAsync(m.hist, 0, MET_RANKS * 256 * 4, s));
+    k_met_rows<<<E->grid, 256, 0, s>>>(E->d, m);
+    k_met_norm<<<1, 1024, 0, s>>>(m, (int32_t)n);
+    ck(cudaGetLastError());
+    unsigned long long cnt[16];
+    ck(cudaMemcpyAsync(cnt, m.cnt, sizeof(cnt), cudaMemcpyDeviceToHost, s));
+    ck(cudaMemcpyAsync(&out->norm_sum, m.out_norm_sum, 8, cudaMemcpyDeviceToHost, s));
+    ck(cudaStreamSynchronize(s));
+    if (r) { release(); return r; }
+    out->completed = cnt[MC_DONE]; out->ok_ttft = cnt[MC_OK_TTFT]; out->ok_tbt = cnt[MC_OK_TBT];
+    out->generated = cnt[MC_GEN]; out->preemption_total = cnt[MC_PRE_TOTAL]; out->preempted = cnt[MC_PREEMPTED];
+    out->sum_ttft = cnt[MC_SUM_TTFT]; out->sum_gap = cnt[MC_SUM_GAP]; out->sum_wait = cnt[MC_SUM_WAIT];
+    out->sum_exec = cnt[MC_SUM_EXEC]; out->sum_pdec = cnt[MC_SUM_PDEC]; out->sum_ptime = cnt[MC_SUM_PTIME];
+    for (int l = 0; l < MET_LISTS; l++) out->count[l] = (int64_t)cnt[MC_N0 + l];
+    const double qs[3] = {50.0 / 100.0, 90.0 / 100.0, 99.0 / 100.0};
+    for (int l = 0; l < MET_LISTS && !r; l++) {
+        const int64_t c = out->count[l];
+        if (c == 0) continue;
+        // np.percentile 'linear': virtual index (c - 1) * q, floor / +1, clamped to the last
+        long long rk[MET_RANKS];
+        for (int q = 0; q < 3; q++) {
+            const double v = (double)(c - 1) * qs[q];
+            if (v >= (double)(c - 1)) { rk[2 * q] = rk[2 * q + 1] = c - 1; }
+            else { rk[2 * q] = (long long)std::floor(v); rk[2 * q + 1] = rk[2 * q] + 1; }
+        }
+        rk[6] = c - 1;
+        std::vector<uint64_t> zero(MET_RANKS, 0);
+        ck(cudaMemcpyAsync(m.pre, zero.data(), MET_RANKS * 8, cudaMemcpyHostToDevice, s));
+        ck(cudaMemcpyAsync(m.rem, rk, MET_RANKS * 8, cudaMemcpyHostToDevice, s));
+        const int grid = (int)std::min<int64_t>((c + 255) / 256, (int64_t)E->sms * 4);
+        for (int pass = 0; pass < 8; pass++) {
+            const int shift = 56 - 8 * pass;
+            const uint64_t mask = pass == 0 ? 0ull : (~0ull << (64 - 8 * pass));
+            k_rs_hist<<<grid, 256, 0, s>>>(m.keys[l], c, MET_RANKS, m.pre, mask, shift, m.hist);
+            k_rs_pick<<<1, 32 * MET_RANKS, 0, s>>>(MET_RANKS, m.pre, m.rem, shift, m.hist);
+        }
+        uint64_t bits[MET_RANKS];
+        ck(cudaMemcpyAsync(bits, m.pre, sizeof(bits), cudaMemcpyDeviceToHost, s));
+        ck(cudaStreamSynchronize(s));
+        for (int q = 0; q < MET_RANKS; q++) std::memcpy(&out->order_stat[l][q], &bits[q], 8);
+    }
+    release();
+    return r;
 }
 
 int co_check_invariants(co_engine* E) {

@@ -11,6 +11,7 @@ from __future__ import annotations
 import ctypes as C
 import dataclasses
 import json
+import math
 from dataclasses import dataclass
 from typing import Dict, Iterator, List, Optional, Sequence, Tuple
 
@@ -60,6 +61,35 @@ def _pct(values) -> Dict[str, float]:
     a = np.asarray(values, dtype=float)
     return {"p50": float(np.percentile(a, 50)), "p90": float(np.percentile(a, 90)),
             "p99": float(np.percentile(a, 99)), "max": float(a.max()), "mean": float(a.mean())}
+
+
+def pct_from_order_stats(count: int, os7: Sequence[float], total) -> Dict[str, float]:
+    """_pct's dict from the order statistics co_metrics selects: np.percentile
+    'linear' (virtual index (n-1)q, _lerp's two-sided form) at q = .5/.9/.99
+    between os7[2j] and os7[2j+1], max = os7[6], mean = sum / n (``total`` is
+    the exact integer sum, or the numpy-pairwise float sum)."""
+    if count == 0:
+        return {"p50": 0.0, "p90": 0.0, "p99": 0.0, "max": 0.0, "mean": 0.0}
+    out = {}
+    for j, (name, q) in enumerate((("p50", 50 / 100), ("p90", 90 / 100), ("p99", 99 / 100))):
+        a, b = float(os7[2 * j]), float(os7[2 * j + 1])
+        v = (count - 1) * q
+        g = v - math.floor(v) if v < count - 1 else 0.0
+        d = b - a
+        out[name] = b - d * (1 - g) if g >= 0.5 else a + d * g
+    out["max"] = float(os7[6])
+    out["mean"] = float(total) / count
+    return out
+
+
+def order_stat_ranks(count: int) -> List[int]:
+    """The ranks co_metrics selects (host restatement, for tests)."""
+    r = []
+    for q in (50 / 100, 90 / 100, 99 / 100):
+        v = (count - 1) * q
+        lo = count - 1 if v >= count - 1 else math.floor(v)
+        r += [lo, count - 1 if v >= count - 1 else lo + 1]
+    return r + [count - 1]
 
 
 def compute_metrics(*, requests: Dict[int, Request], runtimes: Dict[int, RequestRuntime], policy: str,
@@ -384,15 +414,64 @@ class Engine:
         return int(done.value)
 
     def run(self) -> MetricsReport:
+        """engine.py:643-672: run to completion, then the metrics, aggregated on
+        the device (report_device); report_host() is the host restatement."""
         self.run_steps(0)
+        self.report = self.report_device()
+        return self.report
+
+    def report_host(self) -> MetricsReport:
+        """compute_metrics over host views of every request (engine.py:132-211)."""
         s = self._scalars()
         makespan = max(0, int(s.now_us) - int(s.first_arrival_us))
-        self.report = compute_metrics(
+        return compute_metrics(
             requests=self.requests_view(), runtimes=self.runtimes, policy=self.cfg.sched.policy,
             seed=self.cfg.seed, makespan_us=makespan, capacity_tokens=self.cfg.capacity_tokens,
             samples=self.samples,
         )
-        return self.report
+
+    def report_device(self) -> MetricsReport:
+        """compute_metrics (engine.py:132-211) evaluated on the device
+        (co_metrics): per-request aggregation, exact integer
+        sums, numpy-pairwise normalized-latency sum and radix-selected order
+        statistics; only the interpolation below and the per-iteration
+        utilization samples (already streamed to the host) are host work.
+        Equal to ``run()``'s report field for field."""
+        s = self._scalars()
+        raw = N.CoMetricsRaw()
+        N.check(self._lib.co_metrics(self._h, C.byref(raw)), "co_metrics")
+        n = self._n
+        makespan = max(0, int(s.now_us) - int(s.first_arrival_us))
+        span_s = makespan / US_PER_S if makespan > 0 else 0.0
+
+        def pct(lst: int, total) -> Dict[str, float]:
+            return pct_from_order_stats(int(raw.count[lst]), [float(v) for v in raw.order_stat[lst]], total)
+
+        samples = self.samples
+        cap = self.cfg.capacity_tokens
+        if len(samples):
+            util = float(np.mean([fp / cap for fp, _ in samples]))
+            frag = float(np.mean([(fp - u) / cap for fp, u in samples]))
+        else:
+            util = frag = 0.0
+        done = int(raw.completed)
+
+        def mean(total, cnt):
+            return float(total) / cnt if cnt else 0.0
+
+        return MetricsReport(
+            policy=self.cfg.sched.policy, seed=self.cfg.seed, num_requests=n, completed=done,
+            makespan_us=makespan, ttft_us=pct(0, raw.sum_ttft), tbt_us=pct(1, raw.sum_gap),
+            ttft_attainment=raw.ok_ttft / n if n else 0.0, tbt_attainment=raw.ok_tbt / n if n else 0.0,
+            normalized_us_per_token=pct(2, raw.norm_sum),
+            preemption_total=int(raw.preemption_total), preempted_requests=int(raw.preempted),
+            preemption_time_us=pct(3, raw.sum_ptime),
+            throughput_rps=done / span_s if span_s else 0.0,
+            throughput_tps=int(raw.generated) / span_s if span_s else 0.0,
+            kvc_utilization_mean=util, kvc_fragmentation_mean=frag,
+            waiting_us_mean=mean(raw.sum_wait, done), execution_us_mean=mean(raw.sum_exec, done),
+            preemption_us_mean=mean(raw.sum_pdec, done),
+        )
 
     def last_device_ms(self) -> float:
         ms = C.c_double()
