@@ -163,8 +163,8 @@ class CacheOptOracle:
         ids = [r.id for r in requests]
         if len(set(ids)) != len(ids):
             raise ValueError("request ids must be unique")
-        if cfg.sched.policy != "cacheopt":
-            raise ValueError("oracle restates the cacheopt policy only")
+        if cfg.sched.policy not in ("cacheopt", "vllm_block", "sarathi_chunked", "rlp", "s3"):
+            raise ValueError(f"unknown policy {cfg.sched.policy!r}")
         if cfg.sched.invert_amortization:
             raise ValueError("invert_amortization is not restated")
         self.cfg = cfg
@@ -593,7 +593,164 @@ class CacheOptOracle:
             return int(self.slo_ttft[i]) - (self.now - int(self.arr[i]))
         return int(self.slo_tbt[i]) - (self.now - int(self.last_tok[i]))
 
+    # -- baseline planners (scheduler.py:760-936) ---------------------------
+
+    def _baseline_views(self):
+        live = np.nonzero((self.state >= WAITING) & (self.state <= PREEMPTED))[0]
+        running = [int(i) for i in live if self.state[i] == RUNNING]
+        waiting = [int(i) for i in live if self.state[i] != RUNNING]  # _live order (engine.py:321-324)
+        eff = {i: self.eff_alloc(i) for i in running + waiting}
+        ready = {i: self.state[i] != RUNNING or self.now >= self.ready_at[i] for i in running + waiting}
+        return running, waiting, eff, ready
+
+    def _cost(self, i, grant):
+        """_FreeTracker.alloc_cost (scheduler.py:350-354)."""
+        if self.holds[i] and self.host[i] >= 0:
+            return 0
+        h = int(self.granted[i]) if self.holds[i] else 0
+        return self._fp(h + grant) - self._fp(h)
+
+    def _fcfs(self, waiting):
+        """scheduler.py:760-766: preempted first, FCFS (index = (arrival, id)) within each."""
+        return [i for i in waiting if self.state[i] == PREEMPTED] + [i for i in waiting if self.state[i] != PREEMPTED]
+
+    def _plan_dict(self, members, preempt, actions):
+        bt = sum(t for _, t in members)
+        return dict(members=members, preempt=preempt, actions=actions, claims=[], deferred=[],
+                    overflow=bt > self.cfg.sched.token_budget, batch_tokens=bt)
+
+    def plan_vllm_block(self, chunked=False):
+        """scheduler.py:769-838 (chunked: sarathi_chunked)."""
+        sc = self.cfg.sched
+        running, waiting, eff, ready = self._baseline_views()
+        running = [i for i in running if ready[i]]
+        free = self.free_tokens()
+        step = sc.vllm_block_tokens
+        budget = sc.token_budget
+        members, preempt, actions = [], [], []
+        removed = set()
+        returned = {i: eff[i] < int(self.used[i]) + 1 for i in running}  # every view here is RUNNING
+        for i in running:  # sorted by (arrival, id) = index order
+            if not returned[i] or i in removed:
+                continue
+            while True:
+                cost = self._cost(i, step)
+                if cost <= free:
+                    actions.append(("grow", i, step, 0, -1, 0))
+                    free -= cost
+                    break
+                cands = [x for x in running if x not in removed and self.holds[x]]
+                if not cands:
+                    break
+                victim = cands[-1]  # max (arrival, id)
+                preempt.append((victim, RECOMPUTE))
+                removed.add(victim)
+                free += self.release_gain(victim)
+                if victim == i:
+                    break
+        grown = {a[1] for a in actions}
+        for i in running:
+            if i in removed or self.state[i] != RUNNING:
+                continue
+            if self.prefill[i] < self.kv_need[i]:
+                if not chunked:
+                    continue
+                chunk = min(int(self.kv_need[i] - self.prefill[i]), budget)
+                if chunk > 0:
+                    members.append((i, chunk))
+                    budget -= chunk
+                continue
+            if returned[i] and i not in grown:
+                continue
+            if budget >= 1:
+                members.append((i, 1))
+                budget -= 1
+        for i in self._fcfs(waiting):
+            chunk = int(self.kv_need[i] - self.prefill[i])
+            alloc = ((int(self.kv_need[i]) + 1 + step - 1) // step) * step
+            cost = self._fp(alloc)
+            if cost > free:
+                break
+            if chunk > 0:
+                if chunked:
+                    chunk = min(chunk, budget)
+                    if chunk < 1:
+                        break
+                elif budget < chunk:
+                    break
+                members.append((i, chunk))
+                budget -= chunk
+            actions.append(("allocate", i, alloc, 0, -1, 0))
+            free -= cost
+        return self._plan_dict(members, preempt, actions)
+
+    def _plan_evict_returned(self, strat, order, demand):
+        """scheduler.py:841-936 shared shape of rlp / s3: returned requests
+        evict themselves, decodes join, then admissions in `order` until the
+        first that does not fit."""
+        sc = self.cfg.sched
+        running, waiting, eff, ready = self._baseline_views()
+        running = [i for i in running if ready[i]]
+        free = self.free_tokens()
+        budget = sc.token_budget
+        members, actions = [], []
+        preempt = [(i, strat) for i in running if eff[i] < int(self.used[i]) + 1]
+        removed = {i for i, _ in preempt}
+        for i in running:
+            if i in removed or self.state[i] != RUNNING or self.prefill[i] < self.kv_need[i]:
+                continue
+            if budget >= 1:
+                members.append((i, 1))
+                budget -= 1
+        for i in order([i for i in waiting if ready[i]]):
+            chunk = int(self.kv_need[i] - self.prefill[i])
+            alloc = demand(i, eff[i])
+            cost = self._cost(i, alloc)
+            if cost > free:
+                break
+            if chunk > 0:
+                if budget < chunk:
+                    break
+                members.append((i, chunk))
+                budget -= chunk
+            actions.append(("grow" if self.holds[i] else "allocate", i, alloc, 0, -1, 0))
+            free -= cost
+        return self._plan_dict(members, preempt, actions)
+
+    def plan_rlp(self):
+        """scheduler.py:841-890: shortest predicted remaining bucket first."""
+        pad = self.cfg.sched.rlp_padding
+
+        def rem(i):
+            return max(1, int(self.pred[i] - self.gen[i]))
+
+        def order(w):
+            return sorted(w, key=lambda i: (rem(i) // 50, int(self.arr[i]), self.rid[i]))
+        return self._plan_evict_returned(RECOMPUTE, order,
+                                         lambda i, e: int(self.kv_need[i]) + rem(i) + pad - e)
+
+    def plan_s3(self):
+        """scheduler.py:893-936: FCFS, bucketed output demand doubling per preemption."""
+        bt = self.cfg.sched.s3_bucket_tokens
+
+        def demand(i, e):
+            out = max(1, -(-max(1, int(self.pred[i])) // bt)) * bt * (2 ** int(self.pcount[i]))
+            return max(0, int(self.kv_need[i]) + out - e)
+        return self._plan_evict_returned(SWAP, self._fcfs, demand)
+
     def plan(self):
+        pol = self.cfg.sched.policy
+        if pol == "vllm_block":
+            return self.plan_vllm_block(False)
+        if pol == "sarathi_chunked":
+            return self.plan_vllm_block(True)
+        if pol == "rlp":
+            return self.plan_rlp()
+        if pol == "s3":
+            return self.plan_s3()
+        return self.plan_cacheopt()
+
+    def plan_cacheopt(self):
         """scheduler.py:408-753.  The pool is not mutated while planning, so
         snapshot quantities (engine.py:284-317) are read straight from it."""
         cfg = self.cfg

@@ -29,6 +29,8 @@ OUT = os.path.join(ROOT, "tests", "golden")
 sys.path.insert(0, ROOT)
 
 SEEDS = [0, 1, 2, 5, 9, 13, 21, 34]
+BASELINE_CASES = [("vllm_block", 5), ("vllm_block", 13), ("sarathi_chunked", 13), ("sarathi_chunked", 9),
+                  ("rlp", 6), ("s3", 2), ("s3", 13)]
 
 
 def ref_build(params):
@@ -52,7 +54,7 @@ def ref_build(params):
         swap_true=SwapModel(tr["gamma_s"], tr["delta_s"]),
         recompute_true=RecomputeModel(tr["alpha_r"], tr["beta_r"], tr["kappa_r"], tr["eps_r"]))
     cfg = EngineConfig(capacity_tokens=params["capacity"], reserved_blocks=params["reserved"],
-                       sched=SchedulerConfig(policy="cacheopt", **params["sched"]),
+                       sched=SchedulerConfig(**{"policy": "cacheopt", **params["sched"]}),
                        predictor=PredictorConfig(**params["pred"]), truth=truth, seed=seed,
                        fixed_confidence=params["fixed_confidence"],
                        validate_every=params["validate_every"])
@@ -119,6 +121,15 @@ def main():
         p = case_params(s)
         reqs, cfg = ref_build(p)
         run_and_store(f"case{s:02d}", p, reqs, cfg)
+    # the four baseline planners (scheduler.py:760-936) on regimes that preempt
+    for pol, s in BASELINE_CASES:
+        name = f"base_{pol}_case{s:02d}"
+        if only and name not in only:
+            continue
+        p = case_params(s)
+        p["sched"] = {**p["sched"], "policy": pol}
+        reqs, cfg = ref_build(p)
+        run_and_store(name, p, reqs, cfg)
     # config 2 window: 65,536 requests, first 60 steps (digest + final state only)
     if only and not only & {"config2_60", "config1", "config3"}:
         return

@@ -66,7 +66,7 @@ def build_product(params: dict):
         P.RecomputeModel(tr["alpha_r"], tr["beta_r"], tr["kappa_r"], tr["eps_r"]))
     cfg = P.EngineConfig(
         capacity_tokens=params["capacity"], reserved_blocks=params["reserved"],
-        sched=P.SchedulerConfig(policy="cacheopt", **params["sched"]),
+        sched=P.SchedulerConfig(**{"policy": "cacheopt", **params["sched"]}),
         predictor=P.PredictorConfig(**params["pred"]), truth=truth, seed=seed,
         fixed_confidence=params["fixed_confidence"], validate_every=params["validate_every"],
         record_events=params.get("record_events", True))
