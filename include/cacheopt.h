@@ -92,7 +92,15 @@ typedef struct co_config {
     int64_t host_swap_pages;        /* pinned host swap pool, in pages */
     int32_t decode;                 /* run the paged decode for each step's decode members */
     int32_t decode_split;           /* tokens per split-KV work item */
+    /* planner (scheduler.py:30 POLICIES; plan_batch dispatch :939-950) */
+    int32_t policy;                 /* CO_POLICY_* */
+    int32_t vllm_block_tokens;      /* scheduler.py:45 */
+    int32_t s3_bucket_tokens;       /* scheduler.py:46 */
+    int32_t rlp_padding;            /* scheduler.py:47 */
 } co_config;
+
+enum { CO_POLICY_CACHEOPT = 0, CO_POLICY_VLLM_BLOCK = 1, CO_POLICY_SARATHI_CHUNKED = 2, CO_POLICY_RLP = 3,
+       CO_POLICY_S3 = 4 };
 
 /* One trace, any order (the library sorts by (arrival_us, id) like
  * engine.py:241).  err_draw/flip_draw are the predictor noise draws of

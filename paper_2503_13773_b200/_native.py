@@ -41,7 +41,12 @@ class CoConfig(C.Structure):
         ("record_events", C.c_int32), ("padding", C.c_int32), ("_pad0", C.c_int32), ("s_star", C.c_int64),
         ("t_i_init_us", C.c_int64), ("kv_layers", C.c_int32), ("kv_heads", C.c_int32), ("q_heads", C.c_int32),
         ("head_dim", C.c_int32), ("host_swap_pages", C.c_int64), ("decode", C.c_int32), ("decode_split", C.c_int32),
+        ("policy", C.c_int32), ("vllm_block_tokens", C.c_int32), ("s3_bucket_tokens", C.c_int32),
+        ("rlp_padding", C.c_int32),
     ]
+
+
+POLICY_CODE = {"cacheopt": 0, "vllm_block": 1, "sarathi_chunked": 2, "rlp": 3, "s3": 4}
 
 
 class CoTrace(C.Structure):

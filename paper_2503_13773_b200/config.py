@@ -18,7 +18,7 @@ from typing import Optional, Tuple
 US_PER_S = 1_000_000
 
 POLICIES = ("cacheopt", "vllm_block", "rlp", "s3", "sarathi_chunked")
-DEVICE_POLICIES = ("cacheopt",)
+DEVICE_POLICIES = POLICIES
 VICTIM_RULES = ("slo", "fcfs")
 
 

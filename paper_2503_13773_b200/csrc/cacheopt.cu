@@ -298,6 +298,9 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
         return fail(CO_EINVAL, "invalid configuration scalar");
     if ((int64_t)cfg->reserved_blocks * cfg->block_size > cfg->capacity_tokens)
         return fail(CO_EINVAL, "reserve exceeds capacity");
+    if (cfg->policy < CO_POLICY_CACHEOPT || cfg->policy > CO_POLICY_S3 || cfg->vllm_block_tokens < 1 ||
+        cfg->s3_bucket_tokens < 1 || cfg->rlp_padding < 0)
+        return fail(CO_EINVAL, "invalid policy or policy parameter");
     if (cfg->capacity_tokens > (1ll << 30)) return fail(CO_EINVAL, "capacity_tokens too large for int32 records");
     const int64_t n = tr->n;
     if (n < 0 || n > (1ll << 30)) return fail(CO_EINVAL, "bad trace size");
@@ -390,6 +393,7 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     d.pad = cfg->padding; d.idbits = idbits; d.key_bits = key_bits; d.n_edges = cfg->n_slo_edges; d.token_step = cfg->token_step;
     d.rsv_target = cfg->reserved_blocks; d.eps = cfg->epsilon_us; d.capacity = cfg->capacity_tokens;
     d.s_star = cfg->s_star; d.s_max = lu->s_max;
+    d.policy = cfg->policy; d.vbt = cfg->vllm_block_tokens; d.s3b = cfg->s3_bucket_tokens; d.rlp_pad = cfg->rlp_padding;
     for (int k = 0; k < CO_MAX_SLO_EDGES; k++) d.edges[k] = k < cfg->n_slo_edges ? cfg->slo_edges_us[k] : 0;
     d.base_ms = cfg->iter_base_ms; d.per_token_ms = cfg->iter_per_token_ms;
     d.ev_cap = std::max<int64_t>(1 << 16, 8 * n + 4096);

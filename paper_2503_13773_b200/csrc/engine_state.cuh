@@ -54,6 +54,7 @@ struct Dev {
     int32_t n, bs, B, buffer_b, token_budget, prealloc_m, runway_iters, fcfs;
     int32_t record_events, validate_every, pad, idbits, n_edges, token_step, rsv_target;
     int32_t key_bits;            // composite sort key width: class(2) | blown(1) | time | idrank
+    int32_t policy, vbt, s3b, rlp_pad;  // planner (CO_POLICY_*) and the baselines' parameters
     int64_t eps, capacity, s_star, s_max, ev_cap, mem_cap, sample_cap;
     int64_t edges[CO_MAX_SLO_EDGES];
     double base_ms, per_token_ms;

@@ -128,7 +128,27 @@ __global__ void __launch_bounds__(256) k_classify(Dev d) {
                     const uint4* src = reinterpret_cast<const uint4*>(&v);
                     dst[0] = src[0]; dst[1] = src[1]; dst[2] = src[2]; dst[3] = src[3];
                 }
-                if (s == ST_WAITING || s == ST_PREEMPTED) {
+                if ((s == ST_WAITING || s == ST_PREEMPTED) && d.policy != CO_POLICY_CACHEOPT) {
+                    // baseline planners (scheduler.py:760-766, 869-873): FCFS by
+                    // (arrival, id) = id rank with preempted requests first (the
+                    // block-ordered blown list), or rlp's (bucket, arrival, id)
+                    uint64_t k;
+                    if (d.policy == CO_POLICY_RLP) {
+                        const int32_t r = d.pred[i] - d.gen[i];
+                        k = ((uint64_t)((r > 1 ? r : 1) / 50) << ib) | (uint64_t)d.idrank[i];
+                    } else {
+                        k = (uint64_t)d.idrank[i];
+                    }
+                    if (s == ST_PREEMPTED && d.policy != CO_POLICY_RLP) {
+                        is_blown = 1;
+                    } else {
+                        d.key0[i] = k;
+                        f0 = -2;
+                        nf0++;
+                        kmin = k < kmin ? k : kmin;
+                        kmax = k > kmax ? k : kmax;
+                    }
+                } else if (s == ST_WAITING || s == ST_PREEMPTED) {
                     // every waiting view is ready (engine.py:311-312); rt = D - now
                     const int64_t D = d.first_tok[i] < 0 ? d.arr[i] + d.slo_ttft[i] : d.last_tok[i] + d.slo_tbt[i];
                     const int64_t rt = D - now;

@@ -302,6 +302,139 @@ __device__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64
     }
 }
 
+// The reference's baseline planners (scheduler.py:760-936): vllm_block and
+// sarathi_chunked (one function, `chunked`), rlp and s3.  They are short
+// ordered greedy loops over the running set (arrival order) and the waiting
+// queue (classify keyed it FCFS, preempted first, or by rlp's bucket), so
+// thread 0 runs them; the queue is materialized in 256-item groups.
+template <class Ensure>
+__device__ void plan_baseline(const Dev& d, PlanSh& S, const int32_t* RUN, int32_t n_run, int32_t n_f0,
+                              int32_t n_blown, bool rcached, int32_t sid, Ensure& ensure) {
+    const int tid = threadIdx.x, bs = d.bs, pol = d.policy;
+    const bool vllm = pol == CO_POLICY_VLLM_BLOCK || pol == CO_POLICY_SARATHI_CHUNKED;
+    const bool chunked = pol == CO_POLICY_SARATHI_CHUNKED;
+    auto RV = [&](int32_t k) -> PV { return rcached ? S.rv[k] : view_of(d, RUN[k]); };
+    auto returned = [&](const PV& v) { return (v.flags & PV_RUNNING) && v.eff < v.used + 1; };
+    auto admit_one = [&](int32_t i, int64_t& budget) -> bool {  // false: stop admitting
+        const PV v = view_of(d, i);
+        int64_t chunk = (int64_t)v.kvn - v.pre, alloc, cost;
+        if (vllm) {  // scheduler.py:820-835: round_up(kv_need + 1), costed as a fresh footprint
+            alloc = (((int64_t)v.kvn + 1 + d.vbt - 1) / d.vbt) * d.vbt;
+            cost = fp_tokens(alloc, bs);
+        } else if (pol == CO_POLICY_RLP) {  // scheduler.py:874-877 rlp_demand
+            int64_t rem = (int64_t)d.pred[i] - d.gen[i];
+            alloc = (int64_t)v.kvn + (rem > 1 ? rem : 1) + d.rlp_pad - v.eff;
+            cost = pv_cost(v, alloc, bs);
+        } else {  // scheduler.py:917-921 s3_demand, doubling per preemption
+            const int64_t p = d.pred[i] > 1 ? d.pred[i] : 1;
+            const int64_t nb = (p + d.s3b - 1) / d.s3b;
+            const int32_t pc = d.pcount[i];
+            int64_t out = (nb > 1 ? nb : 1) * d.s3b;
+            out = pc >= 40 ? ((int64_t)1 << 62) : out << pc;  // beyond any pool: the loop breaks
+            alloc = (int64_t)v.kvn + out - v.eff;
+            if (alloc < 0) alloc = 0;
+            cost = alloc >= ((int64_t)1 << 61) ? alloc : pv_cost(v, alloc, bs);
+        }
+        if (cost > S.free) return false;
+        if (chunk > 0) {
+            if (chunked) {
+                chunk = chunk < budget ? chunk : budget;
+                if (chunk < 1) return false;
+            } else if (budget < chunk) {
+                return false;
+            }
+            push_mem(d, S, i, chunk);
+            budget -= chunk;
+        }
+        push_act(d, S, vllm ? A_ALLOCATE : ((v.flags & PV_HOLDS) ? A_GROW : A_ALLOCATE), i, alloc);
+        S.free -= cost;
+        return true;
+    };
+    if (tid == 0) {
+        int64_t budget = d.token_budget;
+        if (vllm) {
+            // grow exhausted decodes one block, evicting the newest holder (scheduler.py:781-802)
+            int32_t vp = n_run - 1;
+            for (int32_t k = 0; k < n_run; k++) {
+                const PV v = RV(k);
+                const int32_t i = RUN[k];
+                if (!(v.flags & PV_READY) || !returned(v) || d.st_removed[i] == sid) continue;
+                while (true) {
+                    const int64_t cost = pv_cost(v, d.vbt, bs);
+                    if (cost <= S.free) {
+                        push_act(d, S, A_GROW, i, d.vbt);
+                        S.free -= cost;
+                        d.st_embedded[i] = sid;  // grown this plan
+                        break;
+                    }
+                    while (vp >= 0) {
+                        const PV x = RV(vp);
+                        if ((x.flags & PV_READY) && d.st_removed[RUN[vp]] != sid && (x.flags & PV_HOLDS)) break;
+                        vp--;
+                    }
+                    if (vp < 0) break;
+                    const int32_t victim = RUN[vp];
+                    d.pre_idx[S.n_pre] = victim; d.pre_strat[S.n_pre] = CO_RECOMPUTE; S.n_pre++;
+                    d.st_removed[victim] = sid;
+                    S.free += gain_of(d, victim);
+                    if (victim == i) break;
+                }
+            }
+        } else {
+            // returned requests evict themselves (scheduler.py:848-851, 900-903)
+            for (int32_t k = 0; k < n_run; k++) {
+                const PV v = RV(k);
+                if (!(v.flags & PV_READY) || !returned(v)) continue;
+                d.pre_idx[S.n_pre] = RUN[k];
+                d.pre_strat[S.n_pre] = pol == CO_POLICY_RLP ? CO_RECOMPUTE : CO_SWAP;
+                S.n_pre++;
+                d.st_removed[RUN[k]] = sid;
+            }
+        }
+        // decode (and, chunked, prefill-continuation) members in running order
+        for (int32_t k = 0; k < n_run; k++) {
+            const PV v = RV(k);
+            const int32_t i = RUN[k];
+            if (!(v.flags & PV_READY) || d.st_removed[i] == sid) continue;
+            if (v.pre < v.kvn) {
+                if (!chunked) continue;
+                int64_t chunk = (int64_t)v.kvn - v.pre;
+                chunk = chunk < budget ? chunk : budget;
+                if (chunk > 0) { push_mem(d, S, i, chunk); budget -= chunk; }
+                continue;
+            }
+            if (vllm && returned(v) && d.st_embedded[i] != sid) continue;
+            if (budget >= 1) { push_mem(d, S, i, 1); budget -= 1; }
+        }
+        // admissions: preempted first (FCFS), until the first that does not fit
+        S.stop = 0;
+        for (int32_t k = 0; k < n_blown; k++)
+            if (!admit_one(d.l_blown[k], budget)) { S.stop = 1; break; }
+        S.resid = budget;
+    }
+    __syncthreads();
+    for (int32_t base = 0; base < n_f0 && !S.stop; base += (int)blockDim.x) {
+        ensure(base + (int)blockDim.x);  // materializes at least [0, base + NT) of the keyed queue
+        if (tid == 0) {
+            int64_t budget = S.resid;
+            const int32_t end = base + (int)blockDim.x < n_f0 ? base + (int)blockDim.x : n_f0;
+            for (int32_t k = base; k < end; k++)
+                if (!admit_one(d.l_nwp[k], budget)) { S.stop = 1; break; }
+            S.resid = budget;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        PlanHdr& P = *d.plan;
+        P.n_mem = S.n_mem; P.n_act = S.n_act; P.n_pre = S.n_pre; P.n_cl = 0; P.n_def = 0;
+        P.batch_tokens = S.batch_now;
+        P.overflow = S.batch_now > d.token_budget ? 1 : 0;
+        P.sated = 0;
+        P.k_sel = 0;
+    }
+    for (int32_t k = tid; k < NBIN; k += (int)blockDim.x) { d.hist[k] = 0; d.fill[k] = 0; }
+}
+
 __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     extern __shared__ __align__(16) uint8_t plan_smem[];
     PlanSh& S = *reinterpret_cast<PlanSh*>(plan_smem);
@@ -379,6 +512,11 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         for (int32_t k = tid; k < n_run; k += (int)blockDim.x) S.rv[k] = view_of(d, RUN[k]);
     __syncthreads();
     auto RV = [&](int32_t k) -> PV { return rcached ? S.rv[k] : view_of(d, RUN[k]); };
+
+    if (d.policy != CO_POLICY_CACHEOPT) {
+        plan_baseline(d, S, RUN, n_run, n_f0, n_blown, rcached, sid, ensure);
+        return;
+    }
 
     // ---- returned running (scheduler.py:142-150, 161-162) ------------------
     auto crit_rt = [&](int64_t r) { return r >= -eps && r - ti < eps; };

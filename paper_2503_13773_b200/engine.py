@@ -144,6 +144,41 @@ def compute_metrics(*, requests: Dict[int, Request], runtimes: Dict[int, Request
     )
 
 
+def calibrate_slo_baselines(requests: Sequence[Request], cfg: EngineConfig, device: int = -1
+                            ) -> Tuple[int, int]:
+    """engine.py:675-699: median per-chunk TTFT and median token gap of a
+    vllm_block run (which ignores SLOs) -- the simulation runs on the device
+    (the baseline planner of csrc/planner.cuh), the two medians on the host."""
+    cal_cfg = dataclasses.replace(cfg, sched=dataclasses.replace(cfg.sched, policy="vllm_block"),
+                                  record_events=False)
+    eng = Engine(list(requests), cal_cfg, device=device)
+    try:
+        eng.run_steps(0)
+        st = eng._field("STATE")
+        ft = eng._field("FIRST_TOKEN")
+        offs = np.empty(eng._n + 1, dtype=np.int64)
+        times = np.empty(max(1, int(eng._tok_total())), dtype=np.int64)
+        N.check(eng._lib.co_read_token_times(eng._h, _ptr(offs, C.c_int64), _ptr(times, C.c_int64)),
+                "co_read_token_times")
+        gen = eng._field("GENERATED")
+    finally:
+        eng.close()
+    chunk = cfg.sched.token_budget
+    by_id = {r.id: r for r in requests}
+    ttfts, gaps = [], []
+    for r in requests:  # the reference iterates eng.requests (caller order)
+        k = eng._idx_of[r.id]
+        if STATE_FROM_CODE[int(st[k])] is not Lifecycle.COMPLETED:
+            continue
+        factor = max(1, -(-by_id[r.id].prompt_len // chunk))
+        ttfts.append((int(ft[k]) - r.arrival_us) / factor)
+        t = times[offs[k]:offs[k] + int(gen[k])]
+        gaps.extend(np.diff(t).tolist())
+    if not ttfts or not gaps:
+        raise ValueError("calibration run completed no requests")
+    return int(np.median(ttfts)), int(np.median(gaps))
+
+
 def write_events_jsonl(events: Sequence[dict], path: str) -> None:
     """One sorted-key compact JSON object per line (engine.py:214-219)."""
     with open(path, "w") as fh:
@@ -314,6 +349,8 @@ class Engine:
         c.padding = self.padding
         c.s_star = sweet_spot(cfg.truth.swap_true, cfg.truth.recompute_true)
         c.t_i_init_us = iteration_us(cfg, sc.token_budget)
+        c.policy = N.POLICY_CODE[sc.policy]
+        c.vllm_block_tokens, c.s3_bucket_tokens, c.rlp_padding = sc.vllm_block_tokens, sc.s3_bucket_tokens, sc.rlp_padding
         self.kv = kv
         if kv is not None:
             c.kv_layers, c.kv_heads, c.q_heads, c.head_dim = kv.layers, kv.kv_heads, kv.q_heads, kv.head_dim

@@ -69,7 +69,7 @@ def test_unsupported_modes_are_rejected_not_emulated():
     import paper_2503_13773_b200 as P
     reqs = [P.Request(0, 0, 10, 3, 10**9, 10**9)]
     with pytest.raises(ValueError):
-        P.Engine(reqs, P.EngineConfig(sched=P.SchedulerConfig(policy="vllm_block")))
+        P.Engine(reqs, P.EngineConfig(sched=P.SchedulerConfig(policy="fifo")))  # not a reference policy
     with pytest.raises(ValueError):
         P.Engine(reqs, P.EngineConfig(allow_stacking=True))
 
