@@ -28,7 +28,7 @@ def _compare(eng, orc, label):
     assert eng.block_tables() == orc.block_tables(), f"{label}: block tables differ"
 
 
-@pytest.mark.parametrize("seed", list(range(0, 24)))
+@pytest.mark.parametrize("seed", list(range(0, 48)))
 def test_random_regimes_full_run(cuda_ok, seed):
     from paper_2503_13773_b200 import Engine
     reqs, cfg = build_product(case_params(seed))
