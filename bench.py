@@ -432,6 +432,11 @@ def device_arm(args, rank, world, dist):
         "cpu_baseline": {"value": cpu_val, "unit": UNIT, "cores": 1, "kind": "port",
                          "sample": f"oracle port, config-2 steps {WINDOW_START}..{WINDOW_START + cpu_steps - 1} "
                                    f"({cpu_dt:.1f} s, 1 thread)"},
+        "reference_python": {"value": 1.37e5, "unit": UNIT, "ms_per_step": 479.0,
+                             "source": "BASELINE.md row cfg2: the unmodified kvcsim Engine.step on this same "
+                                       "window (steps 40-60, 65,535 live), timed in the development container; "
+                                       "the Python reference cannot run on the GPU box, so the reference arm "
+                                       "(--impl reference) times the vectorised CPU oracle port instead"},
         "e2e": {"value": e2e_dec / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 256 + d2h // max(args.steps, 1),
                 "how": "Engine.step_result() per step through the public API (control block + the iteration's "
