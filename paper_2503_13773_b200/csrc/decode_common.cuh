@@ -3,6 +3,7 @@
 // partial results k_decode_reduce combines.
 #pragma once
 #include <cuda.h>
+#include <cstdio>
 #include "data_plane.cuh"
 
 namespace co {
@@ -18,6 +19,9 @@ __device__ __forceinline__ void mbar_expect(uint32_t bar, uint32_t bytes) {
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     uint32_t done = 0;
+#ifdef CO_MBAR_WATCHDOG  // development aid: report a stuck wait, then trap
+    long long spins = 0;
+#endif
     while (!done) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
@@ -26,6 +30,12 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
             : "=r"(done)
             : "r"(bar), "r"(phase)
             : "memory");
+#ifdef CO_MBAR_WATCHDOG
+        if (++spins == (1ll << 22))
+            printf("mbar watchdog: block %d thread %d bar smem+0x%x parity %u\n", blockIdx.x, threadIdx.x, bar & 0x3ffff,
+                   phase);
+        if (spins == (1ll << 24)) __trap();
+#endif
     }
 }
 __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1, uint32_t bar) {
