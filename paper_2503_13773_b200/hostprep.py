@@ -16,7 +16,7 @@ round-to-nearest double intrinsics.
 from __future__ import annotations
 
 import math
-from typing import Sequence, Tuple
+from typing import Tuple
 
 import numpy as np
 

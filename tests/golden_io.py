@@ -7,7 +7,6 @@ import gzip
 import hashlib
 import json
 import os
-from types import SimpleNamespace
 
 import numpy as np
 

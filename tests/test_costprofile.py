@@ -6,7 +6,6 @@ run that stays bit-identical to the CPU oracle."""
 import json
 import os
 
-import numpy as np
 import pytest
 
 from paper_2503_13773_b200 import costprofile as cp

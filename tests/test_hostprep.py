@@ -4,7 +4,6 @@ import math
 import random
 from fractions import Fraction
 
-import pytest
 
 import paper_2503_13773_b200 as P
 from oracle.cacheopt_oracle import split_largest_remainder
