@@ -14,7 +14,7 @@ namespace co {
 constexpr int NT = 256;   // threads of the single-CTA planner / apply kernels (max; 256 measured best)
 constexpr int TCHUNK = 64;  // pages per block-table chunk
 constexpr int NBIN = 4096;  // N'_w deadline buckets
-constexpr int GRP = 256;    // N'_w materialization group (items)
+constexpr int GRP = 64;     // N'_w materialization group (items)
 constexpr int ST_PENDING = CO_PENDING, ST_WAITING = CO_WAITING, ST_RUNNING = CO_RUNNING,
               ST_PREEMPTED = CO_PREEMPTED, ST_COMPLETED = CO_COMPLETED;
 

@@ -36,7 +36,7 @@ struct PlanSh {
     int32_t blkoff[2][1288];     // prefix of the classify blocks' running / blown counts
     int32_t mat, any_feasible;
     unsigned __int128 wsum;
-    int64_t free, shortfall, runway, batch_now, gm_tokens;
+    int64_t free, shortfall, runway, batch_now, gm_tokens, probe_tok;
     int64_t f_total, a_total, f_supply, a_supply, tbt_floor, lim, resid;
     int32_t rsvb, n_mem, n_act, n_pre, n_cl, n_def, n_gm, n_pend, n_mready, n_part;
     int32_t k_sel, search, cur, pos, stop, sated, overflow, g_nlive, g_left;
@@ -755,7 +755,32 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         const int64_t budget = d.token_budget;
         int64_t used_base = consumed;
         int32_t ksel = n_nwp;
-        for (int32_t base = 0; base < n_nwp; base += (int)blockDim.x) {
+        // warp probe of the queue head first: the budget usually fills within
+        // a few prompts, so only the first (small) group is materialized
+        int32_t base0 = 0;
+        if (n_nwp > 0) {
+            ensure(32);
+            if (tid < 32) {
+                const int32_t k = tid;
+                int64_t ch = 0;
+                if (k < n_nwp) { const PV v = view_of(d, NWP[k]); ch = v.kvn - v.pre; }
+                int64_t inc = ch;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (tid >= o) inc += y;
+                }
+                const unsigned over = __ballot_sync(0xffffffffu, k < n_nwp && used_base + inc > budget);
+                const int64_t tot = __shfl_sync(0xffffffffu, inc, 31);
+                if (tid == 0) { S.k_sel = over ? __ffs(over) - 1 : -1; S.probe_tok = tot; }
+            }
+            __syncthreads();
+            if (S.k_sel >= 0) ksel = S.k_sel;
+            used_base += S.probe_tok;
+            base0 = S.k_sel >= 0 ? n_nwp : 32;
+            __syncthreads();
+        }
+        for (int32_t base = base0; base < n_nwp; base += (int)blockDim.x) {
             ensure(base + (int)blockDim.x);
             int32_t k = base + tid;
             int32_t ch = 0;
