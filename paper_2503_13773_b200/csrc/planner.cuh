@@ -124,9 +124,59 @@ __device__ __forceinline__ int32_t& part_grant(const Dev& d, PlanSh& S, int32_t 
     return p < PV_CAP ? S.pgrant[p] : d.l_part_grant[p];
 }
 
+// The exact share computation of a warp of demands with a 128-bit weight sum
+// (some weight >= 2^57; never on realistic traces).
+__device__ __forceinline__ int64_t amortize_lane_wide(const Dev& d, const PV& v, bool live, int64_t supply,
+                                                   int64_t tot) {
+    const uint64_t w = live ? amort_weight(v) : 0;
+    uint64_t lo = w, hi = 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        uint64_t lo2 = __shfl_xor_sync(0xffffffffu, lo, o), hi2 = __shfl_xor_sync(0xffffffffu, hi, o);
+        uint64_t nl = lo + lo2;
+        hi = hi + hi2 + (nl < lo ? 1 : 0);
+        lo = nl;
+    }
+    const unsigned __int128 W = ((unsigned __int128)hi << 64) | lo;
+    uint64_t q = 0;
+    unsigned __int128 r = 0;
+    if (live) divmod_small_q((unsigned __int128)(uint64_t)supply * w, W, q, r);
+    int64_t g = (int64_t)q;
+    const int64_t left = supply - warp_sum64(g);
+    const uint64_t rhi = (uint64_t)(r >> 64), rlo = (uint64_t)r;
+    const uint32_t id = live ? (uint32_t)v.idrank : 0xffffffffu;
+    int32_t rank = 0;
+    for (int j = 0; j < 32; j++) {
+        const uint64_t jhi = __shfl_sync(0xffffffffu, rhi, j), jlo = __shfl_sync(0xffffffffu, rlo, j);
+        const uint32_t jid = __shfl_sync(0xffffffffu, id, j);
+        const bool jlive = __shfl_sync(0xffffffffu, live ? 1 : 0, j);
+        const bool before = jhi > rhi || (jhi == rhi && (jlo > rlo || (jlo == rlo && jid < id)));
+        rank += (jlive && before) ? 1 : 0;
+    }
+    if (live && rank < left) g += 1;
+    if (tot > supply) {
+        const int bs = d.bs;
+        const int64_t fl = (g / bs) * bs;
+        const int64_t left_blocks = (supply - warp_sum64(live ? fl : 0)) / bs;
+        const uint64_t rem = (uint64_t)(g - fl);
+        int32_t rk = 0;
+        for (int j = 0; j < 32; j++) {
+            const uint64_t jr = __shfl_sync(0xffffffffu, rem, j);
+            const uint32_t jid = __shfl_sync(0xffffffffu, id, j);
+            const bool jlive = __shfl_sync(0xffffffffu, live ? 1 : 0, j);
+            rk += (jlive && (jr > rem || (jr == rem && jid < id))) ? 1 : 0;
+        }
+        g = fl + ((live && rk < left_blocks) ? bs : 0);
+    }
+    return live ? g : 0;
+}
+
 // amortize() for groups of at most 32 demands, entirely in warp 0 (lane =
 // demand): same exact integer arithmetic, ranks by pairwise shuffles, one
-// block barrier at the end.
+// block barrier at the end.  With every weight below 2^57 the weight sum W
+// fits 62 bits, so q = floor(supply w / W) (< supply < 2^31) comes from a
+// double estimate corrected by exact 64-bit wrap-around remainders (the true
+// remainder lies in (-2W, 2W)): no 128-bit arithmetic, no 64-bit division.
 __device__ void amortize_warp(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64_t supply, int64_t now,
                               int64_t* total_out) {
     const int lane = threadIdx.x & 31;
@@ -144,48 +194,59 @@ __device__ void amortize_warp(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, 
             } else {
                 const PV v = live ? part_pv(d, S, p, now) : PV{};
                 const uint64_t w = live ? amort_weight(v) : 0;
-                // W = sum w (u128)
-                uint64_t lo = w, hi = 0;
+                if (__any_sync(0xffffffffu, w >= (1ull << 57))) {
+                    g = amortize_lane_wide(d, v, live, supply, tot);
+                } else {
+                    uint64_t W = w;
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    uint64_t lo2 = __shfl_xor_sync(0xffffffffu, lo, o), hi2 = __shfl_xor_sync(0xffffffffu, hi, o);
-                    uint64_t nl = lo + lo2;
-                    hi = hi + hi2 + (nl < lo ? 1 : 0);
-                    lo = nl;
-                }
-                const unsigned __int128 W = ((unsigned __int128)hi << 64) | lo;
-                uint64_t q = 0;
-                unsigned __int128 r = 0;
-                if (live) divmod_small_q((unsigned __int128)(uint64_t)supply * w, W, q, r);
-                g = (int64_t)q;
-                const int64_t left = supply - warp_sum64(g);
-                const uint64_t rhi = (uint64_t)(r >> 64), rlo = (uint64_t)r;
-                const uint32_t id = live ? (uint32_t)v.idrank : 0xffffffffu;
-                // rank by (-r, id) among live lanes
-                int32_t rank = 0;
-                for (int j = 0; j < 32; j++) {
-                    const uint64_t jhi = __shfl_sync(0xffffffffu, rhi, j), jlo = __shfl_sync(0xffffffffu, rlo, j);
-                    const uint32_t jid = __shfl_sync(0xffffffffu, id, j);
-                    const bool jlive = __shfl_sync(0xffffffffu, live ? 1 : 0, j);
-                    const bool before = jhi > rhi || (jhi == rhi && (jlo > rlo || (jlo == rlo && jid < id)));
-                    rank += (jlive && before) ? 1 : 0;
-                }
-                if (live && rank < left) g += 1;
-                if (tot > supply) {
-                    const int bs = d.bs;
-                    const int64_t fl = (g / bs) * bs;
-                    const int64_t left_blocks = (supply - warp_sum64(live ? fl : 0)) / bs;
-                    const uint64_t rem = (uint64_t)(g - fl);
-                    int32_t rk = 0;
+                    for (int o = 16; o > 0; o >>= 1) W += __shfl_xor_sync(0xffffffffu, W, o);
+                    int64_t q = 0;
+                    uint64_t r = 0;
+                    if (live) {
+                        int64_t qe = (int64_t)((double)supply * (double)w / (double)W);
+                        int64_t rr = (int64_t)((uint64_t)supply * w - (uint64_t)qe * W);
+                        while (rr < 0) { qe--; rr += (int64_t)W; }
+                        while (rr >= (int64_t)W) { qe++; rr -= (int64_t)W; }
+                        q = qe;
+                        r = (uint64_t)rr;
+                    }
+                    const int32_t sup = (int32_t)supply;
+                    int32_t gi = (int32_t)q;
+                    int32_t sq = gi;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+                    const int32_t left = sup - sq;
+                    const uint32_t id = live ? (uint32_t)v.idrank : 0xffffffffu;
+                    // largest remainder first, ties by id (scheduler.py:240-242)
+                    int32_t rank = 0;
+#pragma unroll 4
                     for (int j = 0; j < 32; j++) {
-                        const uint64_t jr = __shfl_sync(0xffffffffu, rem, j);
+                        const uint64_t jr = __shfl_sync(0xffffffffu, r, j);
                         const uint32_t jid = __shfl_sync(0xffffffffu, id, j);
                         const bool jlive = __shfl_sync(0xffffffffu, live ? 1 : 0, j);
-                        rk += (jlive && (jr > rem || (jr == rem && jid < id))) ? 1 : 0;
+                        rank += (jlive && (jr > r || (jr == r && jid < id))) ? 1 : 0;
                     }
-                    g = fl + ((live && rk < left_blocks) ? bs : 0);
+                    if (live && rank < left) gi += 1;
+                    if (tot > supply) {  // block flooring, leftover blocks by remainder (scheduler.py:653-659)
+                        const int32_t bs = d.bs;
+                        const int32_t fl = (gi / bs) * bs;
+                        int32_t sfl = live ? fl : 0;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) sfl += __shfl_xor_sync(0xffffffffu, sfl, o);
+                        const int32_t left_blocks = (sup - sfl) / bs;
+                        const int32_t rem = gi - fl;
+                        int32_t rk = 0;
+#pragma unroll 4
+                        for (int j = 0; j < 32; j++) {
+                            const int32_t jr = __shfl_sync(0xffffffffu, rem, j);
+                            const uint32_t jid = __shfl_sync(0xffffffffu, id, j);
+                            const bool jlive = __shfl_sync(0xffffffffu, live ? 1 : 0, j);
+                            rk += (jlive && (jr > rem || (jr == rem && jid < id))) ? 1 : 0;
+                        }
+                        gi = fl + ((live && rk < left_blocks) ? bs : 0);
+                    }
+                    g = live ? gi : 0;
                 }
-                if (!live) g = 0;
             }
         }
         if (in) part_grant(d, S, p) = (int32_t)g;
