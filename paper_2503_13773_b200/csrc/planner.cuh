@@ -532,14 +532,15 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     __syncthreads();
     blk_scan_smem(S.blkoff[0], d.nblk + 1, S.b);
     blk_scan_smem(S.blkoff[1], d.nblk + 1, S.b);
-    {
-        const int nw = (int)(blockDim.x >> 5), lane = tid & 31;
-        for (int32_t b = tid >> 5; b < d.nblk; b += nw) {
-            const int32_t r0 = S.blkoff[0][b], nr = S.blkoff[0][b + 1] - r0;
-            const int32_t b0 = S.blkoff[1][b], nb = S.blkoff[1][b + 1] - b0, src = b * d.chunk;
-            for (int32_t k = lane; k < nr; k += 32) d.l_run[r0 + k] = d.run_tmp[src + k];
-            for (int32_t k = lane; k < nb; k += 32) d.l_blown[b0 + k] = d.blown_tmp[src + k];
-        }
+    // one thread per classify block: the lists are short per block, so all
+    // blocks' copies are in flight at once
+    for (int32_t b = tid; b < d.nblk; b += (int)blockDim.x) {
+        const int32_t r0 = S.blkoff[0][b], nr = S.blkoff[0][b + 1] - r0;
+        const int32_t b0 = S.blkoff[1][b], nb = S.blkoff[1][b + 1] - b0, src = b * d.chunk;
+#pragma unroll 4
+        for (int32_t k = 0; k < nr; k++) d.l_run[r0 + k] = d.run_tmp[src + k];
+#pragma unroll 4
+        for (int32_t k = 0; k < nb; k++) d.l_blown[b0 + k] = d.blown_tmp[src + k];
     }
     __syncthreads();
     // N_w by (rt, id) (scheduler.py:159); D = rt + now, unique with the id rank
