@@ -116,25 +116,35 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
     for (int32_t m = tid; m < nm; m += (int)blockDim.x) {
         const int32_t i = d.mem_idx[m];
         const int32_t tok = d.mem_tok[m];
+        // every field the decision reads, loaded up front: one round trip
+        // instead of one per branch (the guest's offset is the only dependent load)
+        const int32_t failed = d.st_failed[i];
+        const uint64_t seen = d.seen64[i];
+        const int8_t st = d.state[i];
+        const uint8_t holds = d.holds[i];
+        const int32_t granted = d.granted[i], prefill = d.prefill[i], kvn = d.kv_need[i], used = d.used[i];
+        const int32_t gu = d.guest[i];
+        const int64_t ready = d.ready_at[i], fstart = d.first_start[i];
         int32_t f = 0;  // bit0 survive, bit1 admit event
-        if (d.st_failed[i] != sid && d.seen64[i] == (stamp | (0xFFFFFFu - (uint32_t)m))) {
-            const int8_t st = d.state[i];
+        if (failed != sid && seen == (stamp | (0xFFFFFFu - (uint32_t)m))) {
             bool go = live_state(st);
             if (go && st == ST_WAITING) {
-                if (!d.holds[i] || d.granted[i] < d.prefill[i] + tok) {
+                if (!holds || granted < prefill + tok) {
                     go = false;
                 } else {
                     f |= 4;  // becomes RUNNING
-                    if (d.first_start[i] < 0) f |= 2;
+                    if (fstart < 0) f |= 2;
                 }
             } else if (go && st != ST_RUNNING) {
                 go = false;
             }
-            if (go && d.ready_at[i] > now) go = false;
+            if (go && ready > now) go = false;
             if (go) {
-                if (d.prefill[i] >= d.kv_need[i]) {
-                    if (eff_of(d, i) < d.used[i] + 1) go = false;
-                } else if (d.granted[i] < d.prefill[i] + tok) {
+                if (prefill >= kvn) {
+                    int32_t eff = holds ? granted : 0;  // eff_of (engine.py:275-282)
+                    if (holds && gu >= 0) { const int32_t o = d.off[gu]; eff = o < granted ? o : granted; }
+                    if (eff < used + 1) go = false;
+                } else if (granted < prefill + tok) {
                     go = false;
                 }
             }
@@ -271,35 +281,39 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
     for (int32_t k = tid; k < ns; k += (int)blockDim.x) {
         const int32_t i = d.l_surv_idx[k];
         const int32_t tok = d.l_surv_tok[k];
+        // the member's fields up front (members are distinct: no other thread writes them)
+        const int32_t prefill = d.prefill[i], kvn = d.kv_need[i], used = d.used[i], gen = d.gen[i];
+        const int32_t granted = d.granted[i];
+        const int64_t ftok = d.first_tok[i], ltok = d.last_tok[i], mtbt = d.max_tbt[i], toff = d.tok_off[i];
         bool token = false;
         int32_t nu;
-        if (d.prefill[i] < d.kv_need[i]) {
-            d.l_fill_t0[k] = d.prefill[i];  // N2: the chunk's KV is written this iteration
+        if (prefill < kvn) {
+            d.l_fill_t0[k] = prefill;  // N2: the chunk's KV is written this iteration
             d.l_fill_n[k] = tok;
-            d.prefill[i] += tok;
-            nu = d.prefill[i];
-            token = d.prefill[i] >= d.kv_need[i] && d.gen[i] == 0;
+            nu = prefill + tok;
+            d.prefill[i] = nu;
+            token = nu >= kvn && gen == 0;
         } else {
-            d.l_fill_t0[k] = d.used[i];     // decode writes the KV of position used
-            d.l_fill_n[k] = -1;             // (negative: decode member)
-            nu = d.used[i] + 1;
+            d.l_fill_t0[k] = used;     // decode writes the KV of position used
+            d.l_fill_n[k] = -1;        // (negative: decode member)
+            nu = used + 1;
             token = true;
         }
-        if (nu < 0 || nu > d.granted[i]) { c.error = 2; c.err_info[0] = i; c.err_info[1] = nu; }
-        dused += (int64_t)nu - d.used[i];
+        if (nu < 0 || nu > granted) { c.error = 2; c.err_info[0] = i; c.err_info[1] = nu; }
+        dused += (int64_t)nu - used;
         d.used[i] = nu;
         if (token) {
-            int32_t g = d.gen[i] + 1;
+            const int32_t g = gen + 1;
             d.gen[i] = g;
             dgen += 1;
-            if (d.first_tok[i] < 0) {
+            if (ftok < 0) {
                 d.first_tok[i] = end;
             } else {
-                int64_t gap = end - d.last_tok[i];
-                if (gap > d.max_tbt[i]) d.max_tbt[i] = gap;
+                const int64_t gap = end - ltok;
+                if (gap > mtbt) d.max_tbt[i] = gap;
             }
             d.last_tok[i] = end;
-            d.tok_times[d.tok_off[i] + g - 1] = end;
+            d.tok_times[toff + g - 1] = end;
         }
     }
     dused = blk_sum(dused, S.b);
