@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
     for (int32_t m = tid; m < nm; m += (int)blockDim.x) atomicMax((unsigned long long*)&d.seen64[d.mem_idx[m]],
                                                       (unsigned long long)(stamp | (0xFFFFFFu - (uint32_t)m)));
     __syncthreads();
+    int32_t my_i = -1, my_tok = 0, my_f = 0;  // this thread's member when nm <= blockDim.x
     for (int32_t m = tid; m < nm; m += (int)blockDim.x) {
         const int32_t i = d.mem_idx[m];
         const int32_t tok = d.mem_tok[m];
@@ -151,7 +152,33 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
             if (go) f |= 1;
         }
         d.l_mflag[m] = f;
+        if (m == tid) { my_i = i; my_tok = tok; my_f = f; }
     }
+    int32_t n_admit = 0, ns0 = 0;
+    int64_t bsum = 0;
+    if (nm <= (int)blockDim.x) {
+        // one member per thread, decisions in registers: the state changes,
+        // then ONE scan placing admit events (high half) and survivors (low
+        // half) in member order
+        if (my_f & 4) {
+            d.state[my_i] = ST_RUNNING;
+            if (my_f & 2) d.first_start[my_i] = now;
+        }
+        const int32_t packed = ((my_f & 2) ? (1 << 16) : 0) | (my_f & 1);
+        int32_t tot;
+        const int32_t ex = blk_excl_scan(packed, &tot, S.b);
+        if (d.record_events) {
+            if (my_f & 2) {
+                co_event e;
+                e.kind = CO_EV_ADMIT; e.idx = my_i; e.t = now; e.a = e.b = e.c = 0;
+                d.events[c.ev_count + (ex >> 16)] = e;
+            }
+            n_admit = tot >> 16;
+        }
+        if (my_f & 1) { d.l_surv_idx[ex & 0xffff] = my_i; d.l_surv_tok[ex & 0xffff] = my_tok; }
+        ns0 = tot & 0xffff;
+        bsum = blk_sum((my_f & 1) ? my_tok : 0, S.b);  // (its barriers publish the survivor lists)
+    } else {
     __syncthreads();
     for (int32_t m = tid; m < nm; m += (int)blockDim.x) {
         const int32_t f = d.l_mflag[m];
@@ -161,7 +188,6 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
             if (f & 2) d.first_start[i] = now;
         }
     }
-    int32_t n_admit = 0;
     if (d.record_events) {
         const int64_t ev_base = c.ev_count;
         int32_t base = 0;
@@ -180,8 +206,7 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
         n_admit = base;
     }
     // survivors in member order: positions first, then (idx, tokens)
-    const int32_t ns0 = blk_compact(nullptr, nm, d.l_surv_tok, [&](int32_t m) { return (d.l_mflag[m] & 1) != 0; }, S.b);
-    int64_t bsum = 0;
+    ns0 = blk_compact(nullptr, nm, d.l_surv_tok, [&](int32_t m) { return (d.l_mflag[m] & 1) != 0; }, S.b);
     for (int32_t k = tid; k < ns0; k += (int)blockDim.x) bsum += d.mem_tok[d.l_surv_tok[k]];
     bsum = blk_sum(bsum, S.b);
     for (int32_t k = tid; k < ns0; k += (int)blockDim.x) {
@@ -190,6 +215,7 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
     }
     __syncthreads();
     for (int32_t k = tid; k < ns0; k += (int)blockDim.x) d.l_surv_tok[k] = d.mem_tok[d.l_surv_tok[k]];  // position -> tokens
+    }
     __syncthreads();
     if (tid == 0) {
         const int32_t ns = ns0;
