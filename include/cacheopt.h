@@ -295,6 +295,58 @@ typedef struct co_metrics_raw {
 } co_metrics_raw;
 int co_metrics(co_engine* eng, co_metrics_raw* out);
 
+/* ---- the run's random streams on the device --------------
+ * Bit-exact device versions of the reference's numpy draws (default_rng
+ * ([seed, k]) = SeedSequence + PCG64, numpy's ziggurat exponential / normal,
+ * uniform, Lemire bounded integers).  Output pointers are DEVICE pointers on
+ * `device` (< 0: current device); every call is synchronous. */
+
+/* default_rng(entropy) -> PCG64 (state_hi, state_lo, inc_hi, inc_lo) */
+int co_pcg64_seed(const uint64_t* entropy, int32_t n_entropy, uint64_t out[4]);
+/* the first `count` raw 64-bit outputs of default_rng([seed, stream]) */
+int co_gen_raw(uint64_t seed, uint64_t stream, int64_t count, int device, uint64_t* out);
+/* n draws of default_rng([seed, stream]).standard_exponential (kind 0) or
+ * .standard_normal (kind 1) */
+int co_gen_std(int32_t kind, uint64_t seed, uint64_t stream, int64_t n, int device, double* out);
+
+/* workload.py:85-109 generate(spec, seed): arrivals from exponential gaps of
+ * default_rng([seed, 0]), prompt / output lengths from the lognormals of
+ * default_rng([seed, 1]) / ([seed, 2]), clipped.  mu / sigma are the host's
+ * _lognormal_params (workload.py:79-82); gap_scale = 1.0 / arrival_rate. */
+typedef struct co_trace_spec {
+    int64_t n;
+    double gap_scale;
+    double mu_in, sigma_in;
+    double mu_out, sigma_out;
+    int32_t input_min, input_max;
+    int32_t output_min, output_max;
+} co_trace_spec;
+int co_gen_trace(const co_trace_spec* spec, uint64_t seed, int device, int64_t* arrival_us, int32_t* prompt_len,
+                 int32_t* output_len);
+
+/* workload.py:181-194 assign_slos(requests, base_ttft, base_tbt, policy, seed) */
+typedef struct co_slo_spec {
+    int64_t base_ttft_us, base_tbt_us;
+    double scale_lo, scale_hi;
+    int32_t chunk_budget;
+    int32_t _pad;
+} co_slo_spec;
+int co_gen_slos(int64_t n, const int32_t* prompt_len /* device */, const co_slo_spec* spec, uint64_t seed,
+                int device, int64_t* slo_ttft_us, int64_t* slo_tbt_us);
+
+/* estimation.py:76-99 predictor draws for n arrivals in admission order from
+ * default_rng([seed, 3]) (engine.py:267): err = _sample_error, flip = the
+ * direction-flip test (1 - direction_accuracy). */
+enum { CO_ERR_ZERO = 0, CO_ERR_UNIFORM = 1, CO_ERR_NORMAL = 2 };
+typedef struct co_predictor_spec {
+    int32_t error_dist;
+    int32_t _pad;
+    double error_scale;
+    double direction_accuracy;
+} co_predictor_spec;
+int co_gen_predictor(int64_t n, const co_predictor_spec* spec, uint64_t seed, int device, int32_t* err_draw,
+                     uint8_t* flip_draw);
+
 const char* co_last_error(void);
 const char* co_version(void);
 

@@ -86,7 +86,8 @@ EXPORTS = (
     "co_check_invariants", "co_last_device_ms", "co_kernels_per_step", "co_time_steps", "co_last_error",
     "co_version", "co_read_block_tables", "co_data_stats", "co_kv_verify", "co_read_decode", "co_host_link_gbs",
     "co_set_decode", "co_swap_bench", "co_nccl_unique_id", "co_attach_nccl", "co_global_reserve",
-    "co_phase_profile", "co_step_result", "co_metrics",
+    "co_phase_profile", "co_step_result", "co_metrics", "co_pcg64_seed", "co_gen_raw", "co_gen_std",
+    "co_gen_trace", "co_gen_slos", "co_gen_predictor",
 )
 
 _lib = None
@@ -97,6 +98,25 @@ class CoMetricsRaw(C.Structure):
                                          "preempted", "sum_ttft", "sum_gap", "sum_wait", "sum_exec", "sum_pdec",
                                          "sum_ptime")] + [
         ("count", C.c_int64 * 4), ("norm_sum", C.c_double), ("order_stat", (C.c_double * 7) * 4)]
+
+
+class CoTraceSpec(C.Structure):
+    _fields_ = [("n", C.c_int64), ("gap_scale", C.c_double), ("mu_in", C.c_double), ("sigma_in", C.c_double),
+                ("mu_out", C.c_double), ("sigma_out", C.c_double), ("input_min", C.c_int32),
+                ("input_max", C.c_int32), ("output_min", C.c_int32), ("output_max", C.c_int32)]
+
+
+class CoSloSpec(C.Structure):
+    _fields_ = [("base_ttft_us", C.c_int64), ("base_tbt_us", C.c_int64), ("scale_lo", C.c_double),
+                ("scale_hi", C.c_double), ("chunk_budget", C.c_int32), ("_pad", C.c_int32)]
+
+
+class CoPredictorSpec(C.Structure):
+    _fields_ = [("error_dist", C.c_int32), ("_pad", C.c_int32), ("error_scale", C.c_double),
+                ("direction_accuracy", C.c_double)]
+
+
+ERR_DIST = {"zero": 0, "uniform": 1, "normal": 2}
 
 
 class NativeError(RuntimeError):
@@ -142,6 +162,12 @@ def load() -> C.CDLL:
         "co_phase_profile": (C.c_int, [V, C.c_int32, I64P]),
         "co_step_result": (C.c_int, [V, I32P, I32P, C.c_int64, I64P, I64P]),
         "co_metrics": (C.c_int, [V, C.POINTER(CoMetricsRaw)]),
+        "co_pcg64_seed": (C.c_int, [C.POINTER(C.c_uint64), C.c_int32, C.POINTER(C.c_uint64)]),
+        "co_gen_raw": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int64, C.c_int, V]),
+        "co_gen_std": (C.c_int, [C.c_int32, C.c_uint64, C.c_uint64, C.c_int64, C.c_int, V]),
+        "co_gen_trace": (C.c_int, [C.POINTER(CoTraceSpec), C.c_uint64, C.c_int, V, V, V]),
+        "co_gen_slos": (C.c_int, [C.c_int64, V, C.POINTER(CoSloSpec), C.c_uint64, C.c_int, V, V]),
+        "co_gen_predictor": (C.c_int, [C.c_int64, C.POINTER(CoPredictorSpec), C.c_uint64, C.c_int, V, V]),
         "co_last_error": (C.c_char_p, []),
         "co_version": (C.c_char_p, []),
     }

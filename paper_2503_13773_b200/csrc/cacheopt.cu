@@ -32,6 +32,7 @@
 #include "data_plane.cuh"
 #include "decode_tc05.cuh"
 #include "metrics.cuh"
+#include "trace_gen.cuh"
 #include <cudaTypedefs.h>
 
 using namespace co;
@@ -1240,6 +1241,228 @@ int co_kernels_per_step(co_engine* E, int32_t* n) {
     if (!E || !n) return fail(CO_EINVAL, "null argument");
     *n = 4;  // begin, classify(+admit), plan, apply(+check); plus the CUB sort passes
     return CO_OK;
+}
+
+}  // extern "C"
+
+// ---- random streams on the device (csrc/trace_gen.cuh) -----
+
+namespace {
+struct GenCtx {
+    cudaStream_t s = nullptr;
+    int sms = 148;
+    int r = CO_OK;
+    std::vector<void*> bufs;
+    ~GenCtx() {
+        for (void* p : bufs) cudaFree(p);
+        if (s) cudaStreamDestroy(s);
+    }
+    bool ck(cudaError_t e) {
+        if (e != cudaSuccess && r == CO_OK) r = fail(CO_ECUDA, cudaGetErrorString(e));
+        return r == CO_OK;
+    }
+    template <class T>
+    T* get(int64_t n) {
+        void* p = nullptr;
+        if (!ck(cudaMalloc(&p, (size_t)std::max<int64_t>(n, 1) * sizeof(T)))) return nullptr;
+        bufs.push_back(p);
+        return (T*)p;
+    }
+    int init(int device) {
+        if (device >= 0 && !ck(cudaSetDevice(device))) return r;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        return r;
+    }
+    int grid(int64_t n, int threads = 256) const {
+        return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, (int64_t)sms * 8));
+    }
+};
+
+void stream_seed(uint64_t seed, uint64_t stream, u128& st, u128& inc) {
+    const uint64_t ent[2] = {seed, stream};
+    seed_pcg64(ent, 2, st, inc);
+}
+
+void pcg_fill(GenCtx& G, u128 st, u128 inc, int64_t count, uint64_t* out) {
+    const int grid = G.grid(count);
+    u128 jm, jp;
+    pcg_jump(inc, (uint64_t)grid * 256, jm, jp);
+    k_pcg_fill<<<grid, 256, 0, G.s>>>(to_u(st), to_u(inc), to_u(jm), to_u(jp), count, out);
+    G.ck(cudaGetLastError());
+}
+
+// n ziggurat samples (+ the u53 of `extra` trailing words per sample)
+int zig_stream(GenCtx& G, int kind, u128 st, u128 inc, int64_t n, int extra, double* out, double* ex) {
+    if (n == 0) return CO_OK;
+    const int64_t M = ((n * (1 + extra) + n / 8 + 8192) + ORB_CHUNK - 1) / ORB_CHUNK * ORB_CHUNK, R = M + 4096,
+                  nch = M / ORB_CHUNK;
+    uint64_t* raw = G.get<uint64_t>(R);
+    uint8_t* len = G.get<uint8_t>(M);
+    uint32_t* accw = G.get<uint32_t>(M / 32);
+    uint32_t* vis = G.get<uint32_t>(M / 32);
+    double* val = G.get<double>(M);
+    int64_t* ex_ = G.get<int64_t>(nch);
+    int64_t* cnt = G.get<int64_t>(nch);
+    int64_t* total = G.get<int64_t>(1);
+    int32_t* bad = G.get<int32_t>(1);
+    if (G.r) return G.r;
+    pcg_fill(G, st, inc, R, raw);
+    if (kind == ZIG_EXP) k_zig_local<ZIG_EXP><<<G.grid(M), 256, 0, G.s>>>(raw, R, M, extra, len, accw, val);
+    else k_zig_local<ZIG_NOR><<<G.grid(M), 256, 0, G.s>>>(raw, R, M, extra, len, accw, val);
+    k_orbit_spec<<<(int)((nch + 127) / 128), 128, 0, G.s>>>(len, M, nch, vis, ex_);
+    k_orbit_fix<<<1, 1, 0, G.s>>>(len, nch, vis, ex_, bad);
+    k_orbit_count<<<(int)((nch * 32 + 255) / 256), 256, 0, G.s>>>(vis, accw, nch, cnt);
+    k_orbit_scan<<<1, 1024, 0, G.s>>>(cnt, nch, total);
+    k_orbit_emit<<<(int)((nch * 32 + 255) / 256), 256, 0, G.s>>>(vis, accw, cnt, len, val, raw, nch, n, extra, out,
+                                                                  ex);
+    G.ck(cudaGetLastError());
+    int64_t got = 0;
+    G.ck(cudaMemcpyAsync(&got, total, 8, cudaMemcpyDeviceToHost, G.s));
+    G.ck(cudaStreamSynchronize(G.s));
+    if (G.r) return G.r;
+    if (got < n) return fail(CO_EDEVICE, "ziggurat stream budget exhausted");
+    return CO_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int co_pcg64_seed(const uint64_t* entropy, int32_t n, uint64_t out[4]) {
+    if (!entropy || !out || n < 1) return fail(CO_EINVAL, "bad entropy");
+    u128 st, inc;
+    seed_pcg64(entropy, n, st, inc);
+    out[0] = (uint64_t)(st >> 64); out[1] = (uint64_t)st;
+    out[2] = (uint64_t)(inc >> 64); out[3] = (uint64_t)inc;
+    return CO_OK;
+}
+
+int co_gen_raw(uint64_t seed, uint64_t stream, int64_t count, int device, uint64_t* out) {
+    if (count < 0 || (count && !out)) return fail(CO_EINVAL, "bad arguments");
+    GenCtx G;
+    if (G.init(device)) return G.r;
+    u128 st, inc;
+    stream_seed(seed, stream, st, inc);
+    if (count) pcg_fill(G, st, inc, count, out);
+    G.ck(cudaStreamSynchronize(G.s));
+    return G.r;
+}
+
+int co_gen_std(int32_t kind, uint64_t seed, uint64_t stream, int64_t n, int device, double* out) {
+    if (n < 0 || (n && !out) || (kind != ZIG_EXP && kind != ZIG_NOR)) return fail(CO_EINVAL, "bad arguments");
+    GenCtx G;
+    if (G.init(device)) return G.r;
+    u128 st, inc;
+    stream_seed(seed, stream, st, inc);
+    return zig_stream(G, kind, st, inc, n, 0, out, nullptr);
+}
+
+int co_gen_trace(const co_trace_spec* sp, uint64_t seed, int device, int64_t* arrival_us, int32_t* prompt_len,
+                 int32_t* output_len) {
+    if (!sp || sp->n < 0 || sp->n > (1ll << 30)) return fail(CO_EINVAL, "bad trace spec");
+    const int64_t n = sp->n;
+    if (n && (!arrival_us || !prompt_len || !output_len)) return fail(CO_EINVAL, "null output");
+    if (!(sp->gap_scale > 0) || sp->input_min < 1 || sp->input_min > sp->input_max || sp->output_min < 1 ||
+        sp->output_min > sp->output_max)
+        return fail(CO_EINVAL, "invalid trace spec (workload.py:33-47 rules)");
+    if (n == 0) return CO_OK;
+    GenCtx G;
+    if (G.init(device)) return G.r;
+    double* z = G.get<double>(n);
+    if (G.r) return G.r;
+    u128 st, inc;
+    stream_seed(seed, 0, st, inc);
+    if (int r = zig_stream(G, ZIG_EXP, st, inc, n, 0, z, nullptr)) return r;
+    k_arrivals<<<1, 32, 0, G.s>>>(z, n, sp->gap_scale, arrival_us);
+    G.ck(cudaStreamSynchronize(G.s));  // z is reused below
+    stream_seed(seed, 1, st, inc);
+    if (int r = zig_stream(G, ZIG_NOR, st, inc, n, 0, z, nullptr)) return r;
+    k_lognormal_len<<<G.grid(n), 256, 0, G.s>>>(z, n, sp->mu_in, sp->sigma_in, sp->input_min, sp->input_max,
+                                                prompt_len);
+    G.ck(cudaStreamSynchronize(G.s));
+    stream_seed(seed, 2, st, inc);
+    if (int r = zig_stream(G, ZIG_NOR, st, inc, n, 0, z, nullptr)) return r;
+    k_lognormal_len<<<G.grid(n), 256, 0, G.s>>>(z, n, sp->mu_out, sp->sigma_out, sp->output_min, sp->output_max,
+                                                output_len);
+    G.ck(cudaGetLastError());
+    G.ck(cudaStreamSynchronize(G.s));
+    return G.r;
+}
+
+int co_gen_slos(int64_t n, const int32_t* prompt_len, const co_slo_spec* sp, uint64_t seed, int device,
+                int64_t* slo_ttft_us, int64_t* slo_tbt_us) {
+    if (!sp || n < 0 || (n && (!prompt_len || !slo_ttft_us || !slo_tbt_us))) return fail(CO_EINVAL, "bad arguments");
+    if (sp->base_ttft_us <= 0 || sp->base_tbt_us <= 0) return fail(CO_EINVAL, "baselines must be > 0");
+    if (!(0 < sp->scale_lo && sp->scale_lo <= sp->scale_hi) || sp->chunk_budget < 1)
+        return fail(CO_EINVAL, "invalid SloPolicy (workload.py:156-166 rules)");
+    if (n == 0) return CO_OK;
+    GenCtx G;
+    if (G.init(device)) return G.r;
+    uint64_t* ra = G.get<uint64_t>(n);
+    uint64_t* rb = G.get<uint64_t>(n);
+    if (G.r) return G.r;
+    u128 st, inc;
+    stream_seed(seed, 10, st, inc);
+    pcg_fill(G, st, inc, n, ra);
+    stream_seed(seed, 11, st, inc);
+    pcg_fill(G, st, inc, n, rb);
+    k_slos<<<G.grid(n), 256, 0, G.s>>>(ra, rb, prompt_len, n, sp->scale_lo, sp->scale_hi - sp->scale_lo,
+                                       sp->base_ttft_us, sp->base_tbt_us, sp->chunk_budget, slo_ttft_us, slo_tbt_us);
+    G.ck(cudaGetLastError());
+    G.ck(cudaStreamSynchronize(G.s));
+    return G.r;
+}
+
+int co_gen_predictor(int64_t n, const co_predictor_spec* sp, uint64_t seed, int device, int32_t* err,
+                     uint8_t* flip) {
+    if (!sp || n < 0 || (n && (!err || !flip))) return fail(CO_EINVAL, "bad arguments");
+    if (sp->error_dist < CO_ERR_ZERO || sp->error_dist > CO_ERR_NORMAL || !(sp->error_scale >= 0) ||
+        !(sp->direction_accuracy >= 0.0 && sp->direction_accuracy <= 1.0))
+        return fail(CO_EINVAL, "invalid PredictorConfig (estimation.py:29-42 rules)");
+    if (n == 0) return CO_OK;
+    GenCtx G;
+    if (G.init(device)) return G.r;
+    const int flip_on = sp->direction_accuracy < 1.0;
+    const double miss = 1.0 - sp->direction_accuracy;
+    u128 st, inc;
+    stream_seed(seed, 3, st, inc);
+    const int64_t s_int = (int64_t)sp->error_scale;  // int(cfg.error_scale)
+    if (sp->error_dist == CO_ERR_NORMAL) {
+        double* z = G.get<double>(n);
+        double* u = flip_on ? G.get<double>(n) : nullptr;
+        if (G.r) return G.r;
+        if (int r = zig_stream(G, ZIG_NOR, st, inc, n, flip_on, z, u)) return r;
+        k_pred_normal<<<G.grid(n), 256, 0, G.s>>>(z, u, n, sp->error_scale, miss, flip_on, err, flip);
+    } else if (sp->error_dist == CO_ERR_UNIFORM && s_int > 0) {
+        if (s_int >= (1ll << 31) - 1) return fail(CO_EINVAL, "error_scale too large for int32 draws");
+        const int64_t R = (flip_on ? 3 * ((n + 1) / 2) + 2 : (n + 1) / 2 + 1) + 4096;
+        uint64_t* raw = G.get<uint64_t>(R);
+        unsigned long long* rej = G.get<unsigned long long>(1);
+        int32_t* bad = G.get<int32_t>(1);
+        if (G.r) return G.r;
+        pcg_fill(G, st, inc, R, raw);
+        G.ck(cudaMemsetAsync(rej, 0xff, 8, G.s));
+        G.ck(cudaMemsetAsync(bad, 0, 4, G.s));
+        k_pred_uniform<<<G.grid(n), 256, 0, G.s>>>(raw, n, (uint32_t)s_int, miss, flip_on, err, flip, rej);
+        k_pred_uniform_fix<<<1, 1, 0, G.s>>>(raw, R, n, (uint32_t)s_int, miss, flip_on, err, flip, rej, bad);
+        int32_t hb = 0;
+        G.ck(cudaMemcpyAsync(&hb, bad, 4, cudaMemcpyDeviceToHost, G.s));
+        G.ck(cudaStreamSynchronize(G.s));
+        if (!G.r && hb) return fail(CO_EDEVICE, "predictor stream budget exhausted");
+    } else if (flip_on) {
+        uint64_t* raw = G.get<uint64_t>(n);
+        if (G.r) return G.r;
+        pcg_fill(G, st, inc, n, raw);
+        k_pred_flip_only<<<G.grid(n), 256, 0, G.s>>>(raw, n, miss, err, flip);
+    } else {
+        G.ck(cudaMemsetAsync(err, 0, n * 4, G.s));
+        G.ck(cudaMemsetAsync(flip, 0, n, G.s));
+    }
+    G.ck(cudaGetLastError());
+    G.ck(cudaStreamSynchronize(G.s));
+    return G.r;
 }
 
 }  // extern "C"

@@ -21,7 +21,8 @@ from . import _native as N
 from .config import DEVICE_POLICIES, EngineConfig
 from .core import (STATE_FROM_CODE, STRATEGY_FROM_CODE, US_PER_S, Direction, LengthEstimate,
                    Lifecycle, Request, RequestRuntime, Strategy)
-from .hostprep import (bin_of, charge_luts, iteration_us, noise_draws, run_confidence, run_padding,
+from .devrng import predictor_draws_device
+from .hostprep import (bin_of, charge_luts, iteration_us, run_confidence, run_padding,
                        sweet_spot)
 
 STRATEGY_CODE = {Strategy.SWAP: 0, Strategy.RECOMPUTE: 1}
@@ -315,7 +316,9 @@ class Engine:
         arr_sorted = arr[order]
         self.confidence = run_confidence(cfg, arr_sorted)
         self.padding = run_padding(cfg, self.confidence)
-        err, flip = noise_draws(cfg, n)
+        # estimation.py:76-99 noise, drawn on the GPU from default_rng([seed, 3])
+        err_d, flip_d = predictor_draws_device(cfg.predictor, cfg.seed, n, device)
+        err, flip = err_d.cpu().numpy(), flip_d.cpu().numpy()
         s_max = int((prompt.astype(np.int64) + tout).max()) if n else 1
         luts = charge_luts(cfg, max(s_max, 1))
         self._keep = [req_id, arr, prompt, tout, ttft, tbt, err, flip, *luts]
