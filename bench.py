@@ -315,6 +315,56 @@ def costmodel_leg(dev):
                 "kv_integrity": {"mismatches": bad, "checked": checked}}}
 
 
+def tracegen_leg(dev, n=524_288, reps=3):
+    """the config-4 trace (512K requests) with its SLOs and
+    predictor noise drawn on the GPU (csrc/trace_gen.cuh) vs numpy on the host
+    (the reference's own generators), and checked bit-exact against it."""
+    import paper_2503_13773_b200 as P
+    from paper_2503_13773_b200 import devrng, hostprep
+    from paper_2503_13773_b200.config import EngineConfig, PredictorConfig
+    spec = P.PRESETS["sharegpt"].sized(n, 1e6)
+    pol = P.SloPolicy()
+    pc = PredictorConfig(error_dist="uniform", error_scale=24, direction_accuracy=0.9)
+
+    def device_once():
+        cols = devrng.trace_arrays_device(spec, 0, dev)
+        t, b = devrng.assign_slos_device(cols["prompt_len"], 2_000_000, 200_000, pol, 0)
+        e, f = devrng.predictor_draws_device(pc, 0, n, dev)
+        return cols, t, b, e, f
+
+    device_once()  # module load / first-touch
+    ms = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        out = device_once()
+        ms.append((time.perf_counter() - t0) * 1e3)
+    cols, t, b, e, f = out
+    t0 = time.perf_counter()
+    h = P.trace_arrays(spec, 0)
+    ht, hb = P.workload.slo_arrays(h["prompt_len"], 2_000_000, 200_000, pol, 0)
+    t_host_trace = time.perf_counter() - t0
+    cfg = EngineConfig(predictor=pc)
+    t0 = time.perf_counter()
+    he, hf = hostprep.noise_draws(cfg, n)
+    t_host_pred = time.perf_counter() - t0
+    exact = bool((cols["arrival_us"].cpu().numpy() == h["arrival_us"]).all()
+                 and (cols["prompt_len"].cpu().numpy() == h["prompt_len"]).all()
+                 and (cols["true_output_len"].cpu().numpy() == h["true_output_len"]).all()
+                 and (t.cpu().numpy() == ht).all() and (b.cpu().numpy() == hb).all()
+                 and (e.cpu().numpy() == he).all() and (f.cpu().numpy() == hf).all())
+    dev_ms = min(ms)
+    host_ms = (t_host_trace + t_host_pred) * 1e3
+    return {"metric": "trace generation requests/s", "requests": n,
+            "workload": "BASELINE config 4 trace: sharegpt x 524,288 @1e6 req/s + assign_slos(2 s, 200 ms) + "
+                        "uniform(24) / 90%-direction predictor draws, seed 0",
+            "device_ms": dev_ms, "device_ms_all": ms, "value": n / (dev_ms * 1e-3),
+            "host_numpy_ms": host_ms, "host_numpy_value": n / (host_ms * 1e-3),
+            "host_breakdown_ms": {"trace+slos": t_host_trace * 1e3, "predictor": t_host_pred * 1e3},
+            "bit_exact_vs_numpy": exact,
+            "how": "wall clock around the synchronous C-ABI calls (outputs allocated by torch), best of "
+                   f"{reps} after one warm call; host = numpy Generator + the reference's per-request loops"}
+
+
 def peak_kind_label(kind):
     return f"{kind} (MEASURED_PEAKS.json hbm_gbs)" if kind == "measured" else kind
 
@@ -416,6 +466,10 @@ def device_arm(args, rank, world, dist):
             extra["costmodel"] = costmodel_leg(dev)
         except Exception as exc:
             extra["costmodel"] = {"error": repr(exc)}
+        try:
+            extra["tracegen"] = tracegen_leg(dev)
+        except Exception as exc:
+            extra["tracegen"] = {"error": repr(exc)}
     line = {
         "metric": METRIC, "value": decisions / (dev_ms * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,

@@ -22,6 +22,8 @@
 #include <numeric>
 #include <string>
 #include <vector>
+#include <map>
+#include <mutex>
 
 #include "engine_state.cuh"
 #include "block_ops.cuh"
@@ -1248,32 +1250,51 @@ int co_kernels_per_step(co_engine* E, int32_t* n) {
 // ---- random streams on the device (csrc/trace_gen.cuh) -----
 
 namespace {
+// Scratch and stream of the generator calls: grow-only per-device slots,
+// reused call after call (slot i = the i-th buffer a call asks for), so a
+// generation costs kernels, not cudaMalloc / cudaFree / stream creation.
+// Calls are serialized by a process-wide mutex and end with a stream sync.
+struct GenArena {
+    cudaStream_t s = nullptr;
+    std::vector<std::pair<void*, size_t>> slots;
+};
+std::mutex g_gen_mu;
+std::map<int, GenArena> g_gen_arena;
+
 struct GenCtx {
+    std::lock_guard<std::mutex> lk{g_gen_mu};
+    GenArena* A = nullptr;
     cudaStream_t s = nullptr;
     int sms = 148;
     int r = CO_OK;
-    std::vector<void*> bufs;
-    ~GenCtx() {
-        for (void* p : bufs) cudaFree(p);
-        if (s) cudaStreamDestroy(s);
-    }
+    size_t slot = 0;
     bool ck(cudaError_t e) {
         if (e != cudaSuccess && r == CO_OK) r = fail(CO_ECUDA, cudaGetErrorString(e));
         return r == CO_OK;
     }
     template <class T>
     T* get(int64_t n) {
-        void* p = nullptr;
-        if (!ck(cudaMalloc(&p, (size_t)std::max<int64_t>(n, 1) * sizeof(T)))) return nullptr;
-        bufs.push_back(p);
-        return (T*)p;
+        const size_t bytes = (size_t)std::max<int64_t>(n, 1) * sizeof(T);
+        if (r) return nullptr;
+        if (A->slots.size() <= slot) A->slots.push_back({nullptr, 0});
+        auto& sl = A->slots[slot++];
+        if (sl.second < bytes) {
+            if (sl.first) cudaFree(sl.first);
+            sl = {nullptr, 0};
+            const size_t want = bytes + bytes / 4;
+            if (!ck(cudaMalloc(&sl.first, want))) return nullptr;
+            sl.second = want;
+        }
+        return (T*)sl.first;
     }
     int init(int device) {
         if (device >= 0 && !ck(cudaSetDevice(device))) return r;
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        A = &g_gen_arena[dev];
+        if (!A->s) ck(cudaStreamCreateWithFlags(&A->s, cudaStreamNonBlocking));
+        s = A->s;
         return r;
     }
     int grid(int64_t n, int threads = 256) const {
@@ -1302,9 +1323,10 @@ int zig_stream(GenCtx& G, int kind, u128 st, u128 inc, int64_t n, int extra, dou
     uint64_t* raw = G.get<uint64_t>(R);
     uint8_t* len = G.get<uint8_t>(M);
     uint32_t* accw = G.get<uint32_t>(M / 32);
-    uint32_t* vis = G.get<uint32_t>(M / 32);
+    uint32_t* vis = G.get<uint32_t>(nch * ORB_K * 32);
     double* val = G.get<double>(M);
-    int64_t* ex_ = G.get<int64_t>(nch);
+    int64_t* ex_ = G.get<int64_t>(nch * ORB_K);
+    int8_t* choice = G.get<int8_t>(nch);
     int64_t* cnt = G.get<int64_t>(nch);
     int64_t* total = G.get<int64_t>(1);
     int32_t* bad = G.get<int32_t>(1);
@@ -1312,12 +1334,12 @@ int zig_stream(GenCtx& G, int kind, u128 st, u128 inc, int64_t n, int extra, dou
     pcg_fill(G, st, inc, R, raw);
     if (kind == ZIG_EXP) k_zig_local<ZIG_EXP><<<G.grid(M), 256, 0, G.s>>>(raw, R, M, extra, len, accw, val);
     else k_zig_local<ZIG_NOR><<<G.grid(M), 256, 0, G.s>>>(raw, R, M, extra, len, accw, val);
-    k_orbit_spec<<<(int)((nch + 127) / 128), 128, 0, G.s>>>(len, M, nch, vis, ex_);
-    k_orbit_fix<<<1, 1, 0, G.s>>>(len, nch, vis, ex_, bad);
-    k_orbit_count<<<(int)((nch * 32 + 255) / 256), 256, 0, G.s>>>(vis, accw, nch, cnt);
+    k_orbit_spec<<<(int)((nch + ORB_WARPS - 1) / ORB_WARPS), ORB_WARPS * 32, 0, G.s>>>(len, M, nch, vis, ex_);
+    k_orbit_fix<<<1, 256, 0, G.s>>>(len, nch, vis, ex_, choice, bad);
+    k_orbit_count<<<(int)((nch * 32 + 255) / 256), 256, 0, G.s>>>(vis, choice, accw, nch, cnt);
     k_orbit_scan<<<1, 1024, 0, G.s>>>(cnt, nch, total);
-    k_orbit_emit<<<(int)((nch * 32 + 255) / 256), 256, 0, G.s>>>(vis, accw, cnt, len, val, raw, nch, n, extra, out,
-                                                                  ex);
+    k_orbit_emit<<<(int)((nch * 32 + 255) / 256), 256, 0, G.s>>>(vis, choice, accw, cnt, len, val, raw, nch, n,
+                                                                  extra, out, ex);
     G.ck(cudaGetLastError());
     int64_t got = 0;
     G.ck(cudaMemcpyAsync(&got, total, 8, cudaMemcpyDeviceToHost, G.s));
@@ -1375,7 +1397,7 @@ int co_gen_trace(const co_trace_spec* sp, uint64_t seed, int device, int64_t* ar
     u128 st, inc;
     stream_seed(seed, 0, st, inc);
     if (int r = zig_stream(G, ZIG_EXP, st, inc, n, 0, z, nullptr)) return r;
-    k_arrivals<<<1, 32, 0, G.s>>>(z, n, sp->gap_scale, arrival_us);
+    k_arrivals<<<1, ARR_T, 0, G.s>>>(z, n, sp->gap_scale, arrival_us);
     G.ck(cudaStreamSynchronize(G.s));  // z is reused below
     stream_seed(seed, 1, st, inc);
     if (int r = zig_stream(G, ZIG_NOR, st, inc, n, 0, z, nullptr)) return r;

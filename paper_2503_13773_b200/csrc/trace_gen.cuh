@@ -163,73 +163,105 @@ __global__ void k_zig_local(const uint64_t* __restrict__ raw, int64_t R, int64_t
     }
 }
 
-// speculative orbit of each chunk from its first position; exit[k] = the
-// first orbit position past the chunk (-1: ran into an invalid position)
-__global__ void k_orbit_spec(const uint8_t* __restrict__ len, int64_t M, int64_t nch, uint32_t* vis, int64_t* exit_) {
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// speculative orbits of each chunk from its first ORB_K positions (the true
+// orbit enters a chunk at most a sample's length past its start, so one of
+// them almost always IS the true orbit there; with a trailing word per
+// sample, entries at odd offsets are as common as even ones).  One warp per
+// chunk: the warp stages the chunk's lens in shared memory, lane v chases
+// from position v.  exit[k][v] = the first orbit position past the chunk
+// (-1: the chase ran into an invalid position).
+constexpr int ORB_WARPS = 4, ORB_K = 4;
+__global__ void __launch_bounds__(ORB_WARPS * 32) k_orbit_spec(const uint8_t* __restrict__ len, int64_t M,
+                                                                int64_t nch, uint32_t* vis, int64_t* exit_) {
+    __shared__ uint8_t sl[ORB_WARPS][ORB_CHUNK];
+    __shared__ uint32_t sw[ORB_WARPS][ORB_K][ORB_CHUNK / 32];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t k = (int64_t)blockIdx.x * ORB_WARPS + wid;
     if (k >= nch) return;
-    const int64_t s = k * ORB_CHUNK, e = s + ORB_CHUNK;
-    uint32_t* w = vis + (s >> 5);
-    uint32_t cur = 0;
-    int cw = 0;
-    int64_t p = s;
-    while (p < e) {
-        const int c = len[p];
-        if (c == 0) { p = -1; break; }
-        const int wi = (int)((p - s) >> 5);
-        while (cw < wi) { w[cw++] = cur; cur = 0; }
-        cur |= 1u << (p & 31);
-        p += c;
-    }
-    if (p < 0) {
-        for (; cw < ORB_CHUNK / 32; cw++) { w[cw] = cur; cur = 0; }
-        exit_[k] = -1;
-        return;
-    }
-    for (; cw < ORB_CHUNK / 32; cw++) { w[cw] = cur; cur = 0; }
-    exit_[k] = p;
-}
-
-// true entries, chunk by chunk (one thread): repair the prefix of a chunk
-// the true orbit enters past its first position, until it merges
-__global__ void k_orbit_fix(const uint8_t* __restrict__ len, int64_t nch, uint32_t* vis, const int64_t* exit_,
-                            int32_t* bad) {
-    int64_t t = 0;
-    for (int64_t k = 0; k < nch; k++) {
-        const int64_t s = k * ORB_CHUNK, e = s + ORB_CHUNK;
-        uint32_t* w = vis + (s >> 5);
-        if (t < 0) {
-            for (int i = 0; i < ORB_CHUNK / 32; i++) w[i] = 0;
-            continue;
-        }
-        if (t >= e) {
-            for (int i = 0; i < ORB_CHUNK / 32; i++) w[i] = 0;
-            continue;
-        }
-        if (t == s) { t = exit_[k]; continue; }
-        for (int64_t q = s; q < t; q++) w[(q - s) >> 5] &= ~(1u << (q & 31));
-        int64_t p = t;
+    const int64_t s = k * ORB_CHUNK;
+    const uint4* src = reinterpret_cast<const uint4*>(len + s);
+    for (int i = lane; i < ORB_CHUNK / 16; i += 32) reinterpret_cast<uint4*>(sl[wid])[i] = src[i];
+#pragma unroll
+    for (int v = 0; v < ORB_K; v++) sw[wid][v][lane] = 0;
+    __syncwarp();
+    if (lane < ORB_K) {
+        int p = lane;
+        int64_t ex = 0;
         for (;;) {
-            if (p >= e) { t = p; break; }
-            if (w[(p - s) >> 5] >> (p & 31) & 1) { t = exit_[k]; break; }
-            const int c = len[p];
-            if (c == 0) { t = -1; break; }
-            w[(p - s) >> 5] |= 1u << (p & 31);
-            const int64_t q_end = p + c < e ? p + c : e;
-            for (int64_t q = p + 1; q < q_end; q++) w[(q - s) >> 5] &= ~(1u << (q & 31));
+            if (p >= ORB_CHUNK) { ex = s + p; break; }
+            const int c = sl[wid][p];
+            if (c == 0) { ex = -1; break; }
+            sw[wid][lane][p >> 5] |= 1u << (p & 31);
             p += c;
         }
+        exit_[k * ORB_K + lane] = ex;
     }
-    if (t < 0) *bad = 1;
+    __syncwarp();
+#pragma unroll
+    for (int v = 0; v < ORB_K; v++) vis[(k * ORB_K + v) * 32 + lane] = sw[wid][v][lane];
+}
+
+// true entries, chunk by chunk (one thread walks; the block stages the
+// speculative exits in shared memory a tile at a time): choice[k] = the
+// variant whose orbit is the true one, -1 for a chunk the orbit skips.  An
+// entry past the first ORB_K positions (not seen in practice) is repaired in
+// variant 0's bitmap by a chase from the entry until it merges.
+__global__ void k_orbit_fix(const uint8_t* __restrict__ len, int64_t nch, uint32_t* vis, const int64_t* exit_,
+                            int8_t* choice, int32_t* bad) {
+    constexpr int TILE = 1024;
+    __shared__ int64_t se[TILE * ORB_K];
+    __shared__ int64_t t_s;
+    if (threadIdx.x == 0) t_s = 0;
+    for (int64_t k0 = 0; k0 < nch; k0 += TILE) {
+        const int m = (int)(nch - k0 < TILE ? nch - k0 : TILE);
+        __syncthreads();
+        for (int i = threadIdx.x; i < m * ORB_K; i += blockDim.x) se[i] = exit_[k0 * ORB_K + i];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int64_t t = t_s;
+            for (int i = 0; i < m; i++) {
+                const int64_t k = k0 + i, s = k * ORB_CHUNK, e = s + ORB_CHUNK;
+                const int64_t off = t - s;
+                if (t >= 0 && off >= 0 && off < ORB_K) {
+                    choice[k] = (int8_t)off;
+                    t = se[i * ORB_K + off];
+                    continue;
+                }
+                if (t < 0 || t >= e) { choice[k] = -1; continue; }
+                choice[k] = 0;
+                uint32_t* w = vis + k * ORB_K * 32;
+                for (int64_t q = s; q < t; q++) w[(q - s) >> 5] &= ~(1u << (q & 31));
+                int64_t p = t;
+                for (;;) {
+                    if (p >= e) { t = p; break; }
+                    if (w[(p - s) >> 5] >> (p & 31) & 1) { t = se[i * ORB_K]; break; }
+                    const int c = len[p];
+                    if (c == 0) { t = -1; break; }
+                    w[(p - s) >> 5] |= 1u << (p & 31);
+                    const int64_t q_end = p + c < e ? p + c : e;
+                    for (int64_t q = p + 1; q < q_end; q++) w[(q - s) >> 5] &= ~(1u << (q & 31));
+                    p += c;
+                }
+            }
+            t_s = t;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && t_s < 0) *bad = 1;
+}
+
+__device__ __forceinline__ uint32_t orbit_word(const uint32_t* vis, const int8_t* choice, int64_t k, int lane) {
+    const int c = choice[k];
+    return c < 0 ? 0u : vis[(k * ORB_K + c) * 32 + lane];
 }
 
 // accepted samples per chunk (warp per chunk)
-__global__ void k_orbit_count(const uint32_t* __restrict__ vis, const uint32_t* __restrict__ accw, int64_t nch,
-                              int64_t* cnt) {
+__global__ void k_orbit_count(const uint32_t* __restrict__ vis, const int8_t* __restrict__ choice,
+                              const uint32_t* __restrict__ accw, int64_t nch, int64_t* cnt) {
     const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (k >= nch) return;
-    int c = __popc(vis[k * 32 + lane] & accw[k * 32 + lane]);
+    int c = __popc(orbit_word(vis, choice, k, lane) & accw[k * 32 + lane]);
     for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     if (lane == 0) cnt[k] = c;
 }
@@ -255,14 +287,15 @@ __global__ void k_orbit_scan(int64_t* cnt, int64_t nch, int64_t* total) {
 
 // ordered compaction: sample j = j-th accepting orbit position; `ex` gets the
 // u53 of the trailing word when extra > 0
-__global__ void k_orbit_emit(const uint32_t* __restrict__ vis, const uint32_t* __restrict__ accw,
+__global__ void k_orbit_emit(const uint32_t* __restrict__ vis, const int8_t* __restrict__ choice,
+                             const uint32_t* __restrict__ accw,
                              const int64_t* __restrict__ off, const uint8_t* __restrict__ len,
                              const double* __restrict__ val, const uint64_t* __restrict__ raw, int64_t nch, int64_t n,
                              int extra, double* out, double* ex) {
     const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (k >= nch) return;
-    uint32_t m = vis[k * 32 + lane] & accw[k * 32 + lane];
+    uint32_t m = orbit_word(vis, choice, k, lane) & accw[k * 32 + lane];
     const int c = __popc(m);
     int inc = c;
     for (int o = 1; o < 32; o <<= 1) {
@@ -285,25 +318,120 @@ __global__ void k_orbit_emit(const uint32_t* __restrict__ vis, const uint32_t* _
 // -- consumers of the samples --------------------------------------------------
 
 // workload.py:92-93: gaps = scale * E; arrival_us = floor(cumsum(gaps) * 1e6 + 0.5).
-// np.cumsum is a left-to-right running sum, so lane 0 adds serially while the
-// warp stages tiles through shared memory.
-__global__ void k_arrivals(const double* __restrict__ e, int64_t n, double scale, int64_t* arrival) {
-    __shared__ double tile[1024];
-    __shared__ double cs[1024];
-    double acc = 0.0;
-    for (int64_t b = 0; b < n; b += 1024) {
-        const int m = (int)(n - b < 1024 ? n - b : 1024);
-        for (int i = threadIdx.x; i < m; i += blockDim.x) tile[i] = __dmul_rn(scale, e[b + i]);
-        __syncwarp();
-        if (threadIdx.x == 0) {
-            int i = 0;
-            if (b == 0) { acc = tile[0]; cs[0] = acc; i = 1; }
-            for (; i < m; i++) { acc = __dadd_rn(acc, tile[i]); cs[i] = acc; }
+//
+// np.cumsum is the left-to-right running sum s_i = fl(s_{i-1} + g_i).  It is
+// evaluated exactly in parallel: while s stays in one binade [2^e, 2^(e+1))
+// every partial sum is an integer multiple of u = ulp(s) = 2^(e-52), and
+// fl(x + g) = x + u * rne(g / u) -- an INTEGER increment independent of x --
+// unless g / u sits exactly on a half (a tie: round-half-even then depends on
+// the parity of x / u) or the sum leaves the binade.  So one CTA sweeps the
+// array in tiles: increments k_i = rint(g_i / u) and a block-wide int64 prefix
+// give every s_i = (x/u + P_i) * u exactly up to the first tie or binade exit;
+// that one element is added in double the sequential way, and the sweep
+// resumes after it.  Rounds = tiles + binades (~20) + ties (~1 per 2^19
+// elements at config-2 magnitudes).
+constexpr int ARR_T = 1024, ARR_I = 8;
+__global__ void __launch_bounds__(ARR_T) k_arrivals(const double* __restrict__ e, int64_t n, double scale,
+                                                    int64_t* arrival) {
+    __shared__ long long wsum[ARR_T / 32];
+    __shared__ int64_t s_f;
+    __shared__ double s_x;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (n <= 0) return;
+    double x = __dmul_rn(scale, e[0]);  // s_0 = g_0
+    if (tid == 0) arrival[0] = (int64_t)floor(__dadd_rn(__dmul_rn(x, 1000000.0), 0.5));
+    int64_t pos = 1;
+    while (pos < n) {
+        const int64_t end = pos + (int64_t)ARR_T * ARR_I < n ? pos + (int64_t)ARR_T * ARR_I : n;
+        int ex = 0;
+        const double m = frexp(x, &ex);  // x = m 2^ex, m in [0.5, 1): u = 2^(ex-53), X = m 2^53
+        const long long X = (long long)ldexp(m, 53);
+        const bool xok = x > 0.0;
+        // this thread's items: pos + tid*ARR_I + j
+        long long k[ARR_I];
+        bool bad[ARR_I];
+        double g[ARR_I];
+        long long tsum = 0;
+#pragma unroll
+        for (int j = 0; j < ARR_I; j++) {
+            const int64_t i = pos + (int64_t)tid * ARR_I + j;
+            g[j] = i < end ? __dmul_rn(scale, e[i]) : 0.0;
+            const double q = ldexp(g[j], 53 - ex);
+            const double fq = floor(q);
+            bad[j] = i < end && (!xok || q - fq == 0.5 || q >= 4.0e18);
+            k[j] = (i < end && !bad[j]) ? (long long)rint(q) : 0;
+            tsum += k[j];
         }
-        __syncwarp();
-        for (int i = threadIdx.x; i < m; i += blockDim.x)
-            arrival[b + i] = (int64_t)floor(__dadd_rn(__dmul_rn(cs[i], 1000000.0), 0.5));
-        __syncwarp();
+        // block exclusive scan of the thread sums
+        long long inc = tsum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) wsum[w] = inc;
+        if (tid == 0) s_f = end;
+        __syncthreads();
+        if (w == 0) {
+            long long v = wsum[lane], z = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long y = __shfl_up_sync(0xffffffffu, z, o);
+                if (lane >= o) z += y;
+            }
+            wsum[lane] = z - v;
+        }
+        __syncthreads();
+        long long P = wsum[w] + inc - tsum;  // prefix before this thread's first item
+        // first exception: a tie / unrepresentable increment, or leaving the binade
+        int64_t my_f = end;
+        {
+            long long Q = P;
+#pragma unroll
+            for (int j = 0; j < ARR_I; j++) {
+                const int64_t i = pos + (int64_t)tid * ARR_I + j;
+                if (i >= end) break;
+                if (bad[j]) { my_f = i; break; }
+                Q += k[j];
+                if (X + Q >= (1ll << 53)) { my_f = i; break; }
+            }
+        }
+        if (my_f < end) atomicMin((unsigned long long*)&s_f, (unsigned long long)my_f);
+        __syncthreads();
+        const int64_t f = s_f;
+        // exact partial sums before the exception
+        {
+            long long Q = P;
+#pragma unroll
+            for (int j = 0; j < ARR_I; j++) {
+                const int64_t i = pos + (int64_t)tid * ARR_I + j;
+                Q += k[j];
+                if (i < f) {
+                    const double si = ldexp((double)(X + Q), ex - 53);
+                    arrival[i] = (int64_t)floor(__dadd_rn(__dmul_rn(si, 1000000.0), 0.5));
+                    if (i == f - 1 && f == end) s_x = si;
+                }
+                if (i == f - 1 && f < end) s_x = ldexp((double)(X + Q), ex - 53);
+            }
+        }
+        __syncthreads();
+        if (f < end) {
+            // the exception element, the sequential way (thread owning it)
+            const int64_t rel = f - pos;
+            if (tid == (int)(rel / ARR_I)) {
+                const double prev = f == pos ? x : s_x;
+                const double sf = __dadd_rn(prev, g[rel % ARR_I]);
+                arrival[f] = (int64_t)floor(__dadd_rn(__dmul_rn(sf, 1000000.0), 0.5));
+                s_x = sf;
+            }
+            __syncthreads();
+            x = s_x;
+            pos = f + 1;
+        } else {
+            x = s_x;
+            pos = end;
+        }
+        __syncthreads();
     }
 }
 
