@@ -6,8 +6,10 @@ Python's own IEEE-double semantics, and handed to the device as integers:
 - the sweet spot s* (scheduler.py:378-393, preemption.py:176-195)
 - per-length swap / recompute charge LUTs (engine.py:372, 392-397;
   scheduler.py:368-374)
-- the predictor noise draws, consumed from default_rng([seed, 3]) in
-  (arrival, id) order exactly as engine.py:267/344-351 consumes it.
+- ``noise_draws``: the host twin of the predictor noise draws (consumed from
+  default_rng([seed, 3]) in (arrival, id) order exactly as engine.py:267/344-351
+  consumes it); the engine itself draws them on the GPU (devrng.py), this one
+  is the bench's host-side comparison.
 
 The device never evaluates a transcendental; the only float expression it
 evaluates is the iteration latency (costmodel.py:51-55), with explicit
