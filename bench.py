@@ -49,14 +49,26 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def make_trace(rank: int, world: int):
+def make_trace(rank: int, world: int, device=None):
     """Shard `rank` of a ShareGPT trace of 65,536*world requests (ids are
-    arrival-ordered, so a contiguous id slice is a contiguous time slice)."""
+    arrival-ordered, so a contiguous id slice is a contiguous time slice).
+    With a device, the whole trace and its SLOs are drawn on that GPU
+    (devrng, bit-identical to numpy's) and only the shard is materialised."""
     import paper_2503_13773_b200 as P
     spec = P.PRESETS["sharegpt"].sized(N_PER_GPU * world, 1e6 * world)
-    reqs = P.generate(spec, 0)
-    P.assign_slos(reqs, 2_000_000, 200_000, P.SloPolicy(), 0)
-    shard = reqs[rank * N_PER_GPU:(rank + 1) * N_PER_GPU]
+    lo, hi = rank * N_PER_GPU, (rank + 1) * N_PER_GPU
+    if device is not None:
+        from paper_2503_13773_b200 import devrng
+        cols = devrng.trace_arrays_device(spec, 0, device)
+        ttft, tbt = devrng.assign_slos_device(cols["prompt_len"], 2_000_000, 200_000, P.SloPolicy(), 0)
+        a, p, o = (cols[k][lo:hi].cpu().tolist() for k in ("arrival_us", "prompt_len", "true_output_len"))
+        t, b = ttft[lo:hi].cpu().tolist(), tbt[lo:hi].cpu().tolist()
+        shard = [P.Request(id=lo + i, arrival_us=a[i], prompt_len=p[i], true_output_len=o[i], slo_ttft_us=t[i],
+                           slo_tbt_us=b[i]) for i in range(len(a))]
+    else:
+        reqs = P.generate(spec, 0)
+        P.assign_slos(reqs, 2_000_000, 200_000, P.SloPolicy(), 0)
+        shard = reqs[lo:hi]
     cfg = P.EngineConfig(capacity_tokens=CAPACITY, reserved_blocks=8,
                          sched=P.SchedulerConfig(small_block_b=16), seed=0)
     return shard, cfg
@@ -377,7 +389,7 @@ def device_arm(args, rank, world, dist):
 
     torch.cuda.set_device(rank % max(1, torch.cuda.device_count()))
     dev = torch.cuda.current_device()
-    reqs, cfg = make_trace(rank, world)
+    reqs, cfg = make_trace(rank, world, dev)
     cfg.record_events = True
     eng = Engine(reqs, cfg, device=dev)
     if dist:
