@@ -275,7 +275,9 @@ int co_kernels_per_step(co_engine* eng, int32_t* n);
  * step by an L2 flush (a memset of flush_bytes), and returns the device time
  * of each step (step_ms[k], flush excluded) and the summed device time of
  * each stage over the k steps (stage_ms[CO_NSTAGES]).  Stages: begin+admit,
- * classify, bucket, plan, apply, check, data (N2 moves + KV fills), decode (N3). */
+ * classify, bucket, plan, apply, check, data (N2 moves + KV fills), decode (N3).
+ * stage_ms may be NULL: then only the step boundaries carry events, and the
+ * step kernels chain through programmatic-dependent-launch edges. */
 #define CO_NSTAGES 8
 int co_time_steps(co_engine* eng, int32_t k, int64_t flush_bytes, double* step_ms, double* stage_ms);
 

@@ -49,6 +49,7 @@ struct ApplySh {
 };
 
 __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
+    pdl_enter();
     __shared__ ApplySh S;
     Ctl& c = *d.ctl;
     if (!c.active) return;

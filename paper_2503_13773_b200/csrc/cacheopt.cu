@@ -129,6 +129,7 @@ struct co_engine {
     CUtensorMap kvmap;
     cudaGraphExec_t graph1 = nullptr;  // one step, step() semantics
     void* result_host = nullptr;
+    bool pdl = true;         // programmatic dependent launch between step kernels (CACHEOPT_PDL=0: off)
     bool tc_decode = false;  // tcgen05 (k_decode_tc05) when the block size tiles by 16; else CUDA cores
     int64_t page_bytes = 0;
     std::vector<co_event> st_events;   // host staging of drained device events
@@ -167,20 +168,40 @@ static inline void mark(cudaEvent_t e, cudaStream_t s) {
     cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
 }
 
+// a step kernel launched with programmatic stream serialization (see pdl_enter)
+template <typename... KArgs, typename... Args>
+static void launch_pdl(bool pdl, void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s,
+                       Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
     Dev& d = E->d;
     cudaStream_t s = E->stream;
     if (ev) mark(ev[0], s);
     k_begin<<<1, 32, 0, s>>>(d, guard);
     if (ev) mark(ev[1], s);
-    k_classify<<<d.nblk, 256, 0, s>>>(d);
+    // PDL edges only between back-to-back kernels (an event node in between
+    // is a full dependency anyway)
+    const bool pdl = E->pdl;
+    launch_pdl(pdl && !ev, k_classify, d.nblk, 256, 0, s, d);
     if (ev) mark(ev[2], s);
-    k_bins<<<E->grid, 256, 0, s>>>(d);
-    k_scatter<<<E->grid, 256, 0, s>>>(d);
+    launch_pdl(pdl && !ev, k_bins, E->grid, 256, 0, s, d);
+    launch_pdl(pdl, k_scatter, E->grid, 256, 0, s, d);
     if (ev) mark(ev[3], s);
-    k_plan<<<1, E->plan_threads, sizeof(PlanSh), s>>>(d);
+    launch_pdl(pdl && !ev, k_plan, 1, E->plan_threads, sizeof(PlanSh), s, d);
     if (ev) mark(ev[4], s);
-    k_apply<<<1, E->plan_threads, 0, s>>>(d);
+    launch_pdl(pdl && !ev, k_apply, 1, E->plan_threads, 0, s, d);
     if (ev) mark(ev[5], s);
     if (ev) mark(ev[6], s);  // (the validate_every check runs inside k_apply)
     if (E->comm) {
@@ -384,6 +405,7 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, E->device);
     E->grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8));
     E->sms = sms;
+    if (const char* pv = std::getenv("CACHEOPT_PDL")) E->pdl = std::atoi(pv) != 0;
     if (const char* pt = std::getenv("CACHEOPT_PLAN_THREADS")) {
         int v = std::atoi(pt);
         if (v >= 64 && v <= NT && v % 32 == 0) E->plan_threads = v;
@@ -978,9 +1000,18 @@ int co_time_steps(co_engine* E, int32_t k, int64_t flush_bytes, double* step_ms,
     cudaGraphExec_t ge = nullptr;
     int r = CO_OK;
     CK(cudaStreamBeginCapture(E->stream, cudaStreamCaptureModeThreadLocal));
+    const bool stages = stage_ms != nullptr;  // stage events split the graph; without them the
+                                              // step kernels chain through PDL edges
     for (int32_t j = 0; j < k && !r; j++) {
         if (flush) cudaMemsetAsync(flush, j & 0xff, flush_bytes, E->stream);
-        r = launch_step(E, 1, evs.data() + (size_t)j * NE);
+        cudaEvent_t* e = evs.data() + (size_t)j * NE;
+        if (stages) {
+            r = launch_step(E, 1, e);
+        } else {
+            mark(e[0], E->stream);
+            r = launch_step(E, 1, nullptr);
+            mark(e[NE - 1], E->stream);
+        }
     }
     CK(cudaStreamEndCapture(E->stream, &g));
     if (!r) {
@@ -988,13 +1019,14 @@ int co_time_steps(co_engine* E, int32_t k, int64_t flush_bytes, double* step_ms,
         CK(cudaGraphLaunch(ge, E->stream));
         if (E->comm) E->reduce_calls += k;
         CK(cudaStreamSynchronize(E->stream));
-        for (int q = 0; q < CO_NSTAGES; q++) stage_ms[q] = 0;
+        if (stages)
+            for (int q = 0; q < CO_NSTAGES; q++) stage_ms[q] = 0;
         for (int32_t j = 0; j < k; j++) {
             cudaEvent_t* e = evs.data() + (size_t)j * NE;
             float ms = 0;
             CK(cudaEventElapsedTime(&ms, e[0], e[NE - 1]));
             step_ms[j] = ms;
-            for (int q = 0; q < CO_NSTAGES; q++) {
+            for (int q = 0; q < CO_NSTAGES && stages; q++) {
                 float x = 0;
                 CK(cudaEventElapsedTime(&x, e[q], e[q + 1]));
                 stage_ms[q] += x;

@@ -11,6 +11,15 @@
 
 namespace co {
 
+// Programmatic dependent launch inside the step graph: a step kernel waits
+// for its predecessor's completion (and memory) here, then lets its own
+// successor launch, so each launch's latency overlaps the previous kernel's
+// tail.  A no-op when the kernel was launched without the PDL attribute.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 constexpr int NT = 256;   // threads of the single-CTA planner / apply kernels (max; 256 measured best)
 constexpr int TCHUNK = 64;  // pages per block-table chunk
 constexpr int NBIN = 4096;  // N'_w deadline buckets

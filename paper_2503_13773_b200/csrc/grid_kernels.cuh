@@ -100,6 +100,7 @@ __device__ __forceinline__ void admit_one(const Dev& d, int32_t i, int32_t lo, i
 //   N'_w blown, rt < 0 (arrival order) -> blown_tmp (block-ordered; SoA order IS (arrival, id))
 //   N'_w rt >= 0 ordered by (D, id)    -> key0 = D << idbits | idrank, range kmin..kmax
 __global__ void __launch_bounds__(256) k_classify(Dev d) {
+    pdl_enter();
     __shared__ int32_t sc[32];
     __shared__ int32_t tot_s[2];
     __shared__ uint64_t kr[2][8];
@@ -236,6 +237,7 @@ __device__ __forceinline__ int bin_shift(uint64_t range) {
 
 // histogram of the non-blown N'_w keys over NBIN range-adaptive buckets
 __global__ void __launch_bounds__(256) k_bins(Dev d) {
+    pdl_enter();
     __shared__ int32_t h[NBIN];
     const Ctl& c = *d.ctl;
     if (!c.active || c.cnt_nwp == 0) return;
@@ -259,6 +261,7 @@ __global__ void __launch_bounds__(256) k_bins(Dev d) {
 // scatter into bucket order (unordered within a bucket; the planner sorts
 // each bucket group by key when it first needs it)
 __global__ void __launch_bounds__(256) k_scatter(Dev d) {
+    pdl_enter();
     __shared__ int32_t off[NBIN];
     __shared__ int32_t wsum[8];
     const Ctl& c = *d.ctl;

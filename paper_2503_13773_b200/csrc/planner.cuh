@@ -497,6 +497,7 @@ __device__ void plan_baseline(const Dev& d, PlanSh& S, const int32_t* RUN, int32
 }
 
 __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
+    pdl_enter();
     extern __shared__ __align__(16) uint8_t plan_smem[];
     PlanSh& S = *reinterpret_cast<PlanSh*>(plan_smem);
     const Ctl& c = *d.ctl;
