@@ -34,6 +34,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
            "-I", str(PKG.parent / "include"), "-o", str(tmp), str(SRC), "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
+    # development builds only (e.g. -DCO_MBAR_WATCHDOG); never set for the product
+    cmd[1:1] = os.environ.get("CACHEOPT_NVCC_EXTRA", "").split()
     subprocess.run(cmd, check=True)
     tmp.replace(OUT)
     return OUT

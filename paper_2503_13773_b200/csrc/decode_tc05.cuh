@@ -24,11 +24,11 @@
 // the tile stream alternates between the groups' items, so one group's
 // softmax overlaps the other's and the MMAs of both (FA4-style).
 //
-// Roles (384 threads): warps 0 / 3 = TMA producers of the K / V rings (lanes
+// Roles (416 threads): warps 0 / 3 = TMA producers of the K / V rings (lanes
 // 0..7 issue the boxes of one 16-position group each), warp 1 = TMEM owner +
-// MMA issuer (lane 0), warp 2 = query producer (the synthetic q of each
+// S = K Q^T issuer (lane 0), warp 2 = query producer (the synthetic q of each
 // group's next item, double buffered), warps 4..7 = softmax group 0, 8..11 =
-// group 1.
+// group 1, warp 12 = O = V^T P issuer (lane 0).
 #pragma once
 #include <cuda.h>
 #include "decode_common.cuh"
@@ -39,7 +39,9 @@ constexpr int T5_TILE = 128;                          // positions per tile (MMA
 constexpr int T5_NH = 16;                             // MMA N: query heads per KV head, padded
 constexpr int T5_STAGES = 3;
 constexpr int T5_GROUPS = 2;                          // softmax groups
-constexpr int T5_THREADS = 128 + T5_GROUPS * 128;
+constexpr int T5_SM_WARP0 = 4;                        // first softmax warp
+constexpr int T5_O_WARP = T5_SM_WARP0 + 4 * T5_GROUPS;  // the PV (O) issuer
+constexpr int T5_THREADS = 32 * (T5_O_WARP + 1);
 constexpr int T5_KV_BYTES = T5_TILE * 128 * 2;        // one K (or V) tile: 32 KB
 constexpr int T5_STAGE_BYTES = 2 * T5_KV_BYTES;       // K + V
 constexpr int T5_QP_BYTES = T5_NH * 128 * 2;          // one Q or P operand: 4 KB
@@ -301,31 +303,10 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
-            constexpr uint32_t ID_S = t5_idesc(false), ID_O = t5_idesc(true);
+            constexpr uint32_t ID_S = t5_idesc(false);
             T5Cursor cur;
             cur.init(d, x, dc, nitems);
             uint32_t T = 0, Tg0 = 0, Tg1 = 0, Ig0 = 0, Ig1 = 0;
-            int pg1 = -1, pg2 = -1;  // the last two stream tiles whose O is pending
-            uint32_t ptg1 = 0, pst1 = 0, ptg2 = 0, pst2 = 0;
-            auto issue_o = [&](int og, uint32_t tg, uint32_t st, uint32_t tv) {
-                const int ob = (int)(tg & 1);
-                mbar_wait(PF(og, ob), (tg >> 1) & 1);
-                mbar_wait(OE(og, ob), ((tg >> 1) & 1) ^ 1);
-                mbar_wait(FULL(1, (int)st), (tv / T5_STAGES) & 1);
-                t5_fence_after();
-                const uint32_t vb = sb + st * T5_STAGE_BYTES + T5_KV_BYTES;
-                const uint32_t pb = sb + PBUF(og, ob);
-#pragma unroll
-                for (int kk = 0; kk < T5_TILE / 16; kk++) {
-                    // A = V^T: M = head dim (MN-major, 64-dim halves 16 KB apart),
-                    // K = 16 positions = 2048 B of rows
-                    const uint64_t a = t5_desc(vb + kk * 2048, T5_KV_BYTES / 2, 1024);
-                    const uint64_t b = t5_desc(pb + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024);
-                    t5_mma(tmem + 64 + 32 * og + 16 * ob, a, b, ID_O, kk > 0 ? 1u : 0u);
-                }
-                t5_commit(OF(og, ob));
-                t5_commit(EMPTY(1, (int)st));
-            };
             while (cur.next(nitems)) {
                 const int g = cur.g;
                 const int s = (int)(T % T5_STAGES);
@@ -347,18 +328,47 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
                 t5_commit(SF(g, sbuf));
                 t5_commit(EMPTY(0, s));
                 if (last) t5_commit(QE(g, qb));
-                // O of the tile two stream steps back (the same group's
-                // previous tile when the groups alternate): this group's next
-                // S is already in flight when its softmax finishes
-                if (pg2 >= 0) issue_o(pg2, ptg2, pst2, T - 2);
-                pg2 = pg1; ptg2 = ptg1; pst2 = pst1;
-                pg1 = g; ptg1 = tg; pst1 = (uint32_t)s;
                 if (g) { Tg1++; Ig1 += last; } else { Tg0++; Ig0 += last; }
                 T++;
                 cur.advance(d, x, dc, nitems);
             }
-            if (pg2 >= 0) issue_o(pg2, ptg2, pst2, T - 2);
-            if (pg1 >= 0) issue_o(pg1, ptg1, pst1, T - 1);
+        }
+        __syncwarp();
+    } else if (warp == T5_O_WARP) {
+        // ---------------- PV issuer: O = V^T P per tile, in stream order ----------------
+        // A thread of its own so that a group's O never waits behind the
+        // next S (and its K load) of the issuer above: a softmax group folds
+        // its previous tile's O right after producing this tile's P.
+        if (lane == 0) {
+            constexpr uint32_t ID_O = t5_idesc(true);
+            T5Cursor cur;
+            cur.init(d, x, dc, nitems);
+            uint32_t T = 0, Tg0 = 0, Tg1 = 0;
+            while (cur.next(nitems)) {
+                const int og = cur.g;
+                const uint32_t tg = og ? Tg1 : Tg0;
+                const int st = (int)(T % T5_STAGES);
+                const int ob = (int)(tg & 1);
+                mbar_wait(PF(og, ob), (tg >> 1) & 1);
+                mbar_wait(OE(og, ob), ((tg >> 1) & 1) ^ 1);
+                mbar_wait(FULL(1, st), (T / T5_STAGES) & 1);
+                t5_fence_after();
+                const uint32_t vb = sb + (uint32_t)st * T5_STAGE_BYTES + T5_KV_BYTES;
+                const uint32_t pb = sb + PBUF(og, ob);
+#pragma unroll
+                for (int kk = 0; kk < T5_TILE / 16; kk++) {
+                    // A = V^T: M = head dim (MN-major, 64-dim halves 16 KB apart),
+                    // K = 16 positions = 2048 B of rows
+                    const uint64_t a = t5_desc(vb + kk * 2048, T5_KV_BYTES / 2, 1024);
+                    const uint64_t b = t5_desc(pb + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024);
+                    t5_mma(tmem + 64 + 32 * og + 16 * ob, a, b, ID_O, kk > 0 ? 1u : 0u);
+                }
+                t5_commit(OF(og, ob));
+                t5_commit(EMPTY(1, st));
+                if (og) Tg1++; else Tg0++;
+                T++;
+                cur.advance(d, x, dc, nitems);
+            }
         }
         __syncwarp();
     } else if (warp == 2) {
@@ -395,9 +405,9 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
             }
             cur.advance(d, x, dc, nitems);
         }
-    } else if (warp >= 4) {
+    } else if (warp >= T5_SM_WARP0 && warp < T5_O_WARP) {
         // ---------------- softmax + output (group g) ----------------
-        const int g = (warp - 4) >> 2, q4 = warp & 3;
+        const int g = (warp - T5_SM_WARP0) >> 2, q4 = warp & 3;
         const int r = q4 * 32 + lane;  // TMEM lane: tile position (S) / head dim (O)
         const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
         float* red = reinterpret_cast<float*>(base + T5_OFF_RED) + g * T5_RED_FLOATS;

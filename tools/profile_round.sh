@@ -21,4 +21,8 @@ WARM=3000 timeout 900 ncu --set full --clock-control none --import-source on -k 
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:"k_data" -c 1 \
     -o $O/prof_k_data python tools/decode_once.py swap > $O/ncu_swap.log 2>&1
 fi
+python tools/ncu_summary.py $O/prof_*.ncu-rep > $O/ncu_full_summary.csv 2>&1
+python tools/launch_summary.py $O/launches.csv > $O/launches_summary.csv 2>&1
+# gpurun returns at most 64 MiB: keep the summaries, drop the big reports
+find $O -name '*.ncu-rep' -size +6M -delete
 ls -la $O
