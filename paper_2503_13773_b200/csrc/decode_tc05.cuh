@@ -37,19 +37,28 @@ namespace co {
 
 constexpr int T5_TILE = 128;                          // positions per tile (MMA M)
 constexpr int T5_NH = 16;                             // MMA N: query heads per KV head, padded
-constexpr int T5_STAGES = 3;
+#ifndef T5_KS_DEF
+#define T5_KS_DEF 3
+#endif
+#ifndef T5_VS_DEF
+#define T5_VS_DEF 3
+#endif
+// K and V rings of their own depth (a K slot frees as soon as its S product
+// completes, a V slot only after the softmax and the O product); measured on
+// config 5: 3/3 = 84.9 %, 2/4 = 84.6 %, 1/5 = 64.9 % of HBM
+constexpr int T5_KS = T5_KS_DEF;
+constexpr int T5_VS = T5_VS_DEF;
 constexpr int T5_GROUPS = 2;                          // softmax groups
 constexpr int T5_SM_WARP0 = 4;                        // first softmax warp
 constexpr int T5_O_WARP = T5_SM_WARP0 + 4 * T5_GROUPS;  // the PV (O) issuer
 constexpr int T5_THREADS = 32 * (T5_O_WARP + 1);
 constexpr int T5_KV_BYTES = T5_TILE * 128 * 2;        // one K (or V) tile: 32 KB
-constexpr int T5_STAGE_BYTES = 2 * T5_KV_BYTES;       // K + V
 constexpr int T5_QP_BYTES = T5_NH * 128 * 2;          // one Q or P operand: 4 KB
-constexpr int T5_OFF_Q = T5_STAGES * T5_STAGE_BYTES;  // Q [group][2]
+constexpr int T5_OFF_Q = (T5_KS + T5_VS) * T5_KV_BYTES;  // Q [group][2]
 constexpr int T5_OFF_P = T5_OFF_Q + 2 * T5_GROUPS * T5_QP_BYTES;  // P [group][2]
 constexpr int T5_OFF_BAR = T5_OFF_P + 2 * T5_GROUPS * T5_QP_BYTES;
 constexpr int T5_GBAR = 14;                           // per group: q, s, o full/empty + p full, x2
-constexpr int T5_NBAR = 4 * T5_STAGES + T5_GROUPS * T5_GBAR;  // K full/empty, V full/empty + groups
+constexpr int T5_NBAR = 2 * (T5_KS + T5_VS) + T5_GROUPS * T5_GBAR;  // K full/empty, V full/empty + groups
 constexpr int T5_OFF_RED = (T5_OFF_BAR + T5_NBAR * 8 + 8 + 15) & ~15;  // + TMEM base slot, 16 B aligned
 constexpr int T5_RED_FLOATS = 2 * T5_NH * 4 + 4 * T5_NH;  // max [2][16 heads][4 warps], l [4 warps][16]
 constexpr int T5_SMEM = T5_OFF_RED + T5_GROUPS * T5_RED_FLOATS * 4 + 1024;  // + alignment slack
@@ -216,9 +225,10 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
     const uint32_t bar0 = sb + T5_OFF_BAR;
     // K and V rings are separate: a K slot is free again as soon as its S
     // product completes, a V slot only after the O product (after softmax)
-    auto FULL = [&](int kv, int s) { return bar0 + 8u * (2 * kv * T5_STAGES + s); };
-    auto EMPTY = [&](int kv, int s) { return bar0 + 8u * (2 * kv * T5_STAGES + T5_STAGES + s); };
-    auto GB = [&](int g, int k, int b) { return bar0 + 8u * (4 * T5_STAGES + g * T5_GBAR + 2 * k + b); };
+    // barriers: K full[KS], K empty[KS], V full[VS], V empty[VS], then the groups'
+    auto FULL = [&](int kv, int s) { return bar0 + 8u * (kv ? 2 * T5_KS + s : s); };
+    auto EMPTY = [&](int kv, int s) { return bar0 + 8u * (kv ? 2 * T5_KS + T5_VS + s : T5_KS + s); };
+    auto GB = [&](int g, int k, int b) { return bar0 + 8u * (2 * (T5_KS + T5_VS) + g * T5_GBAR + 2 * k + b); };
     auto QF = [&](int g, int b) { return GB(g, 0, b); };
     auto QE = [&](int g, int b) { return GB(g, 1, b); };
     auto SF = [&](int g, int b) { return GB(g, 2, b); };
@@ -235,8 +245,8 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
     for (uint32_t o = threadIdx.x * 16; o < (uint32_t)T5_OFF_BAR; o += blockDim.x * 16)
         *reinterpret_cast<uint4*>(base + o) = make_uint4(0, 0, 0, 0);
     if (threadIdx.x == 0) {
-        for (int s = 0; s < T5_STAGES; s++)
-            for (int kv = 0; kv < 2; kv++) { mbar_init(FULL(kv, s), 1); mbar_init(EMPTY(kv, s), 1); }
+        for (int s = 0; s < T5_KS; s++) { mbar_init(FULL(0, s), 1); mbar_init(EMPTY(0, s), 1); }
+        for (int s = 0; s < T5_VS; s++) { mbar_init(FULL(1, s), 1); mbar_init(EMPTY(1, s), 1); }
         for (int g = 0; g < T5_GROUPS; g++)
             for (int b = 0; b < 2; b++) {
                 mbar_init(QF(g, b), 1); mbar_init(QE(g, b), 1);
@@ -271,7 +281,8 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
         uint32_t T = 0;
         while (cur.next(nitems)) {
             const DecItem& w = cur.w();
-            const int s = (int)(T % T5_STAGES);
+            const uint32_t NS = kv ? T5_VS : T5_KS;
+            const int s = (int)(T % NS);
             const int32_t P0 = w.nt0 + cur.t() * T5_TILE;
             int32_t ngrp = (w.pos_hi - P0 + 15) / 16;
             if (ngrp > T5_TILE / 16) ngrp = T5_TILE / 16;
@@ -287,12 +298,12 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
                 rr = (page * x.rows + row) * bs + pos % bs;
             }
             if (lane == 0) {
-                mbar_wait(EMPTY(kv, s), ((T / T5_STAGES) & 1) ^ 1);
+                mbar_wait(EMPTY(kv, s), ((T / NS) & 1) ^ 1);
                 mbar_expect(FULL(kv, s), (uint32_t)ngrp * 16 * 128 * 2);
             }
             __syncwarp();
             if (mine) {
-                const uint32_t dst = sb + (uint32_t)s * T5_STAGE_BYTES + (uint32_t)kv * T5_KV_BYTES + (uint32_t)off * 128;
+                const uint32_t dst = sb + (uint32_t)((kv ? T5_KS : 0) + s) * T5_KV_BYTES + (uint32_t)off * 128;
                 tma_2d(dst, &kvmap, 0, rr, FULL(kv, s));
                 tma_2d(dst + T5_KV_BYTES / 2, &kvmap, 64, rr, FULL(kv, s));
             }
@@ -309,15 +320,15 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
             uint32_t T = 0, Tg0 = 0, Tg1 = 0, Ig0 = 0, Ig1 = 0;
             while (cur.next(nitems)) {
                 const int g = cur.g;
-                const int s = (int)(T % T5_STAGES);
+                const int s = (int)(T % T5_KS);
                 const uint32_t tg = g ? Tg1 : Tg0, ig = g ? Ig1 : Ig0;
                 const int sbuf = (int)(tg & 1), qb = (int)(ig & 1);
                 const bool first = cur.t() == 0, last = cur.t() == cur.nt() - 1;
                 if (first) mbar_wait(QF(g, qb), (ig >> 1) & 1);
-                mbar_wait(FULL(0, s), (T / T5_STAGES) & 1);
+                mbar_wait(FULL(0, s), (T / T5_KS) & 1);
                 mbar_wait(SE(g, sbuf), ((tg >> 1) & 1) ^ 1);
                 t5_fence_after();
-                const uint32_t kb = sb + (uint32_t)s * T5_STAGE_BYTES;
+                const uint32_t kb = sb + (uint32_t)s * T5_KV_BYTES;
                 const uint32_t qbase = sb + QBUF(g, qb);
 #pragma unroll
                 for (int kk = 0; kk < 8; kk++) {
@@ -347,13 +358,13 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
             while (cur.next(nitems)) {
                 const int og = cur.g;
                 const uint32_t tg = og ? Tg1 : Tg0;
-                const int st = (int)(T % T5_STAGES);
+                const int st = (int)(T % T5_VS);
                 const int ob = (int)(tg & 1);
                 mbar_wait(PF(og, ob), (tg >> 1) & 1);
                 mbar_wait(OE(og, ob), ((tg >> 1) & 1) ^ 1);
-                mbar_wait(FULL(1, st), (T / T5_STAGES) & 1);
+                mbar_wait(FULL(1, st), (T / T5_VS) & 1);
                 t5_fence_after();
-                const uint32_t vb = sb + (uint32_t)st * T5_STAGE_BYTES + T5_KV_BYTES;
+                const uint32_t vb = sb + (uint32_t)(T5_KS + st) * T5_KV_BYTES;
                 const uint32_t pb = sb + PBUF(og, ob);
 #pragma unroll
                 for (int kk = 0; kk < T5_TILE / 16; kk++) {
