@@ -262,7 +262,9 @@ int co_host_link_gbs(int64_t bytes, double* d2h, double* h2d);
 int co_check_invariants(co_engine* eng);
 
 /* Device time of the last co_run/co_step launch sequence (CUDA events on
- * the engine stream), milliseconds. */
+ * the engine stream), milliseconds.  co_step / co_step_result record their
+ * per-step events only after the first call of this function (the events
+ * cost a few microseconds of every step otherwise). */
 int co_last_device_ms(co_engine* eng, double* ms);
 /* development aid: phase timestamps (ns) of the planner/apply kernels of
  * the last step; enable = 1 allocates the stamp buffer */

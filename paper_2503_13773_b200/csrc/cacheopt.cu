@@ -111,6 +111,7 @@ struct co_engine {
     int32_t graph_k = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double last_ms = 0.0;
+    bool timing = false;  // per-step events for co_last_device_ms (on after its first call)
     int grid = 1;
     int64_t n = 0;
     int64_t tok_total = 0;
@@ -652,9 +653,27 @@ static int ensure_step_graph(co_engine* E) {
     int r;
     CK(cudaStreamBeginCapture(E->stream, cudaStreamCaptureModeThreadLocal));
     if ((r = launch_step(E, 0))) { cudaStreamEndCapture(E->stream, &g); return r; }
+    // the control block comes back inside the graph: one launch + one sync per step
+    cudaMemcpyAsync(E->h_ctl, E->d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, E->stream);
     CK(cudaStreamEndCapture(E->stream, &g));
     CK(cudaGraphInstantiate(&E->graph1, g, 0));
     cudaGraphDestroy(g);
+    return CO_OK;
+}
+
+// one step through graph1 (which ends with the control-block readback);
+// per-step device timing only once co_last_device_ms has been asked for
+static int launch_step1(co_engine* E) {
+    if (E->timing) CK(cudaEventRecord(E->ev0, E->stream));
+    CK(cudaGraphLaunch(E->graph1, E->stream));
+    if (E->comm) E->reduce_calls += 1;
+    if (E->timing) CK(cudaEventRecord(E->ev1, E->stream));
+    CK(cudaStreamSynchronize(E->stream));
+    if (E->timing) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, E->ev0, E->ev1);
+        E->last_ms = ms;
+    }
     return CO_OK;
 }
 
@@ -676,14 +695,7 @@ int co_step_result(co_engine* E, int32_t* result, int32_t* members, int64_t max_
     if ((r = predrain(E))) return r;
     const int32_t* res = static_cast<const int32_t*>(E->result_host);
     for (int attempt = 0; attempt < 3; attempt++) {
-        CK(cudaEventRecord(E->ev0, E->stream));
-        CK(cudaGraphLaunch(E->graph1, E->stream));
-        if (E->comm) E->reduce_calls += 1;
-        CK(cudaEventRecord(E->ev1, E->stream));
-        if ((r = sync_ctl(E))) return r;
-        float ms = 0;
-        cudaEventElapsedTime(&ms, E->ev0, E->ev1);
-        E->last_ms = ms;
+        if ((r = launch_step1(E))) return r;
         if ((r = check_device_error(E))) return r;
         if (E->h_ctl->paused) {
             if (E->comm) return fail(CO_EDEVICE, "step paused with a communicator attached");
@@ -707,14 +719,7 @@ int co_step(co_engine* E, int32_t* result) {
     if (r) return r;
     if ((r = predrain(E))) return r;
     for (int attempt = 0; attempt < 3; attempt++) {
-        CK(cudaEventRecord(E->ev0, E->stream));
-        CK(cudaGraphLaunch(E->graph1, E->stream));
-        if (E->comm) E->reduce_calls += 1;
-        CK(cudaEventRecord(E->ev1, E->stream));
-        if ((r = sync_ctl(E))) return r;
-        float ms = 0;
-        cudaEventElapsedTime(&ms, E->ev0, E->ev1);
-        E->last_ms = ms;
+        if ((r = launch_step1(E))) return r;
         if ((r = check_device_error(E))) return r;
         if (E->h_ctl->paused) {
             if (E->comm) return fail(CO_EDEVICE, "step paused with a communicator attached");
@@ -986,6 +991,7 @@ int co_check_invariants(co_engine* E) {
 int co_last_device_ms(co_engine* E, double* ms) {
     if (!E || !ms) return fail(CO_EINVAL, "null argument");
     *ms = E->last_ms;
+    E->timing = true;
     return CO_OK;
 }
 

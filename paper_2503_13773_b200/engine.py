@@ -437,12 +437,22 @@ class Engine:
         if self._resbuf is None:
             self._resbuf = np.empty(2 * (3 * self._n + 64), dtype=np.int32)
             self._rid_np = np.array(self._rid, dtype=np.int64)
-        r, n, end = C.c_int32(), C.c_int64(), C.c_int64()
-        self._dirty()
-        N.check(self._lib.co_step_result(self._h, C.byref(r), _ptr(self._resbuf, C.c_int32),
-                                         len(self._resbuf) // 2, C.byref(n), C.byref(end)), "co_step_result")
-        m = self._resbuf[:2 * n.value].reshape(-1, 2)
-        out = np.stack([self._rid_np[m[:, 0]], m[:, 1]], axis=1) if n.value else np.zeros((0, 2), np.int64)
+            self._sr_out = (C.c_int32(), C.c_int64(), C.c_int64())
+            r, n, end = self._sr_out
+            self._sr_args = (self._h, C.byref(r), _ptr(self._resbuf, C.c_int32), len(self._resbuf) // 2,
+                             C.byref(n), C.byref(end))
+        r, n, end = self._sr_out
+        self._cache.clear()
+        self._sc = None
+        rc = self._lib.co_step_result(*self._sr_args)
+        if rc:
+            N.check(rc, "co_step_result")
+        k = n.value
+        out = np.empty((k, 2), dtype=np.int64)
+        if k:
+            m = self._resbuf[:2 * k]
+            out[:, 0] = self._rid_np[m[0::2]]
+            out[:, 1] = m[1::2]
         return bool(r.value), out, int(end.value)
 
     def run_steps(self, max_steps: int = 0, steps_per_launch: Optional[int] = None) -> int:
