@@ -23,6 +23,13 @@ timeout 400 ncu --set full --clock-control none --import-source on -k regex:"k_d
 fi
 python tools/ncu_summary.py $O/prof_*.ncu-rep > $O/ncu_full_summary.csv 2>&1
 python tools/launch_summary.py $O/launches.csv > $O/launches_summary.csv 2>&1
+for r in $O/prof_*.ncu-rep; do
+  ncu -i $r --page details --csv > ${r%.ncu-rep}_details.csv 2>/dev/null
+done
+timeout 300 ncu --set full --clock-control none -k regex:"k_arrivals|k_orbit_spec|k_zig_local" -c 3 \
+    -o $O/prof_tracegen python tools/tracegen_probe.py > $O/ncu_tracegen.log 2>&1
+ncu -i $O/prof_tracegen.ncu-rep --page details --csv > $O/prof_tracegen_details.csv 2>/dev/null
+python tools/ncu_summary.py $O/prof_tracegen.ncu-rep > $O/ncu_tracegen_summary.csv 2>&1
 # gpurun returns at most 64 MiB: keep the summaries, drop the big reports
 find $O -name '*.ncu-rep' -size +6M -delete
 ls -la $O
