@@ -226,7 +226,7 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
             } else {
                 k_decode<<<E->sms * 8, DEC_T, 0, s>>>(d, d.dp, d.dctl);
             }
-            k_decode_reduce<<<E->sms * 8, 128, 0, s>>>(d, d.dp, d.dctl);
+            k_decode_reduce<<<E->sms * 8, RED_T, 0, s>>>(d, d.dp, d.dctl);
         }
         if (ev) mark(ev[8], s);
     } else if (ev) {

@@ -419,30 +419,84 @@ __global__ void __launch_bounds__(DEC_T) k_decode(Dev d, DataCfg x, DataCtl* dc)
 }
 
 // combine the splits of every (member, layer, q head)
-__global__ void k_decode_reduce(Dev d, DataCfg x, DataCtl* dc) {
+// Split-KV combine: one work unit = (member, layer, KV head), all G query
+// heads of it at once, so every split's partial rows (G x (D + 2) floats) are
+// read contiguously.  The per-split maxima and sums go through shared memory
+// first; then each thread folds its outputs over the splits with independent
+// loads (the old one-block-per-query-head loop was two dependent load chains
+// per split: 0.2 ms per step at 0.8 TB/s).
+constexpr int RED_T = 256, RED_CAP = 1024;  // threads; split x head slots held in shared memory
+__global__ void __launch_bounds__(RED_T) k_decode_reduce(Dev d, DataCfg x, DataCtl* dc) {
     const Ctl& c = *d.ctl;
     if (!c.active || !x.decode_on || !dc->decode_enabled) return;
-    const int G = x.Hq / x.Hkv, D = x.D;
+    __shared__ float sm[RED_CAP], sl[RED_CAP];  // [split][head]: m, then the scale; l
+    __shared__ float sM[16], sL[16];
+    const int G = x.Hq / x.Hkv, D = x.D, W = D + 2;
     const int32_t nm = dc->n_dec;
-    const int64_t total = (int64_t)nm * x.L * x.Hq;
+    const int64_t total = (int64_t)nm * x.L * x.Hkv;
     for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
-        const int32_t m = (int32_t)(w / ((int64_t)x.L * x.Hq));
-        const int32_t lq = (int32_t)(w % ((int64_t)x.L * x.Hq));
-        const int32_t layer = lq / x.Hq, qh = lq % x.Hq;
-        const int32_t kh = qh / G, g = qh % G;
+        const int32_t m = (int32_t)(w / ((int64_t)x.L * x.Hkv));
+        const int32_t lk = (int32_t)(w % ((int64_t)x.L * x.Hkv));
+        const int32_t layer = lk / x.Hkv, kh = lk % x.Hkv;
         const int32_t ctx = x.dec_ctx[m];
         const int32_t nsplit = (ctx + x.split - 1) / x.split;
         const int64_t base_item = x.dec_item_off[m] + (int64_t)(layer * x.Hkv + kh) * nsplit;
-        float M = -INFINITY;
-        for (int s = 0; s < nsplit; s++) M = fmaxf(M, x.dec_part[((base_item + s) * G + g) * (D + 2) + D]);
-        float Lsum = 0.f, acc = 0.f;
-        for (int s = 0; s < nsplit; s++) {
-            const float* p = x.dec_part + ((base_item + s) * G + g) * (D + 2);
-            float sc = __expf(p[D] - M);
-            Lsum += p[D + 1] * sc;
-            acc += p[threadIdx.x] * sc;
+        const float* part = x.dec_part + base_item * G * W;  // [split][head][W]
+        float* out = x.dec_out + (((int64_t)m * x.L + layer) * x.Hq + (int64_t)kh * G) * D;
+        const int ns = nsplit * G;
+        if (ns <= RED_CAP && G <= 16) {
+            for (int k = threadIdx.x; k < ns; k += RED_T) {
+                sm[k] = part[(int64_t)k * W + D];
+                sl[k] = part[(int64_t)k * W + D + 1];
+            }
+            __syncthreads();
+            if (threadIdx.x < G) {
+                const int g = threadIdx.x;
+                float M = -INFINITY;
+                for (int s2 = 0; s2 < nsplit; s2++) M = fmaxf(M, sm[s2 * G + g]);
+                float L = 0.f;
+                for (int s2 = 0; s2 < nsplit; s2++) {
+                    const float sc = __expf(sm[s2 * G + g] - M);
+                    sm[s2 * G + g] = sc;
+                    L += sl[s2 * G + g] * sc;
+                }
+                sL[g] = L;
+                sM[g] = M;
+            }
+            __syncthreads();
+            for (int o = threadIdx.x; o < G * D; o += RED_T) {
+                const int g = o / D, j = o - g * D;
+                const float* p = part + (int64_t)g * W + j;
+                float acc = 0.f;
+                int s2 = 0;
+                for (; s2 + 4 <= nsplit; s2 += 4) {
+                    const float a0 = p[(int64_t)(s2 + 0) * G * W], a1 = p[(int64_t)(s2 + 1) * G * W];
+                    const float a2 = p[(int64_t)(s2 + 2) * G * W], a3 = p[(int64_t)(s2 + 3) * G * W];
+                    acc += a0 * sm[(s2 + 0) * G + g];
+                    acc += a1 * sm[(s2 + 1) * G + g];
+                    acc += a2 * sm[(s2 + 2) * G + g];
+                    acc += a3 * sm[(s2 + 3) * G + g];
+                }
+                for (; s2 < nsplit; s2++) acc += p[(int64_t)s2 * G * W] * sm[s2 * G + g];
+                out[o] = acc / sL[g];
+            }
+            __syncthreads();
+        } else {
+            // more splits x heads than shared memory holds: per output, two passes
+            for (int o = threadIdx.x; o < G * D; o += RED_T) {
+                const int g = o / D, j = o - g * D;
+                float M = -INFINITY;
+                for (int s2 = 0; s2 < nsplit; s2++) M = fmaxf(M, part[((int64_t)s2 * G + g) * W + D]);
+                float L = 0.f, acc = 0.f;
+                for (int s2 = 0; s2 < nsplit; s2++) {
+                    const float* q = part + ((int64_t)s2 * G + g) * W;
+                    const float sc = __expf(q[D] - M);
+                    L += q[D + 1] * sc;
+                    acc += q[j] * sc;
+                }
+                out[o] = acc / L;
+            }
         }
-        x.dec_out[(((int64_t)m * x.L + layer) * x.Hq + qh) * D + threadIdx.x] = acc / Lsum;
     }
 }
 
