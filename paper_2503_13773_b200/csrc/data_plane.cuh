@@ -419,22 +419,24 @@ __global__ void __launch_bounds__(DEC_T) k_decode(Dev d, DataCfg x, DataCtl* dc)
 }
 
 // combine the splits of every (member, layer, q head)
-// Split-KV combine: one work unit = (member, layer, KV head), all G query
-// heads of it at once, so every split's partial rows (G x (D + 2) floats) are
-// read contiguously.  The per-split maxima and sums go through shared memory
-// first; then each thread folds its outputs over the splits with independent
-// loads (the old one-block-per-query-head loop was two dependent load chains
-// per split: 0.2 ms per step at 0.8 TB/s).
-constexpr int RED_T = 256, RED_CAP = 1024;  // threads; split x head slots held in shared memory
+// Split-KV combine: one WARP per work unit = (member, layer, KV head), all G
+// query heads of it at once, so a split's partial rows (G x (D + 2) floats)
+// are read contiguously and an SM keeps dozens of units in flight (the
+// combine is latency-bound: a few KB per unit).  The per-split maxima go
+// through the warp's shared-memory slice; each lane then folds four outputs
+// at a time over the splits with independent loads.
+constexpr int RED_T = 256, RED_W = RED_T / 32, RED_CAP = 128;  // split x head slots per warp
 __global__ void __launch_bounds__(RED_T) k_decode_reduce(Dev d, DataCfg x, DataCtl* dc) {
     const Ctl& c = *d.ctl;
     if (!c.active || !x.decode_on || !dc->decode_enabled) return;
-    __shared__ float sm[RED_CAP], sl[RED_CAP];  // [split][head]: m, then the scale; l
-    __shared__ float sM[16], sL[16];
+    __shared__ float ssc[RED_W][RED_CAP];  // [split][head]: m, then the scale
+    __shared__ float sL[RED_W][16];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = x.Hq / x.Hkv, D = x.D, W = D + 2;
     const int32_t nm = dc->n_dec;
     const int64_t total = (int64_t)nm * x.L * x.Hkv;
-    for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
+    float* sc = ssc[wid];
+    for (int64_t w = (int64_t)blockIdx.x * RED_W + wid; w < total; w += (int64_t)gridDim.x * RED_W) {
         const int32_t m = (int32_t)(w / ((int64_t)x.L * x.Hkv));
         const int32_t lk = (int32_t)(w % ((int64_t)x.L * x.Hkv));
         const int32_t layer = lk / x.Hkv, kh = lk % x.Hkv;
@@ -445,54 +447,61 @@ __global__ void __launch_bounds__(RED_T) k_decode_reduce(Dev d, DataCfg x, DataC
         float* out = x.dec_out + (((int64_t)m * x.L + layer) * x.Hq + (int64_t)kh * G) * D;
         const int ns = nsplit * G;
         if (ns <= RED_CAP && G <= 16) {
-            for (int k = threadIdx.x; k < ns; k += RED_T) {
-                sm[k] = part[(int64_t)k * W + D];
-                sl[k] = part[(int64_t)k * W + D + 1];
-            }
-            __syncthreads();
-            if (threadIdx.x < G) {
-                const int g = threadIdx.x;
+            for (int k = lane; k < ns; k += 32) sc[k] = part[(int64_t)k * W + D];
+            __syncwarp();
+            if (lane < G) {
                 float M = -INFINITY;
-                for (int s2 = 0; s2 < nsplit; s2++) M = fmaxf(M, sm[s2 * G + g]);
+                for (int s2 = 0; s2 < nsplit; s2++) M = fmaxf(M, sc[s2 * G + lane]);
                 float L = 0.f;
                 for (int s2 = 0; s2 < nsplit; s2++) {
-                    const float sc = __expf(sm[s2 * G + g] - M);
-                    sm[s2 * G + g] = sc;
-                    L += sl[s2 * G + g] * sc;
+                    const float e = __expf(sc[s2 * G + lane] - M);
+                    sc[s2 * G + lane] = e;
+                    L += part[((int64_t)s2 * G + lane) * W + D + 1] * e;
                 }
-                sL[g] = L;
-                sM[g] = M;
+                sL[wid][lane] = L;
             }
-            __syncthreads();
-            for (int o = threadIdx.x; o < G * D; o += RED_T) {
-                const int g = o / D, j = o - g * D;
-                const float* p = part + (int64_t)g * W + j;
-                float acc = 0.f;
-                int s2 = 0;
-                for (; s2 + 4 <= nsplit; s2 += 4) {
-                    const float a0 = p[(int64_t)(s2 + 0) * G * W], a1 = p[(int64_t)(s2 + 1) * G * W];
-                    const float a2 = p[(int64_t)(s2 + 2) * G * W], a3 = p[(int64_t)(s2 + 3) * G * W];
-                    acc += a0 * sm[(s2 + 0) * G + g];
-                    acc += a1 * sm[(s2 + 1) * G + g];
-                    acc += a2 * sm[(s2 + 2) * G + g];
-                    acc += a3 * sm[(s2 + 3) * G + g];
+            __syncwarp();
+            const int GD = G * D;
+            const int64_t SW = (int64_t)G * W;  // floats per split
+            for (int o0 = lane; o0 < GD; o0 += 128) {
+                // the divisions once per output, not per split
+                const float* pp[4];
+                int gg[4];
+                bool ok[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int o = o0 + 32 * u;
+                    ok[u] = o < GD;
+                    const int g = ok[u] ? o / D : 0;
+                    gg[u] = g;
+                    pp[u] = part + (int64_t)g * W + (ok[u] ? o - g * D : 0);
                 }
-                for (; s2 < nsplit; s2++) acc += p[(int64_t)s2 * G * W] * sm[s2 * G + g];
-                out[o] = acc / sL[g];
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                for (int s2 = 0; s2 < nsplit; s2++) {
+                    float v[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) v[u] = ok[u] ? pp[u][s2 * SW] : 0.f;
+                    const float* scs = sc + s2 * G;
+#pragma unroll
+                    for (int u = 0; u < 4; u++) acc[u] += v[u] * scs[gg[u]];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (ok[u]) out[o0 + 32 * u] = acc[u] / sL[wid][gg[u]];
             }
-            __syncthreads();
+            __syncwarp();
         } else {
-            // more splits x heads than shared memory holds: per output, two passes
-            for (int o = threadIdx.x; o < G * D; o += RED_T) {
+            // more splits x heads than the warp's slice holds: per output, two passes
+            for (int o = lane; o < G * D; o += 32) {
                 const int g = o / D, j = o - g * D;
                 float M = -INFINITY;
                 for (int s2 = 0; s2 < nsplit; s2++) M = fmaxf(M, part[((int64_t)s2 * G + g) * W + D]);
                 float L = 0.f, acc = 0.f;
                 for (int s2 = 0; s2 < nsplit; s2++) {
                     const float* q = part + ((int64_t)s2 * G + g) * W;
-                    const float sc = __expf(q[D] - M);
-                    L += q[D + 1] * sc;
-                    acc += q[j] * sc;
+                    const float e = __expf(q[D] - M);
+                    L += q[D + 1] * e;
+                    acc += q[j] * e;
                 }
                 out[o] = acc / L;
             }
