@@ -461,33 +461,71 @@ __global__ void __launch_bounds__(RED_T) k_decode_reduce(Dev d, DataCfg x, DataC
                 sL[wid][lane] = L;
             }
             __syncwarp();
-            const int GD = G * D;
             const int64_t SW = (int64_t)G * W;  // floats per split
-            for (int o0 = lane; o0 < GD; o0 += 128) {
-                // the divisions once per output, not per split
-                const float* pp[4];
-                int gg[4];
-                bool ok[4];
+            if ((D & 1) == 0) {
+                // float2 lanes: W = D + 2 is even, so every (split, head) row is 8-B aligned
+                const int H2 = D >> 1, GD2 = G * H2;
+                for (int f0 = lane; f0 < GD2; f0 += 128) {
+                    const float2* pp[4];
+                    int gg[4];
+                    bool ok[4];
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const int o = o0 + 32 * u;
-                    ok[u] = o < GD;
-                    const int g = ok[u] ? o / D : 0;
-                    gg[u] = g;
-                    pp[u] = part + (int64_t)g * W + (ok[u] ? o - g * D : 0);
+                    for (int u = 0; u < 4; u++) {
+                        const int f = f0 + 32 * u;
+                        ok[u] = f < GD2;
+                        const int g = ok[u] ? f / H2 : 0;
+                        gg[u] = g;
+                        pp[u] = reinterpret_cast<const float2*>(part + (int64_t)g * W) + (ok[u] ? f - g * H2 : 0);
+                    }
+                    float2 acc[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) acc[u] = make_float2(0.f, 0.f);
+                    for (int s2 = 0; s2 < nsplit; s2++) {
+                        float2 v[4];
+#pragma unroll
+                        for (int u = 0; u < 4; u++) v[u] = ok[u] ? pp[u][s2 * (SW >> 1)] : make_float2(0.f, 0.f);
+                        const float* scs = sc + s2 * G;
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            const float e = scs[gg[u]];
+                            acc[u].x += v[u].x * e;
+                            acc[u].y += v[u].y * e;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; u++)
+                        if (ok[u]) {
+                            const float inv = sL[wid][gg[u]];
+                            reinterpret_cast<float2*>(out)[f0 + 32 * u] = make_float2(acc[u].x / inv, acc[u].y / inv);
+                        }
                 }
-                float acc[4] = {0.f, 0.f, 0.f, 0.f};
-                for (int s2 = 0; s2 < nsplit; s2++) {
-                    float v[4];
+            } else {
+                const int GD = G * D;
+                for (int o0 = lane; o0 < GD; o0 += 128) {
+                    const float* pp[4];
+                    int gg[4];
+                    bool ok[4];
 #pragma unroll
-                    for (int u = 0; u < 4; u++) v[u] = ok[u] ? pp[u][s2 * SW] : 0.f;
-                    const float* scs = sc + s2 * G;
+                    for (int u = 0; u < 4; u++) {
+                        const int o = o0 + 32 * u;
+                        ok[u] = o < GD;
+                        const int g = ok[u] ? o / D : 0;
+                        gg[u] = g;
+                        pp[u] = part + (int64_t)g * W + (ok[u] ? o - g * D : 0);
+                    }
+                    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                    for (int s2 = 0; s2 < nsplit; s2++) {
+                        float v[4];
 #pragma unroll
-                    for (int u = 0; u < 4; u++) acc[u] += v[u] * scs[gg[u]];
+                        for (int u = 0; u < 4; u++) v[u] = ok[u] ? pp[u][s2 * SW] : 0.f;
+                        const float* scs = sc + s2 * G;
+#pragma unroll
+                        for (int u = 0; u < 4; u++) acc[u] += v[u] * scs[gg[u]];
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; u++)
+                        if (ok[u]) out[o0 + 32 * u] = acc[u] / sL[wid][gg[u]];
                 }
-#pragma unroll
-                for (int u = 0; u < 4; u++)
-                    if (ok[u]) out[o0 + 32 * u] = acc[u] / sL[wid][gg[u]];
             }
             __syncwarp();
         } else {
