@@ -248,13 +248,13 @@ def swap_leg(dev):
             "kernel": "k_data (SM copy through mapped pinned host pages)"}
 
 
-def decode_leg(dev, warm_steps=6000, k=10):
+def decode_leg(dev, warm_steps=6000, k=10, split=512):
     """N3: paged decode over the engine's block tables, Llama-2-70B layout,
     long-output trace; decode enabled only for the k timed steps."""
     import ctypes as C
     import paper_2503_13773_b200 as P
     from paper_2503_13773_b200 import _native as N
-    kv = P.KVLayout.llama2_70b(host_swap_pages=4096, decode=True, decode_split=512)
+    kv = P.KVLayout.llama2_70b(host_swap_pages=4096, decode=True, decode_split=split)
     cfg = P.EngineConfig(capacity_tokens=65_536, reserved_blocks=8, sched=P.SchedulerConfig(small_block_b=16),
                          record_events=False)
     eng = P.Engine(long_output_trace(), cfg, device=dev, kv=kv)
