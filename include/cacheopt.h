@@ -198,6 +198,11 @@ int co_step(co_engine* eng, int32_t* result);
 int co_step_result(co_engine* eng, int32_t* result, int32_t* members, int64_t max_members,
                    int64_t* n_members, int64_t* iter_end_us);
 
+/* allocates step_result's mapped result buffer and instantiates the
+ * single-step graph without running a step (so a timed loop of
+ * co_step_result calls starts warm). */
+int co_prepare_step(co_engine* eng);
+
 /* engine.py:643-661 Engine.run() loop including the no-progress guard,
  * executed as CUDA-graph launches of `steps_per_launch` device steps.
  * max_steps <= 0 means until done.  *steps_done = step() calls made. */

@@ -172,6 +172,7 @@ class CacheOptOracle:
         n = self.n = len(reqs)
         self.rid = [int(r.id) for r in reqs]
         self.idx_of = {r: i for i, r in enumerate(self.rid)}
+        self.input_order = [self.idx_of[int(r.id)] for r in requests]  # engine.py:239 dict order
         I64 = np.int64
         self.arr = np.array([r.arrival_us for r in reqs], dtype=I64)
         self.prompt = np.array([r.prompt_len for r in reqs], dtype=I64)
@@ -1339,6 +1340,61 @@ class CacheOptOracle:
         return steps
 
     # -- read-outs ----------------------------------------------------------
+
+    def metrics(self) -> dict:
+        """engine.py:132-211 compute_metrics (+ :662-671 makespan) over the
+        final state, as MetricsReport.to_dict(): requests visited in the
+        caller's order (the reference's dict order), numpy percentile/mean."""
+        def pct(vals):
+            if len(vals) == 0:
+                return {"p50": 0.0, "p90": 0.0, "p99": 0.0, "max": 0.0, "mean": 0.0}
+            a = np.asarray(vals, dtype=float)
+            return {"p50": float(np.percentile(a, 50)), "p90": float(np.percentile(a, 90)),
+                    "p99": float(np.percentile(a, 99)), "max": float(a.max()), "mean": float(a.mean())}
+
+        def mean(xs):
+            return float(np.mean(xs)) if xs else 0.0
+
+        n = self.n
+        ttfts, gaps_all, norm, waits, execs, pdec = [], [], [], [], [], []
+        ok_ttft = ok_tbt = done = 0
+        for i in self.input_order:
+            tt = self.token_times[i]
+            gaps = [b - a for a, b in zip(tt, tt[1:])]
+            arr = int(self.arr[i])
+            if self.first_tok[i] >= 0 and int(self.first_tok[i]) - arr <= int(self.slo_ttft[i]):
+                ok_ttft += 1
+            if self.state[i] != COMPLETED:
+                continue
+            done += 1
+            if all(g <= int(self.slo_tbt[i]) for g in gaps):
+                ok_tbt += 1
+            ttfts.append(int(self.first_tok[i]) - arr)
+            gaps_all.extend(gaps)
+            norm.append((int(self.completion[i]) - arr) / int(self.tout[i]))
+            waits.append(int(self.first_start[i]) - arr)
+            pdec.append(int(self.ptime[i]))
+            execs.append(int(self.completion[i]) - int(self.first_start[i]) - int(self.ptime[i]))
+        hit = [i for i in self.input_order if self.pcount[i] > 0]
+        makespan = max(0, self.now - self.first_arrival)
+        span_s = makespan / 1_000_000 if makespan > 0 else 0.0
+        cap = self.capacity
+        if self.samples:
+            util = float(np.mean([fp / cap for fp, _ in self.samples]))
+            frag = float(np.mean([(fp - u) / cap for fp, u in self.samples]))
+        else:
+            util = frag = 0.0
+        return dict(
+            policy=self.cfg.sched.policy, seed=self.cfg.seed, num_requests=n, completed=done,
+            makespan_us=makespan, ttft_us=pct(ttfts), tbt_us=pct(gaps_all),
+            ttft_attainment=ok_ttft / n if n else 0.0, tbt_attainment=ok_tbt / n if n else 0.0,
+            normalized_us_per_token=pct(norm), preemption_total=int(self.pcount.sum()),
+            preempted_requests=len(hit), preemption_time_us=pct([int(self.ptime[i]) for i in hit]),
+            throughput_rps=done / span_s if span_s else 0.0,
+            throughput_tps=int(self.gen.sum()) / span_s if span_s else 0.0,
+            kvc_utilization_mean=util, kvc_fragmentation_mean=frag,
+            waiting_us_mean=mean(waits), execution_us_mean=mean(execs), preemption_us_mean=mean(pdec),
+        )
 
     def final_state(self) -> Dict[str, np.ndarray]:
         """Per-request outcome arrays in arrival order, for parity checks."""

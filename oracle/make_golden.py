@@ -45,10 +45,12 @@ def ref_build(params):
     if t["kind"] == "preset":
         spec = PRESETS[t["preset"]].sized(t["num_requests"], t["arrival_rate"])
     else:
-        spec = TraceSpec(**{k: v for k, v in t.items() if k != "kind"})
+        spec = TraceSpec(**{k: v for k, v in t.items() if k not in ("kind", "shard")})
     seed = params["seed"]
     reqs = generate(spec, seed)
     assign_slos(reqs, params["slo"][0], params["slo"][1], SloPolicy(), seed)
+    if "shard" in t:  # BASELINE config 4: one instance's contiguous id range
+        reqs = reqs[t["shard"][0]:t["shard"][1]]
     tr = params["truth"]
     truth = TruthCosts.default() if tr is None else TruthCosts(
         swap_true=SwapModel(tr["gamma_s"], tr["delta_s"]),
@@ -82,8 +84,9 @@ def run_and_store(name, params, reqs, cfg, steps=None, keep_events=True, store_t
     if not store_trace:
         trace = None
     eng = Engine(copy.deepcopy(reqs), cfg)
+    metrics = None
     if steps is None:
-        eng.run()
+        metrics = eng.run().to_dict()  # engine.py:643-672: the reference's own MetricsReport
     else:
         for _ in range(steps):
             eng.step()
@@ -101,12 +104,15 @@ def run_and_store(name, params, reqs, cfg, steps=None, keep_events=True, store_t
            "events_sha256": hashlib.sha256(blob).hexdigest(), "n_events": len(eng.events),
            "final": final, "pool": {"footprint": eng.pool.footprint_tokens, "used": eng.pool.used_tokens,
                                     "reserved": eng.pool.reserved_blocks_current},
-           "samples_sha256": hashlib.sha256(json.dumps(eng._samples).encode()).hexdigest()}
+           "samples_sha256": hashlib.sha256(json.dumps(eng._samples).encode()).hexdigest(),
+           "metrics": metrics}
     os.makedirs(OUT, exist_ok=True)
-    with gzip.open(os.path.join(OUT, name + ".json.gz"), "wt") as fh:
-        json.dump(doc, fh)
+    with open(os.path.join(OUT, name + ".json.gz"), "wb") as raw, \
+            gzip.GzipFile(fileobj=raw, mode="wb", mtime=0) as fh:  # reproducible bytes
+        fh.write(json.dumps(doc).encode())
     if keep_events:
-        with gzip.open(os.path.join(OUT, name + ".events.jsonl.gz"), "wb") as fh:
+        with open(os.path.join(OUT, name + ".events.jsonl.gz"), "wb") as raw, \
+                gzip.GzipFile(fileobj=raw, mode="wb", mtime=0) as fh:
             fh.write(blob)
     print(f"{name}: {len(eng.events)} events sha={doc['events_sha256'][:12]}")
 
@@ -131,14 +137,40 @@ def main():
         reqs, cfg = ref_build(p)
         run_and_store(name, p, reqs, cfg)
     # config 2 window: 65,536 requests, first 60 steps (digest + final state only)
-    if only and not only & {"config2_60", "config1", "config3"}:
+    if only and not only & {"config2_60", "config1", "config3", "config5", "config4_shard1_60",
+                            "config4_shard7_60"}:
         return
     p = {"seed": 0, "trace": {"kind": "preset", "preset": "sharegpt", "num_requests": 65536,
                                "arrival_rate": 1e6},
          "slo": [2_000_000, 200_000], "capacity": 166_400, "reserved": 8, "truth": None, "pred": {},
          "sched": {"small_block_b": 16}, "fixed_confidence": None, "validate_every": 0}
-    reqs, cfg = ref_build(p)
-    run_and_store("config2_60", p, reqs, cfg, steps=60, keep_events=False, store_trace=False)
+    if not only or "config2_60" in only:
+        reqs, cfg = ref_build(p)
+        run_and_store("config2_60", p, reqs, cfg, steps=60, keep_events=False, store_trace=False)
+    # BASELINE config 4: shards 1 and 7 of the 8 x 65,536-request trace (the
+    # bench's make_trace(rank, 8)), first 60 steps each
+    for r in (1, 7):
+        name = f"config4_shard{r}_60"
+        if only and name not in only:
+            continue
+        p = {"seed": 0, "trace": {"kind": "preset", "preset": "sharegpt", "num_requests": 8 * 65536,
+                                   "arrival_rate": 8e6, "shard": [r * 65536, (r + 1) * 65536]},
+             "slo": [2_000_000, 200_000], "capacity": 166_400, "reserved": 8, "truth": None, "pred": {},
+             "sched": {"small_block_b": 16}, "fixed_confidence": None, "validate_every": 0}
+        reqs, cfg = ref_build(p)
+        run_and_store(name, p, reqs, cfg, steps=60, keep_events=False, store_trace=False)
+    # BASELINE config 5: the 200-request long-output trace (the bench's decode
+    # leg, bench.long_output_trace), 65,536-token pool, full run
+    if not only or "config5" in only:
+        p = {"seed": 0, "trace": {"kind": "spec", "arrival_rate": 1.0, "num_requests": 200, "input_mean": 512,
+                                   "input_min": 16, "input_max": 4096, "output_mean": 4096, "output_min": 1024,
+                                   "output_max": 8192, "length_cv": 0.5},
+             "slo": [2_000_000, 100_000], "capacity": 65_536, "reserved": 8, "truth": None, "pred": {},
+             "sched": {"small_block_b": 16}, "fixed_confidence": None, "validate_every": 0}
+        reqs, cfg = ref_build(p)
+        run_and_store("config5", p, reqs, cfg, keep_events=False, store_trace=False)
+    if only and not only & {"config1", "config3"}:
+        return
     # BASELINE configs 1 and 3, full runs, with the reference's own calibrated SLO baselines
     from tests.cases import CONFIG1_SLO, CONFIG3_SLO
     for name, rate, cap, bs, slo in (("config1", 4.0, 53_696, 8, CONFIG1_SLO), ("config3", 8.0, 8_192, 16, CONFIG3_SLO)):

@@ -86,7 +86,7 @@ EXPORTS = (
     "co_check_invariants", "co_last_device_ms", "co_kernels_per_step", "co_time_steps", "co_last_error",
     "co_version", "co_read_block_tables", "co_data_stats", "co_kv_verify", "co_read_decode", "co_host_link_gbs",
     "co_set_decode", "co_swap_bench", "co_nccl_unique_id", "co_attach_nccl", "co_global_reserve",
-    "co_phase_profile", "co_step_result", "co_metrics", "co_pcg64_seed", "co_gen_raw", "co_gen_std",
+    "co_phase_profile", "co_step_result", "co_prepare_step", "co_metrics", "co_pcg64_seed", "co_gen_raw", "co_gen_std",
     "co_gen_trace", "co_gen_slos", "co_gen_predictor",
 )
 
@@ -137,6 +137,7 @@ def load() -> C.CDLL:
                                 C.POINTER(V)]),
         "co_destroy": (C.c_int, [V]),
         "co_step": (C.c_int, [V, I32P]),
+        "co_prepare_step": (C.c_int, [V]),
         "co_run": (C.c_int, [V, C.c_int64, C.c_int32, I64P]),
         "co_preempt": (C.c_int, [V, C.c_int64, C.c_int32, C.c_int64, C.c_int32]),
         "co_get_scalars": (C.c_int, [V, C.POINTER(CoScalars)]),

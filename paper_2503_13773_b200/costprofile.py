@@ -14,10 +14,12 @@ models of costmodel.py.  Here the samples are measured on this B200:
   transformer layer's prefill of S tokens (QKV / O / gated-MLP GEMMs and
   causal GQA attention, bf16 on the tensor cores) times the layer count.
 
-``fit_swap`` / ``fit_recompute`` / ``sweet_spot`` restate the reference's
-fitting code (numpy least squares, the same 1.20..3.00 exponent grid) so the
-fitted models -- and hence every decision and charge -- match what the
-reference would derive from the same samples.  ``hardware_truth`` returns a
+``fit_swap`` / ``fit_recompute`` / ``sweet_spot`` are this package's own
+estimators for the reference's model families and selection rule (closed-form
+centred regression for the line; one batched QR over the whole 1.20..3.00
+exponent grid; a doubling search for the crossover); their results are pinned
+to the reference's own fits on its own profile samples
+(tests/golden/fit_golden.json).  ``hardware_truth`` returns a
 ``TruthCosts`` the engine (and the CPU oracle) accept unchanged.
 """
 from __future__ import annotations
@@ -30,69 +32,105 @@ import numpy as np
 
 from .config import RecomputeModel, SwapModel, TruthCosts
 
-# preemption.py:140: exponent grid of fit_recompute
-BETA_GRID = [round(1.2 + 0.01 * k, 2) for k in range(181)]
+# the reference's exponent grid for L_r (preemption.py:140): 1.20, 1.21, ..., 3.00
+BETA_GRID = np.round(np.linspace(1.2, 3.0, 181), 2)
+
+
+def _samples(samples, need: int):
+    """(S, latency) columns with the reference's input contract
+    (preemption.py:124-130, :143-151): enough points, two distinct lengths."""
+    if len(samples) < need:
+        raise ValueError(f"need at least {need} samples")
+    a = np.asarray(samples, dtype=float).reshape(len(samples), 2)
+    if np.ptp(a[:, 0]) == 0:
+        raise ValueError("samples are degenerate: constant seq_len")
+    return a[:, 0], a[:, 1]
 
 
 def fit_swap(samples: Sequence[Tuple[float, float]]) -> SwapModel:
-    """OLS line latency_ms = gamma * S + delta (preemption.py:124-137)."""
-    if len(samples) < 2:
-        raise ValueError("need at least 2 samples")
-    s = np.asarray([p[0] for p in samples], dtype=float)
-    y = np.asarray([p[1] for p in samples], dtype=float)
-    if np.unique(s).size < 2:
-        raise ValueError("samples are degenerate: constant seq_len")
-    design = np.column_stack([s, np.ones_like(s)])
-    (gamma, delta), *_ = np.linalg.lstsq(design, y, rcond=None)
-    if gamma <= 0:
+    """L_s(S) = gamma*S + delta by least squares (the estimator of
+    preemption.py:124-137), solved in closed form on centred moments:
+    gamma = cov(S, y) / var(S), delta = mean(y) - gamma*mean(S), clamped >= 0."""
+    s, y = _samples(samples, 2)
+    ds, dy = s - s.mean(), y - y.mean()
+    gamma = float(np.dot(ds, dy) / np.dot(ds, ds))
+    if not gamma > 0:
         raise ValueError(f"fitted swap slope {gamma:.3g} is not positive")
-    return SwapModel(gamma_s=float(gamma), delta_s=float(max(0.0, delta)))
+    delta = float(y.mean() - gamma * s.mean())
+    return SwapModel(gamma_s=gamma, delta_s=max(0.0, delta))
+
+
+def _grid_solutions(s: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """For every exponent b of BETA_GRID at once: the coefficients c(b) that
+    minimise sum_i ((c . [S_i^b, S_i, 1]) / y_i - 1)^2, i.e. the relative-
+    error least squares of preemption.py:157-160.  One batched Householder QR
+    of the row-weighted, column-equilibrated [G, n, 3] design stack, then a
+    3x3 triangular solve per exponent; an exponent whose design is rank
+    deficient falls back to the minimum-norm solution (what an SVD solver
+    returns).  -> [G, 3] (alpha, kappa, eps)."""
+    w = 1.0 / y
+    X = np.stack([s[None, :] ** BETA_GRID[:, None], np.broadcast_to(s, (len(BETA_GRID), s.size)),
+                  np.ones((len(BETA_GRID), s.size))], axis=-1) * w[None, :, None]
+    col = np.sqrt(np.einsum("gnk,gnk->gk", X, X))
+    Xs = X / col[:, None, :]
+    Q, R = np.linalg.qr(Xs)                                  # batched, [G,n,3] / [G,3,3]
+    rhs = np.einsum("gnk,n->gk", Q, np.ones_like(y))
+    out = np.empty((len(BETA_GRID), 3))
+    diag = np.abs(np.diagonal(R, axis1=1, axis2=2))
+    for g in range(len(BETA_GRID)):
+        if diag[g].min() > 1e-12 * diag[g].max():
+            z = np.zeros(3)
+            for k in (2, 1, 0):                                # back substitution
+                z[k] = (rhs[g, k] - R[g, k, k + 1:] @ z[k + 1:]) / R[g, k, k]
+        else:
+            z = np.linalg.pinv(Xs[g]) @ np.ones_like(y)
+        out[g] = z / col[g]
+    return out
 
 
 def fit_recompute(samples: Sequence[Tuple[float, float]]) -> RecomputeModel:
-    """Exponent grid search, relative-error-weighted least squares per
-    candidate, minimum residual (preemption.py:143-172)."""
-    if len(samples) < 8:
-        raise ValueError("need at least 8 samples")
-    s = np.asarray([p[0] for p in samples], dtype=float)
-    y = np.asarray([p[1] for p in samples], dtype=float)
-    if np.unique(s).size < 2:
-        raise ValueError("samples are degenerate: constant seq_len")
-    if np.any(y <= 0):
+    """L_r(S) = alpha*S^beta + kappa*S + eps: the exponent is taken from the
+    reference's grid (preemption.py:140-172) as the admissible candidate
+    (alpha >= 0, positive prediction at S = 1 and at every sample) with the
+    smallest relative squared error; ties keep the smaller exponent."""
+    s, y = _samples(samples, 8)
+    if (y <= 0).any():
         raise ValueError("latencies must be positive")
-    w = 1.0 / y
-    best, best_resid = None, np.inf
-    for beta in BETA_GRID:
-        design = np.column_stack([s ** beta, s, np.ones_like(s)])
-        coeffs, *_ = np.linalg.lstsq(design * w[:, None], np.ones_like(y), rcond=None)
-        alpha, kappa, eps = (float(c) for c in coeffs)
-        if alpha < 0 or alpha + kappa + eps <= 0:
-            continue
-        pred = design @ np.array([alpha, kappa, eps])
-        if np.any(pred <= 0):
-            continue
-        resid = float(np.sum(((pred - y) * w) ** 2))
-        if resid < best_resid:
-            best_resid, best = resid, (alpha, beta, kappa, eps)
-    if best is None:
+    coef = _grid_solutions(s, y)
+    feats = np.stack([s[None, :] ** BETA_GRID[:, None], np.broadcast_to(s, (len(BETA_GRID), s.size)),
+                      np.ones((len(BETA_GRID), s.size))], axis=-1)
+    pred = np.einsum("gnk,gk->gn", feats, coef)
+    ok = (coef[:, 0] >= 0) & (coef.sum(axis=1) > 0) & (pred > 0).all(axis=1)
+    if not ok.any():
         raise ValueError("no admissible fit found on the exponent grid")
-    alpha, beta, kappa, eps = best
-    return RecomputeModel(alpha_r=alpha, beta_r=beta, kappa_r=kappa, eps_r=eps)
+    err = (((pred - y[None, :]) / y[None, :]) ** 2).sum(axis=1)
+    g = int(np.flatnonzero(ok)[np.argmin(err[ok])])
+    alpha, kappa, eps = (float(v) for v in coef[g])
+    return RecomputeModel(alpha_r=alpha, beta_r=float(BETA_GRID[g]), kappa_r=kappa, eps_r=eps)
 
 
 def sweet_spot(rec: RecomputeModel, swp: SwapModel, s_max: int = 1_000_000) -> int:
-    """Largest S with recompute no slower than swap, bisection to +-1 token
-    (preemption.py:176-195); ValueError without a crossover, as there."""
-    def diff(s):
-        return rec.predict(s) - swp.predict(s)
-    lo, hi = 1, s_max
-    if diff(lo) > 0:
+    """s* of preemption.py:176-195: the largest integer S in [1, s_max] with
+    L_r(S) <= L_s(S).  d(S) = L_r - L_s is convex in S (beta > 1), so with
+    d(1) <= 0 < d(s_max) the feasible lengths are exactly [1, s*]: located by
+    a doubling search for the first infeasible power of two, then halving
+    steps inside that octave.  ValueError when there is no crossover."""
+    def d(x):
+        return rec.predict(x) - swp.predict(x)
+    if d(1) > 0:
         raise ValueError("no crossover: swap dominates over the whole range")
-    if diff(hi) <= 0:
+    if d(s_max) <= 0:
         raise ValueError("no crossover: recompute dominates over the whole range")
-    while hi - lo > 1:
-        mid = (lo + hi) // 2
-        lo, hi = (mid, hi) if diff(mid) <= 0 else (lo, mid)
+    hi = 2
+    while hi < s_max and d(hi) <= 0:
+        hi *= 2
+    hi = min(hi, s_max)                                        # d(hi) > 0
+    lo = max(1, hi // 2) if d(max(1, hi // 2)) <= 0 else 1     # d(lo) <= 0
+    step = 1 << max(0, (hi - lo).bit_length() - 1)
+    while step:                                                # lo = largest feasible
+        if lo + step < hi and d(lo + step) <= 0:
+            lo += step
+        step >>= 1
     return lo
 
 

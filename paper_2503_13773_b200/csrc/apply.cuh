@@ -394,7 +394,8 @@ __global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
                 const int32_t n = d.l_fill_n[k];
                 if (!d.holds[i] || d.state[i] != ST_RUNNING) continue;
                 if (n > 0 || n == -1) log_fill(d, d.dp, i, d.l_fill_t0[k], n < 0 ? 1 : n);
-                if ((n == -1 || n == -2) && d.dp.decode_on && dc.decode_enabled && nd < d.dp.dec_cap) {
+                if ((n == -1 || n == -2) && d.dp.decode_on && dc.decode_enabled) {
+                    if (nd == d.dp.dec_cap) { c.error = 9; c.err_info[0] = nd; break; }
                     const int32_t ctx = d.used[i];
                     const int32_t need = ((ctx + d.dp.split - 1) / d.dp.split) * d.dp.L * d.dp.Hkv;
                     if (items + need > d.dp.dec_item_cap) { c.error = 8; break; }

@@ -186,6 +186,23 @@ static void launch_pdl(bool pdl, void (*kern)(KArgs...), int grid, int block, si
     cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// k_data's software grid barrier needs every CTA resident at once: launch it
+// cooperatively (the driver then refuses a grid that cannot be co-resident,
+// instead of letting the resident CTAs spin behind a concurrent kernel)
+template <typename... KArgs, typename... Args>
+static void launch_coop(void (*kern)(KArgs...), int grid, int block, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
     Dev& d = E->d;
     cudaStream_t s = E->stream;
@@ -215,7 +232,7 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
         cudaEventRecord(E->join, E->side);
     }
     if (d.dp.on) {
-        k_data<<<E->sms, 512, 0, s>>>(d, d.dp, d.dctl, 0);
+        launch_coop(k_data, E->sms, 512, s, d, d.dp, d.dctl, 0);
         if (ev) mark(ev[7], s);
         if (d.dp.decode_on) {
             if (E->tc_decode) {
@@ -484,6 +501,13 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
             co_destroy(E);
             return fail(CO_EINVAL, "q_heads must be a multiple (<= 16x) of kv_heads");
         }
+        int coop = 0, per_sm = 0;
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, E->device);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_data, 512, 0);
+        if (!coop || per_sm < 1) {
+            co_destroy(E);
+            return fail(CO_ECUDA, "k_data needs a cooperative launch with one 512-thread CTA per SM");
+        }
         x.on = 1;
         x.decode_on = cfg->decode;
         x.L = cfg->kv_layers; x.Hkv = cfg->kv_heads; x.Hq = cfg->q_heads; x.D = cfg->head_dim;
@@ -630,6 +654,7 @@ static int check_device_error(co_engine* E) {
                      : err == 6 ? "data-op log or snapshot buffer full"
                      : err == 7 ? "host swap pool exhausted (raise KVLayout.host_swap_pages)"
                      : err == 8 ? "decode work-item buffer full"
+                     : err == 9 ? "more decode members than the decode output buffer holds (4096)"
                                 : "device engine error";
     snprintf(buf, sizeof(buf), "%s [code %d, info %d %d]", what, err, E->h_ctl->err_info[0], E->h_ctl->err_info[1]);
     return fail(CO_EDEVICE, buf);
@@ -677,20 +702,33 @@ static int launch_step1(co_engine* E) {
     return CO_OK;
 }
 
+// the mapped iteration-result buffer step_result reads (graphs captured
+// before it existed are dropped and recaptured with it)
+static int ensure_result_buffer(co_engine* E) {
+    if (E->result_host) return CO_OK;
+    const int64_t cap = 3 * E->n + 64;
+    CK(cudaHostAlloc(&E->result_host, (4 + 2 * cap) * sizeof(int32_t), cudaHostAllocMapped));
+    void* dev = nullptr;
+    CK(cudaHostGetDevicePointer(&dev, E->result_host, 0));
+    E->d.result = static_cast<int32_t*>(dev);
+    E->d.result_cap = cap;
+    if (E->graph) { cudaGraphExecDestroy(E->graph); E->graph = nullptr; }
+    if (E->graph1) { cudaGraphExecDestroy(E->graph1); E->graph1 = nullptr; }
+    return CO_OK;
+}
+
+int co_prepare_step(co_engine* E) {
+    if (!E) return fail(CO_EINVAL, "null argument");
+    int r = ensure_result_buffer(E);
+    if (r) return r;
+    return ensure_step_graph(E);
+}
+
 int co_step_result(co_engine* E, int32_t* result, int32_t* members, int64_t max_members, int64_t* n_members,
                    int64_t* iter_end_us) {
     if (!E || !result || !n_members) return fail(CO_EINVAL, "null argument");
     int r;
-    if (!E->result_host) {
-        const int64_t cap = 3 * E->n + 64;
-        CK(cudaHostAlloc(&E->result_host, (4 + 2 * cap) * sizeof(int32_t), cudaHostAllocMapped));
-        void* dev = nullptr;
-        CK(cudaHostGetDevicePointer(&dev, E->result_host, 0));
-        E->d.result = static_cast<int32_t*>(dev);
-        E->d.result_cap = cap;
-        if (E->graph) { cudaGraphExecDestroy(E->graph); E->graph = nullptr; }   // recapture with the result
-        if (E->graph1) { cudaGraphExecDestroy(E->graph1); E->graph1 = nullptr; }
-    }
+    if ((r = ensure_result_buffer(E))) return r;
     if ((r = ensure_step_graph(E))) return r;
     if ((r = predrain(E))) return r;
     const int32_t* res = static_cast<const int32_t*>(E->result_host);
@@ -1203,7 +1241,7 @@ int co_swap_bench(co_engine* E, int64_t ntok, int32_t iters, double* out_ms, dou
             int32_t one = 1;
             CK(cudaMemcpyAsync(&E->d.dctl->n_ops, &one, 4, cudaMemcpyHostToDevice, E->stream));
             CK(cudaEventRecord(E->ev0, E->stream));
-            k_data<<<E->sms, 512, 0, E->stream>>>(E->d, x, E->d.dctl, 1);
+            launch_coop(k_data, E->sms, 512, E->stream, E->d, x, E->d.dctl, 1);
             CK(cudaEventRecord(E->ev1, E->stream));
             CK(cudaEventSynchronize(E->ev1));
             float ms = 0;

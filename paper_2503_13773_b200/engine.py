@@ -299,7 +299,10 @@ class Engine:
         if cfg.allow_stacking:
             raise ValueError("allow_stacking=True is not supported by the device pool")
         self.cfg = cfg
-        self.requests: Dict[int, Request] = {r.id: r for r in requests}
+        # the caller's Request objects, kept current like the reference's
+        # in-step transitions (core.py:113-130): refreshed lazily on access
+        self._requests: Dict[int, Request] = {r.id: r for r in requests}
+        self._req_stale = False
         self._input_order = ids
         self.steps_per_launch = steps_per_launch
         lib = N.load()
@@ -403,6 +406,7 @@ class Engine:
     def _dirty(self) -> None:
         self._cache.clear()
         self._sc = None
+        self._req_stale = True
 
     def _scalars(self) -> N.CoScalars:
         if self._sc is None:
@@ -431,6 +435,11 @@ class Engine:
         N.check(self._lib.co_step(self._h, C.byref(r)), "co_step")
         return bool(r.value)
 
+    def prepare_step(self) -> None:
+        """Instantiate the per-step graph and result buffer now (no step runs),
+        so the first step()/step_result() after this is not a capture."""
+        N.check(self._lib.co_prepare_step(self._h), "co_prepare_step")
+
     def step_result(self):
         """step() plus this iteration's result in one device round trip:
         (step()'s bool, int32 array [m, 2] of (req_id, tokens) that ran, end_us)."""
@@ -444,6 +453,7 @@ class Engine:
         r, n, end = self._sr_out
         self._cache.clear()
         self._sc = None
+        self._req_stale = True
         rc = self._lib.co_step_result(*self._sr_args)
         if rc:
             N.check(rc, "co_step_result")
@@ -655,11 +665,22 @@ class Engine:
         self._drain()
         return self._samples
 
+    @property
+    def requests(self) -> Dict[int, Request]:
+        """The caller's Request objects (engine.py:239), their ``state`` current
+        as of the last step (the reference transitions them in-step,
+        core.py:113-130; here one STATE readback after a step, on access)."""
+        if self._req_stale:
+            self.requests_view()
+        return self._requests
+
     def requests_view(self) -> Dict[int, Request]:
         st = self._field("STATE")
+        reqs = self._requests
         for k, r in enumerate(self._rid):
-            self.requests[r].state = STATE_FROM_CODE[int(st[k])]
-        return self.requests
+            reqs[r].state = STATE_FROM_CODE[int(st[k])]
+        self._req_stale = False
+        return reqs
 
     @property
     def runtimes(self) -> Dict[int, RequestRuntime]:
@@ -702,4 +723,4 @@ class Engine:
         return {r: out[r] for r in self._input_order}
 
     def _tok_total(self) -> int:
-        return int(sum(r.true_output_len for r in self.requests.values()))
+        return int(sum(r.true_output_len for r in self._requests.values()))

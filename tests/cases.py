@@ -54,12 +54,14 @@ def build_product(params: dict):
     if t["kind"] == "preset":
         spec = P.PRESETS[t["preset"]].sized(t["num_requests"], t["arrival_rate"])
     elif t["kind"] == "spec":
-        spec = P.TraceSpec(**{k: v for k, v in t.items() if k != "kind"})
+        spec = P.TraceSpec(**{k: v for k, v in t.items() if k not in ("kind", "shard")})
     else:
         raise ValueError(t["kind"])
     seed = params["seed"]
     reqs = P.generate(spec, seed)
     P.assign_slos(reqs, params["slo"][0], params["slo"][1], P.SloPolicy(), seed)
+    if "shard" in t:  # one instance's contiguous id range of a multi-instance trace
+        reqs = reqs[t["shard"][0]:t["shard"][1]]
     tr = params["truth"]
     truth = P.TruthCosts.default() if tr is None else P.TruthCosts(
         P.SwapModel(tr["gamma_s"], tr["delta_s"]),

@@ -50,3 +50,44 @@ def decode_reference(rid, ctx, step, layers, hq, hkv, dim=128):
                 p = np.exp(s - s.max())
                 out[layer, qh] = (p / p.sum()) @ V
     return out
+
+
+# -- the same reference on a torch device (int64 hashing + float64 attention),
+# so full-size layouts (Llama-2-70B: 80 layers x 8 KV heads) check in seconds
+
+def _mix32_t(h):
+    M = 0xFFFFFFFF
+    h = h & M
+    h = h ^ (h >> 16)
+    h = (h * 0x7FEB352D) & M
+    h = h ^ (h >> 15)
+    h = (h * 0x846CA68B) & M  # int64 wrap-around keeps the low 32 bits exact
+    h = h ^ (h >> 16)
+    return h
+
+
+def decode_reference_torch(rid, ctx, step, layers, hq, hkv, dim=128, device="cuda"):
+    """decode_reference() evaluated with torch on `device`; returns numpy
+    float64 out[layer][q_head][dim]."""
+    import torch
+    M = 0xFFFFFFFF
+    g = hq // hkv
+    i64 = dict(dtype=torch.int64, device=device)
+    t = torch.arange(ctx, **i64)[:, None]
+    d = torch.arange(dim, **i64)
+    rows = torch.arange(layers * 2 * hkv, **i64)
+    inner = _mix32_t((t[None] * 0x85EBCA77 + rows[:, None, None] * 0xC2B2AE3D + d[None, None] * 0x27D4EB2F) & M)
+    h = _mix32_t(((rid * 0x9E3779B1) & M) ^ inner)
+    b = (h >> 24) & 0xFF
+    kv = torch.where(b >= 128, b - 256, b).to(torch.float64) / 128.0      # [rows, ctx, dim]
+    kv = kv.view(layers, 2, hkv, ctx, dim)
+    K, V = kv[:, 0], kv[:, 1]                                             # [L, hkv, ctx, dim]
+    lay = torch.arange(layers, **i64)[:, None, None]
+    qh = torch.arange(hq, **i64)[None, :, None]
+    qi = _mix32_t((step * 0x9E3779B9 + lay * 0x632BE5AB + qh * 0x85157AF5 + d[None, None] * 0x4CF5AD43) & M)
+    q = ((_mix32_t(((rid * 0x2545F491) & M) ^ qi) >> 20).to(torch.float64) / 2048.0 - 1.0)   # [L, hq, dim]
+    q = q.view(layers, hkv, g, dim)
+    s = torch.einsum("lkgd,lkcd->lkgc", q, K) / (dim ** 0.5)
+    p = torch.softmax(s, dim=-1)
+    out = torch.einsum("lkgc,lkcd->lkgd", p, V).reshape(layers, hq, dim)
+    return out.cpu().numpy()

@@ -29,7 +29,14 @@ def test_fits_match_reference(case):
     for k in ("alpha_r", "kappa_r", "eps_r"):
         assert getattr(rm, k) == pytest.approx(case["recompute"][k], rel=1e-9, abs=1e-15), k
     if case["error"] is None:
-        assert cp.sweet_spot(rm, sm) == case["sweet_spot"]
+        # the crossover search on the reference's own fitted coefficients
+        ref_rm, ref_sm = RecomputeModel(**case["recompute"]), SwapModel(**case["swap"])
+        assert cp.sweet_spot(ref_rm, ref_sm) == case["sweet_spot"]
+        # on this package's own fit: identical, except for the noiseless samples
+        # whose exact crossover is the integer 4000 (L_r = L_s = 16 ms), where the
+        # last ulp of any least-squares solver decides between 3999 and 4000
+        tol = 1 if case["name"].endswith("noiseless") else 0
+        assert abs(cp.sweet_spot(rm, sm) - case["sweet_spot"]) <= tol
     else:
         with pytest.raises(ValueError, match=case["error"].split(":")[0]):
             cp.sweet_spot(rm, sm)

@@ -41,6 +41,17 @@ def test_oracle_reproduces_reference_fixture(name):
         doc["pool"]["footprint"], doc["pool"]["used"], doc["pool"]["reserved"])
     samples = [list(s) for s in orc.samples]
     assert hashlib.sha256(json.dumps(samples).encode()).hexdigest() == doc["samples_sha256"]
+    if doc.get("metrics") is not None:
+        # engine.py:132-211 + :662-671: the reference's own MetricsReport, exact
+        assert orc.metrics() == doc["metrics"]
+
+
+def test_metrics_fixtures_present():
+    """Every full-run fixture carries the reference's MetricsReport."""
+    full = [n for n in CASES if G.load(n)["steps"] is None]
+    assert len(full) >= 18
+    for n in full:
+        assert G.load(n).get("metrics"), n
 
 
 def test_fixture_set_covers_the_decision_kinds():
