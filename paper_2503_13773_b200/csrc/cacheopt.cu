@@ -101,6 +101,28 @@ __global__ void k_reset_drained(Dev d, int64_t ev, int64_t mem, int64_t smp) {
     }
 }
 
+// The step graph's last kernel copies the control block and the (undrained)
+// append log into mapped pinned memory, so after a step() the host can serve
+// scalars, events, members and samples with no further device round trip.
+constexpr int MIR_EV = 256, MIR_MEM = 4096, MIR_S = 64;
+struct LogMirror {
+    Ctl ctl;
+    co_event ev[MIR_EV];
+    int32_t mem[2 * MIR_MEM];
+    int64_t smp[2 * MIR_S];
+};
+
+__global__ void k_mirror(Dev d, LogMirror* m) {
+    pdl_enter();
+    const Ctl& c = *d.ctl;
+    if (threadIdx.x == 0) m->ctl = c;
+    const int64_t ne = c.ev_count, nm = c.mem_count, ns = c.sample_count;
+    if (ne > MIR_EV || nm > MIR_MEM || ns > MIR_S) return;  // the host drains the slow way
+    for (int64_t k = threadIdx.x; k < ne; k += blockDim.x) m->ev[k] = d.events[k];
+    for (int64_t k = threadIdx.x; k < 2 * nm; k += blockDim.x) m->mem[k] = d.members[k];
+    for (int64_t k = threadIdx.x; k < 2 * ns; k += blockDim.x) m->smp[k] = d.samples[k];
+}
+
 struct co_engine {
     Dev d{};
     int device = 0;
@@ -128,7 +150,13 @@ struct co_engine {
     int64_t* red = nullptr;  // [send 2][recv 2]
     int64_t reduce_calls = 0;
     CUtensorMap kvmap;
-    cudaGraphExec_t graph1 = nullptr;  // one step, step() semantics
+    cudaGraphExec_t graph1 = nullptr;   // one step, step() semantics
+    cudaGraphExec_t graph1r = nullptr;  // the same, starting with an emptied append log
+    LogMirror* mir = nullptr;           // mapped pinned (host view)
+    LogMirror* mir_dev = nullptr;       // its device alias
+    bool ctl_fresh = false;             // h_ctl == the logical device state (no sync needed)
+    bool reset_pending = false;         // log consumed from the mirror; device counts not yet reset
+    int64_t pend_ev = 0, pend_mem = 0, pend_s = 0;
     void* result_host = nullptr;
     bool pdl = true;         // programmatic dependent launch between step kernels (CACHEOPT_PDL=0: off)
     bool tc_decode = false;  // tcgen05 (k_decode_tc05) when the block size tiles by 16; else CUDA cores
@@ -203,11 +231,11 @@ static void launch_coop(void (*kern)(KArgs...), int grid, int block, cudaStream_
     cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
+static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr, int32_t reset = 0) {
     Dev& d = E->d;
     cudaStream_t s = E->stream;
     if (ev) mark(ev[0], s);
-    k_begin<<<1, 32, 0, s>>>(d, guard);
+    k_begin<<<1, 32, 0, s>>>(d, guard, reset);
     if (ev) mark(ev[1], s);
     // PDL edges only between back-to-back kernels (an event node in between
     // is a full dependency anyway)
@@ -254,18 +282,61 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr) {
     return CO_OK;
 }
 
+// device work that changes the control block is about to be enqueued
+static inline void touch(co_engine* E) { E->ctl_fresh = false; }
+
+static int apply_pending_reset(co_engine* E) {
+    if (!E->reset_pending) return CO_OK;
+    k_reset_drained<<<1, 1, 0, E->stream>>>(E->d, E->pend_ev, E->pend_mem, E->pend_s);
+    CK(cudaGetLastError());
+    E->reset_pending = false;
+    return CO_OK;
+}
+
+// before enqueueing device work outside the step graphs
+static int begin_work(co_engine* E) {
+    touch(E);
+    return apply_pending_reset(E);
+}
+
 static int sync_ctl(co_engine* E) {
+    if (E->ctl_fresh) return CO_OK;
+    int r = apply_pending_reset(E);
+    if (r) return r;
     CK(cudaMemcpyAsync(E->h_ctl, E->d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, E->stream));
     CK(cudaStreamSynchronize(E->stream));
     return CO_OK;
+}
+
+static void stage_log(co_engine* E, const co_event* ev, int64_t ne, const int32_t* mem, int64_t nm,
+                      const int64_t* smp, int64_t ns) {
+    const size_t base = E->st_events.size();
+    const int64_t mbase = (int64_t)E->st_members.size() / 2;
+    E->st_events.insert(E->st_events.end(), ev, ev + ne);
+    for (size_t k = base; k < E->st_events.size(); k++)
+        if (E->st_events[k].kind == CO_EV_ITER) E->st_events[k].c += mbase;
+    E->st_members.insert(E->st_members.end(), mem, mem + 2 * nm);
+    E->st_samples.insert(E->st_samples.end(), smp, smp + 2 * ns);
 }
 
 // move device append buffers into host staging and reset the device fill
 static int drain_device(co_engine* E) {
     int r = sync_ctl(E);
     if (r) return r;
-    const Ctl& c = *E->h_ctl;
+    Ctl& c = *E->h_ctl;
     int64_t ne = c.ev_count, nm = c.mem_count, ns = c.sample_count;
+    if (ne == 0 && nm == 0 && ns == 0 && !c.paused) return CO_OK;
+    if (E->ctl_fresh && E->mir && ne <= MIR_EV && nm <= MIR_MEM && ns <= MIR_S) {
+        // fast path: the step graph mirrored the whole log; the device counts
+        // are reset by the next step graph (graph1r) or before any other use
+        stage_log(E, E->mir->ev, ne, E->mir->mem, nm, E->mir->smp, ns);
+        E->pend_ev = ne; E->pend_mem = nm; E->pend_s = ns;
+        E->reset_pending = true;
+        c.ev_count = c.mem_count = c.sample_count = 0;
+        c.paused = 0;
+        return CO_OK;
+    }
+    touch(E);
     if (ne > 0) {
         size_t base = E->st_events.size();
         int64_t mbase = (int64_t)E->st_members.size() / 2;
@@ -313,6 +384,8 @@ int co_destroy(co_engine* E) {
     if (!E) return CO_OK;
     if (E->graph) cudaGraphExecDestroy(E->graph);
     if (E->graph1) cudaGraphExecDestroy(E->graph1);
+    if (E->graph1r) cudaGraphExecDestroy(E->graph1r);
+    if (E->mir) cudaFreeHost(E->mir);
     if (E->result_host) cudaFreeHost(E->result_host);
     if (E->comm) nccl().commDestroy(E->comm);
     if (E->side) cudaStreamDestroy(E->side);
@@ -673,27 +746,42 @@ static int predrain(co_engine* E) {
 }
 
 static int ensure_step_graph(co_engine* E) {
-    if (E->graph1) return CO_OK;
-    cudaGraph_t g;
-    int r;
-    CK(cudaStreamBeginCapture(E->stream, cudaStreamCaptureModeThreadLocal));
-    if ((r = launch_step(E, 0))) { cudaStreamEndCapture(E->stream, &g); return r; }
-    // the control block comes back inside the graph: one launch + one sync per step
-    cudaMemcpyAsync(E->h_ctl, E->d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, E->stream);
-    CK(cudaStreamEndCapture(E->stream, &g));
-    CK(cudaGraphInstantiate(&E->graph1, g, 0));
-    cudaGraphDestroy(g);
+    if (E->graph1 && E->graph1r) return CO_OK;
+    if (!E->mir) {
+        CK(cudaHostAlloc(&E->mir, sizeof(LogMirror), cudaHostAllocMapped));
+        void* dev = nullptr;
+        CK(cudaHostGetDevicePointer(&dev, E->mir, 0));
+        E->mir_dev = static_cast<LogMirror*>(dev);
+    }
+    for (int32_t reset = 0; reset < 2; reset++) {
+        cudaGraphExec_t& ge = reset ? E->graph1r : E->graph1;
+        if (ge) continue;
+        cudaGraph_t g;
+        int r;
+        CK(cudaStreamBeginCapture(E->stream, cudaStreamCaptureModeThreadLocal));
+        if ((r = launch_step(E, 0, nullptr, reset))) { cudaStreamEndCapture(E->stream, &g); return r; }
+        // the control block and the step's log come back inside the graph:
+        // one launch + one sync per step
+        launch_pdl(E->pdl, k_mirror, 1, 256, 0, E->stream, E->d, E->mir_dev);
+        CK(cudaStreamEndCapture(E->stream, &g));
+        CK(cudaGraphInstantiate(&ge, g, 0));
+        cudaGraphDestroy(g);
+    }
     return CO_OK;
 }
 
-// one step through graph1 (which ends with the control-block readback);
-// per-step device timing only once co_last_device_ms has been asked for
+// one step through graph1 (which ends with the mirror kernel); per-step
+// device timing only once co_last_device_ms has been asked for
 static int launch_step1(co_engine* E) {
+    touch(E);
     if (E->timing) CK(cudaEventRecord(E->ev0, E->stream));
-    CK(cudaGraphLaunch(E->graph1, E->stream));
+    CK(cudaGraphLaunch(E->reset_pending ? E->graph1r : E->graph1, E->stream));
+    E->reset_pending = false;
     if (E->comm) E->reduce_calls += 1;
     if (E->timing) CK(cudaEventRecord(E->ev1, E->stream));
     CK(cudaStreamSynchronize(E->stream));
+    std::memcpy(E->h_ctl, &E->mir->ctl, sizeof(Ctl));
+    E->ctl_fresh = true;
     if (E->timing) {
         float ms = 0;
         cudaEventElapsedTime(&ms, E->ev0, E->ev1);
@@ -714,6 +802,7 @@ static int ensure_result_buffer(co_engine* E) {
     E->d.result_cap = cap;
     if (E->graph) { cudaGraphExecDestroy(E->graph); E->graph = nullptr; }
     if (E->graph1) { cudaGraphExecDestroy(E->graph1); E->graph1 = nullptr; }
+        if (E->graph1r) { cudaGraphExecDestroy(E->graph1r); E->graph1r = nullptr; }
     return CO_OK;
 }
 
@@ -772,6 +861,7 @@ int co_step(co_engine* E, int32_t* result) {
 
 int co_run(co_engine* E, int64_t max_steps, int32_t K, int64_t* steps_done) {
     if (!E) return fail(CO_EINVAL, "null argument");
+    { int rw_ = begin_work(E); if (rw_) return rw_; }
     if (E->comm && max_steps <= 0)
         return fail(CO_EINVAL, "with a communicator every rank must run the same fixed number of steps");
     if (K < 1) K = 1;
@@ -827,6 +917,7 @@ int co_run(co_engine* E, int64_t max_steps, int32_t K, int64_t* steps_done) {
 
 int co_preempt(co_engine* E, int64_t idx, int32_t strategy, int64_t now_us, int32_t cause) {
     if (!E || idx < 0 || idx >= E->n) return fail(CO_EINVAL, "bad request index");
+    { int rw_ = begin_work(E); if (rw_) return rw_; }
     k_preempt_one<<<1, 1, 0, E->stream>>>(E->d, (int32_t)idx, strategy, now_us, cause);
     CK(cudaGetLastError());
     return sync_ctl(E);
@@ -942,6 +1033,7 @@ int co_read_token_times(co_engine* E, int64_t* offsets, int64_t* times) {
 
 int co_metrics(co_engine* E, co_metrics_raw* out) {
     if (!E || !out) return fail(CO_EINVAL, "null argument");
+    { int rw_ = begin_work(E); if (rw_) return rw_; }
     const int64_t n = E->n, ntok = std::max<int64_t>(E->tok_total, 1);
     std::memset(out, 0, sizeof(*out));
     if (n == 0) return CO_OK;
@@ -1019,6 +1111,7 @@ int co_metrics(co_engine* E, co_metrics_raw* out) {
 
 int co_check_invariants(co_engine* E) {
     if (!E) return fail(CO_EINVAL, "null argument");
+    { int rw_ = begin_work(E); if (rw_) return rw_; }
     k_check<<<1, NT, 0, E->stream>>>(E->d);
     CK(cudaGetLastError());
     int r = sync_ctl(E);
@@ -1035,6 +1128,7 @@ int co_last_device_ms(co_engine* E, double* ms) {
 
 int co_time_steps(co_engine* E, int32_t k, int64_t flush_bytes, double* step_ms, double* stage_ms) {
     if (!E || k < 1) return fail(CO_EINVAL, "bad arguments");
+    { int rw_ = begin_work(E); if (rw_) return rw_; }
     const int NE = CO_NSTAGES + 1;
     std::vector<cudaEvent_t> evs((size_t)k * NE);
     for (auto& e : evs) CK(cudaEventCreate(&e));
@@ -1129,6 +1223,7 @@ int co_data_stats(co_engine* E, int64_t* st) {
 
 int co_kv_verify(co_engine* E, int64_t* bad, int64_t* checked) {
     if (!E || !bad || !checked) return fail(CO_EINVAL, "null argument");
+    { int rw_ = begin_work(E); if (rw_) return rw_; }
     if (!E->d.dp.on) return fail(CO_EINVAL, "data plane is off (kv_layers = 0)");
     unsigned long long* cnt = nullptr;
     CK(cudaMalloc(&cnt, 16));
@@ -1204,6 +1299,7 @@ int co_host_link_gbs(int64_t bytes, double* d2h, double* h2d) {
 
 int co_set_decode(co_engine* E, int32_t on) {
     if (!E || !E->d.dp.on || !E->d.dp.decode_on) return fail(CO_EINVAL, "decode is not configured");
+    { int rw_ = begin_work(E); if (rw_) return rw_; }
     int32_t v = on ? 1 : 0;
     CK(cudaMemcpyAsync(&E->d.dctl->decode_enabled, &v, 4, cudaMemcpyHostToDevice, E->stream));
     CK(cudaStreamSynchronize(E->stream));
@@ -1216,6 +1312,7 @@ int co_set_decode(co_engine* E, int32_t on) {
 // contents: use a dedicated instance.
 int co_swap_bench(co_engine* E, int64_t ntok, int32_t iters, double* out_ms, double* in_ms) {
     if (!E || !out_ms || !in_ms || iters < 1) return fail(CO_EINVAL, "bad arguments");
+    { int rw_ = begin_work(E); if (rw_) return rw_; }
     DataCfg& x = E->d.dp;
     if (!x.on) return fail(CO_EINVAL, "data plane is off");
     const int bs = E->d.bs;
@@ -1268,6 +1365,7 @@ int co_nccl_unique_id(uint8_t* out) {
 
 int co_attach_nccl(co_engine* E, const uint8_t* uid, int32_t nranks, int32_t rank) {
     if (!E || !uid || nranks < 1 || rank < 0 || rank >= nranks) return fail(CO_EINVAL, "bad arguments");
+    { int rw_ = begin_work(E); if (rw_) return rw_; }
     if (E->comm) return fail(CO_EINVAL, "already attached");
     if (!nccl().ok) return fail(CO_ECUDA, "libnccl.so.2 not loadable");
     ncclUniqueId id;
@@ -1287,6 +1385,7 @@ int co_attach_nccl(co_engine* E, const uint8_t* uid, int32_t nranks, int32_t ran
     E->rank = rank;
     if (E->graph) { cudaGraphExecDestroy(E->graph); E->graph = nullptr; }  // recapture with the collective
     if (E->graph1) { cudaGraphExecDestroy(E->graph1); E->graph1 = nullptr; }
+        if (E->graph1r) { cudaGraphExecDestroy(E->graph1r); E->graph1r = nullptr; }
     return CO_OK;
 }
 
@@ -1302,11 +1401,13 @@ int co_global_reserve(co_engine* E, int64_t* out, int64_t* calls) {
 // development aid: enable/read the %globaltimer phase stamps of k_plan/k_apply
 int co_phase_profile(co_engine* E, int32_t enable, int64_t* out /* 64 */) {
     if (!E) return fail(CO_EINVAL, "null argument");
+    { int rw_ = begin_work(E); if (rw_) return rw_; }
     if (enable && !E->d.prof) {
         CK(cudaMalloc(&E->d.prof, 64 * sizeof(int64_t)));
         CK(cudaMemset(E->d.prof, 0, 64 * sizeof(int64_t)));
         if (E->graph) { cudaGraphExecDestroy(E->graph); E->graph = nullptr; }
         if (E->graph1) { cudaGraphExecDestroy(E->graph1); E->graph1 = nullptr; }
+        if (E->graph1r) { cudaGraphExecDestroy(E->graph1r); E->graph1r = nullptr; }
     }
     if (out && E->d.prof) {
         CK(cudaMemcpyAsync(out, E->d.prof, 64 * sizeof(int64_t), cudaMemcpyDeviceToHost, E->stream));

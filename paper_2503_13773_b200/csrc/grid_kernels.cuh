@@ -11,9 +11,12 @@
 
 namespace co {
 
-__global__ void k_begin(Dev d, int32_t guard) {
+// reset = 1: the host consumed the whole append log from the step mirror
+// (co_engine::drain fast path), so it restarts empty
+__global__ void k_begin(Dev d, int32_t guard, int32_t reset) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     Ctl& c = *d.ctl;
+    if (reset) { c.ev_count = 0; c.mem_count = 0; c.sample_count = 0; c.paused = 0; }
     c.active = 0;
     if (d.result) d.result[0] = -1;
     if (c.done) { c.last_result = 0; return; }

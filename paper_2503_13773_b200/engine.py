@@ -389,6 +389,7 @@ class Engine:
         self.report: Optional[MetricsReport] = None
         self.pool = PoolView(self)
         self._resbuf = None
+        self._evbuf = self._membuf = self._sbuf = None
 
     # -- lifecycle -----------------------------------------------------------
 
@@ -616,22 +617,30 @@ class Engine:
     # -- host views ------------------------------------------------------------
 
     def _drain(self) -> None:
+        """Move the device append log (events, iteration members, utilization
+        samples) into the host lists.  After a step() the library serves it
+        from the step graph's pinned mirror, so this is host-only work."""
         ne, nm = C.c_int64(), C.c_int64()
         N.check(self._lib.co_pending_events(self._h, C.byref(ne), C.byref(nm)), "co_pending_events")
         if ne.value:
-            evs = (N.CoEvent * ne.value)()
-            mem = np.empty(2 * max(nm.value, 1), dtype=np.int32)
+            if self._evbuf is None or len(self._evbuf) < ne.value or len(self._membuf) < 2 * max(nm.value, 1):
+                self._evbuf = (N.CoEvent * max(ne.value, 1024))()
+                self._membuf = np.empty(2 * max(nm.value, 16384), dtype=np.int32)
             got_e, got_m = C.c_int64(), C.c_int64()
-            N.check(self._lib.co_drain_events(self._h, evs, ne.value, _ptr(mem, C.c_int32), nm.value,
-                                              C.byref(got_e), C.byref(got_m)), "co_drain_events")
-            self._events.extend(self._convert(evs, got_e.value, mem))
+            N.check(self._lib.co_drain_events(self._h, self._evbuf, len(self._evbuf), _ptr(self._membuf, C.c_int32),
+                                              len(self._membuf) // 2, C.byref(got_e), C.byref(got_m)),
+                    "co_drain_events")
+            self._events.extend(self._convert(self._evbuf, got_e.value, self._membuf))
+        self._sc = None
         s = self._scalars()
         if s.n_samples:
-            buf = np.empty(2 * s.n_samples, dtype=np.int64)
+            if self._sbuf is None or len(self._sbuf) < 2 * s.n_samples:
+                self._sbuf = np.empty(2 * max(s.n_samples, 1024), dtype=np.int64)
             got = C.c_int64()
-            N.check(self._lib.co_drain_samples(self._h, _ptr(buf, C.c_int64), s.n_samples, C.byref(got)),
-                    "co_drain_samples")
-            self._samples.extend(zip(buf[0:2 * got.value:2].tolist(), buf[1:2 * got.value:2].tolist()))
+            N.check(self._lib.co_drain_samples(self._h, _ptr(self._sbuf, C.c_int64), len(self._sbuf) // 2,
+                                               C.byref(got)), "co_drain_samples")
+            k = got.value
+            self._samples.extend(zip(self._sbuf[0:2 * k:2].tolist(), self._sbuf[1:2 * k:2].tolist()))
         self._sc = None
 
     def _convert(self, evs, n: int, mem: np.ndarray) -> Iterator[dict]:
