@@ -48,11 +48,10 @@ struct ApplySh {
     int32_t n_surv, n_acted, idle;
 };
 
-__global__ void __launch_bounds__(NT, 1) k_apply(Dev d) {
-    pdl_enter();
-    __shared__ ApplySh S;
+// plan application + step remainder (run by k_serial after plan_body; S
+// aliases the planner's shared memory, which is dead by then)
+__device__ __forceinline__ void apply_body(const Dev& d, ApplySh& S) {
     Ctl& c = *d.ctl;
-    if (!c.active) return;
     const int tid = threadIdx.x;
     const int64_t now = c.now;
     const int32_t sid = c.sid;

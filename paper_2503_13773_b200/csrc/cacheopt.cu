@@ -3,9 +3,9 @@
 //
 // Per engine step the stream runs:
 //   k_begin (guards + admission window) -> k_classify (grid: views, classes,
-//   block-ordered running/blown lists, N'_w keys) -> k_bins + k_scatter (grid:
-//   range-adaptive deadline buckets) -> k_plan (1 CTA x 256) -> k_apply
-//   (1 CTA x 256, gated invariant check inside) [-> NCCL reserve all-reduce
+//   block-ordered running/blown lists, the N'_w candidate head) -> k_serial
+//   (1 CTA x 256: the planner, then plan application + the rest of the step,
+//   gated invariant check inside) [-> NCCL reserve all-reduce
 //   on a side stream] [-> k_data -> k_decode_tc05 + k_decode_reduce]
 // co_run captures `steps_per_launch` steps into one CUDA graph and relaunches
 // it; every kernel early-exits once the device control block says the run is
@@ -112,8 +112,7 @@ struct LogMirror {
     int64_t smp[2 * MIR_S];
 };
 
-__global__ void k_mirror(Dev d, LogMirror* m) {
-    pdl_enter();
+__device__ __forceinline__ void mirror_body(const Dev& d, LogMirror* m) {
     const Ctl& c = *d.ctl;
     if (threadIdx.x == 0) m->ctl = c;
     const int64_t ne = c.ev_count, nm = c.mem_count, ns = c.sample_count;
@@ -121,6 +120,25 @@ __global__ void k_mirror(Dev d, LogMirror* m) {
     for (int64_t k = threadIdx.x; k < ne; k += blockDim.x) m->ev[k] = d.events[k];
     for (int64_t k = threadIdx.x; k < 2 * nm; k += blockDim.x) m->mem[k] = d.members[k];
     for (int64_t k = threadIdx.x; k < 2 * ns; k += blockDim.x) m->smp[k] = d.samples[k];
+}
+
+// The step's single-CTA part: MODE 0 = planner only, 1 = apply only (the
+// per-stage timing replay), 2 = planner then apply in one launch; then, when
+// `mir` is set (the step() graph), the control block and the append log into
+// mapped pinned memory.
+template <int MODE>
+__global__ void __launch_bounds__(NT, 1) k_serial(Dev d, LogMirror* mir) {
+    pdl_enter();
+    extern __shared__ __align__(16) uint8_t serial_smem[];
+    if (d.ctl->active) {
+        if (MODE != 1) plan_body(d, *reinterpret_cast<PlanSh*>(serial_smem));
+        if (MODE == 2) __syncthreads();
+        if (MODE != 0) apply_body(d, *reinterpret_cast<ApplySh*>(serial_smem));
+    }
+    if (mir) {
+        __syncthreads();
+        mirror_body(d, mir);
+    }
 }
 
 struct co_engine {
@@ -231,7 +249,8 @@ static void launch_coop(void (*kern)(KArgs...), int grid, int block, cudaStream_
     cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr, int32_t reset = 0) {
+static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr, int32_t reset = 0,
+                       LogMirror* mir = nullptr) {
     Dev& d = E->d;
     cudaStream_t s = E->stream;
     if (ev) mark(ev[0], s);
@@ -242,13 +261,15 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr, i
     const bool pdl = E->pdl;
     launch_pdl(pdl && !ev, k_classify, d.nblk, 256, 0, s, d);
     if (ev) mark(ev[2], s);
-    launch_pdl(pdl && !ev, k_bins, E->grid, 256, 0, s, d);
-    launch_pdl(pdl, k_scatter, E->grid, 256, 0, s, d);
-    if (ev) mark(ev[3], s);
-    launch_pdl(pdl && !ev, k_plan, 1, E->plan_threads, sizeof(PlanSh), s, d);
-    if (ev) mark(ev[4], s);
-    launch_pdl(pdl && !ev, k_apply, 1, E->plan_threads, 0, s, d);
-    if (ev) mark(ev[5], s);
+    if (ev) mark(ev[3], s);  // (no bucket stage: k_classify collects the N'_w head)
+    if (ev) {
+        launch_pdl(false, k_serial<0>, 1, E->plan_threads, sizeof(PlanSh), s, d, (LogMirror*)nullptr);
+        mark(ev[4], s);
+        launch_pdl(false, k_serial<1>, 1, E->plan_threads, sizeof(PlanSh), s, d, (LogMirror*)nullptr);
+        mark(ev[5], s);
+    } else {
+        launch_pdl(pdl, k_serial<2>, 1, E->plan_threads, sizeof(PlanSh), s, d, mir);
+    }
     if (ev) mark(ev[6], s);  // (the validate_every check runs inside k_apply)
     if (E->comm) {
         // global reserve telemetry: overlaps the data plane on a side stream
@@ -553,7 +574,7 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
         d.chunk = (int32_t)chunk;
     }
     AL(d.run_tmp, n); AL(d.blown_tmp, n); AL(d.blk_cnt, 2 * d.nblk + 2); AL(d.crit_idx, n); AL(d.key0, n);
-    AL(d.f0_bin, n); AL(d.hist, NBIN); AL(d.fill, NBIN); AL(d.bin_off, NBIN + 1); AL(d.bucket, n); AL(d.grp_end, n / GRP + 2);
+    AL(d.cand, CAND_CAP);
     AL(d.l_run, n); AL(d.l_blown, n); AL(d.l_nw, n); AL(d.l_nwp, n);
     AL(d.plan, 1);
     AL(d.mem_idx, n3); AL(d.mem_tok, n3);
@@ -668,8 +689,6 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     for (int64_t* p : {d.max_tbt, d.ready_at, d.pstart, d.swap_done, d.ptime, d.rec_seq}) memset_all(p, 0, n8);
     for (int64_t* p : {d.first_tok, d.last_tok, d.first_start, d.completion}) memset_all(p, 0xff, n8);
     memset_all(d.holds, 0, n);
-    memset_all(d.hist, 0, NBIN * 4);
-    memset_all(d.fill, 0, NBIN * 4);
     memset_all(d.seen64, 0, n8);
     memset_all(d.dctl, 0, sizeof(DataCtl));
     if (d.dp.on) {
@@ -709,7 +728,8 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
         co_destroy(E);
         return fail(CO_ECUDA, "ctl upload");
     }
-    cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PlanSh));
+    for (auto k : {k_serial<0>, k_serial<1>, k_serial<2>})
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PlanSh));
     cudaError_t e = cudaStreamSynchronize(E->stream);
     if (e != cudaSuccess) { co_destroy(E); return fail(CO_ECUDA, cudaGetErrorString(e)); }
     *out = E;
@@ -759,10 +779,9 @@ static int ensure_step_graph(co_engine* E) {
         cudaGraph_t g;
         int r;
         CK(cudaStreamBeginCapture(E->stream, cudaStreamCaptureModeThreadLocal));
-        if ((r = launch_step(E, 0, nullptr, reset))) { cudaStreamEndCapture(E->stream, &g); return r; }
-        // the control block and the step's log come back inside the graph:
-        // one launch + one sync per step
-        launch_pdl(E->pdl, k_mirror, 1, 256, 0, E->stream, E->d, E->mir_dev);
+        // the control block and the step's log come back inside the graph
+        // (k_serial's tail): one launch + one sync per step
+        if ((r = launch_step(E, 0, nullptr, reset, E->mir_dev))) { cudaStreamEndCapture(E->stream, &g); return r; }
         CK(cudaStreamEndCapture(E->stream, &g));
         CK(cudaGraphInstantiate(&ge, g, 0));
         cudaGraphDestroy(g);
@@ -1418,7 +1437,9 @@ int co_phase_profile(co_engine* E, int32_t enable, int64_t* out /* 64 */) {
 
 int co_kernels_per_step(co_engine* E, int32_t* n) {
     if (!E || !n) return fail(CO_EINVAL, "null argument");
-    *n = 4;  // begin, classify(+admit), plan, apply(+check); plus the CUB sort passes
+    // begin, classify(+admit, N'_w head), serial (plan + apply + check
+    // [+ mirror]); the data plane adds k_data (+ decode + combine)
+    *n = 3 + (E->d.dp.on ? 1 + (E->d.dp.decode_on ? 2 : 0) : 0);
     return CO_OK;
 }
 

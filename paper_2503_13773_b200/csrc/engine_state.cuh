@@ -22,8 +22,10 @@ __device__ __forceinline__ void pdl_enter() {
 
 constexpr int NT = 256;   // threads of the single-CTA planner / apply kernels (max; 256 measured best)
 constexpr int TCHUNK = 64;  // pages per block-table chunk
-constexpr int NBIN = 4096;  // N'_w deadline buckets
-constexpr int GRP = 64;     // N'_w materialization group (items)
+constexpr int CAND_CAP = 1024;    // candidate head of the keyed N'_w collected by k_classify
+constexpr int CAND_TARGET = 128;  // head size the planner aims the next step's threshold at
+constexpr int XNB = 2048;         // histogram bins of the planner's queue extension
+constexpr int XCHUNK = 2048;      // at most this many items per extension
 constexpr int ST_PENDING = CO_PENDING, ST_WAITING = CO_WAITING, ST_RUNNING = CO_RUNNING,
               ST_PREEMPTED = CO_PREEMPTED, ST_COMPLETED = CO_COMPLETED;
 
@@ -44,6 +46,8 @@ struct Ctl {
     int32_t last_result;                              // step() return value
     int32_t cnt_nw, cnt_nwp, cnt_run;                 // classify counts (N_w, non-blown N'_w, running)
     int32_t cnt_blown;                                // blown N'_w (arrival order)
+    int32_t cnt_cand;                                 // non-blown N'_w with key < thr (k_classify)
+    uint64_t thr;                                     // candidate key bound, set by the planner per step
     uint64_t kmin, kmax;                              // range of the non-blown N'_w keys
     int32_t sid;                                      // stamp id of the current step
     int32_t check_due;
@@ -109,8 +113,8 @@ struct Dev {
     int32_t nblk, chunk;
     int32_t *run_tmp, *blown_tmp, *blk_cnt;
     int32_t* crit_idx;
-    uint64_t* key0;
-    int32_t *f0_bin, *hist, *fill, *bin_off, *bucket, *grp_end;
+    uint64_t* key0;    // waiting-queue key, set when a request starts waiting (wait_key)
+    int32_t* cand;     // this step's candidate head of N'_w (unordered, <= CAND_CAP)
     int32_t *l_run, *l_blown, *l_nw, *l_nwp;
     // plan buffers
     PlanHdr* plan;
@@ -218,6 +222,38 @@ __device__ __forceinline__ double iter_ms(const Dev& d, int64_t tokens) {
 }
 // core.py:21-23 to_us
 __device__ __forceinline__ int64_t to_us_d(double ms) { return (int64_t)floor(__dadd_rn(__dmul_rn(ms, 1000.0), 0.5)); }
+
+// The waiting-queue key of a request, fixed while it waits: set when it
+// becomes WAITING (admission) or PREEMPTED, the only transitions into the
+// waiting states.  CacheOPT (scheduler.py:151-157): (D << idbits | id rank)
+// with D = the deadline, so rt = D - now; the baselines: FCFS by id rank, or
+// rlp's (max(1, predicted - generated) / 50, arrival, id) (scheduler.py:869-873).
+__device__ __forceinline__ uint64_t wait_key(const Dev& d, int32_t i) {
+    if (d.policy == CO_POLICY_CACHEOPT) {
+        const int64_t D = d.first_tok[i] < 0 ? d.arr[i] + d.slo_ttft[i] : d.last_tok[i] + d.slo_tbt[i];
+        return ((uint64_t)D << d.idbits) | (uint64_t)d.idrank[i];
+    }
+    if (d.policy == CO_POLICY_RLP) {
+        const int32_t r = d.pred[i] - d.gen[i];
+        return ((uint64_t)((r > 1 ? r : 1) / 50) << d.idbits) | (uint64_t)d.idrank[i];
+    }
+    return (uint64_t)d.idrank[i];
+}
+
+// Classification of a waiting request (scheduler.py:129-163; baselines
+// scheduler.py:760-766, 869-873) shared by k_classify and the planner's
+// queue extension: N_w (critical), blown N'_w (arrival order) or the keyed
+// N'_w (key order).
+enum WaitClass : int32_t { WC_CRIT = 0, WC_BLOWN = 1, WC_KEYED = 2 };
+__device__ __forceinline__ int32_t wait_class(const Dev& d, int8_t s, uint64_t key, int64_t now, int64_t ti,
+                                              int64_t eps) {
+    if (d.policy != CO_POLICY_CACHEOPT)
+        return (s == ST_PREEMPTED && d.policy != CO_POLICY_RLP) ? WC_BLOWN : WC_KEYED;
+    // every waiting view is ready (engine.py:311-312); rt = D - now
+    const int64_t rt = (int64_t)(key >> d.idbits) - now;
+    if (rt >= -eps && rt - ti < eps) return WC_CRIT;
+    return rt < 0 ? WC_BLOWN : WC_KEYED;
+}
 
 // Planner view of one request (engine.py:284-317 fields the planner reads):
 // one 64-byte record per live request written by k_classify, so the

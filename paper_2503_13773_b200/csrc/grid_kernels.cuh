@@ -41,7 +41,7 @@ __global__ void k_begin(Dev d, int32_t guard, int32_t reset) {
     c.last_result = 0;
     c.sid += 1;
     if (d.dp.on) { d.dctl->n_dec = 0; d.dctl->dec_items = 0; }
-    c.cnt_nw = c.cnt_nwp = c.cnt_run = c.cnt_blown = 0;
+    c.cnt_nw = c.cnt_nwp = c.cnt_run = c.cnt_blown = c.cnt_cand = 0;
     c.kmin = ~0ull;
     c.kmax = 0;
     if (guard) {
@@ -89,6 +89,7 @@ __device__ __forceinline__ void admit_one(const Dev& d, int32_t i, int32_t lo, i
     d.pred[i] = p;
     d.est[i] = e;
     d.state[i] = ST_WAITING;
+    d.key0[i] = wait_key(d, i);
     if (d.record_events) {
         co_event ev;
         ev.kind = CO_EV_ARRIVE; ev.idx = i; ev.t = d.arr[i]; ev.a = ev.b = ev.c = 0;
@@ -96,12 +97,16 @@ __device__ __forceinline__ void admit_one(const Dev& d, int32_t i, int32_t lo, i
     }
 }
 
-// k_classify (contiguous index chunk per block): admission, the planner's
-// 64-byte views, and the classification of scheduler.py:129-163 into
+// k_classify (contiguous index chunk per block): admission, and the
+// classification of scheduler.py:129-163 into
 //   running (index order)              -> run_tmp   (block-ordered)
 //   critical N_w                       -> crit_idx  (unordered; sorted by the planner)
 //   N'_w blown, rt < 0 (arrival order) -> blown_tmp (block-ordered; SoA order IS (arrival, id))
-//   N'_w rt >= 0 ordered by (D, id)    -> key0 = D << idbits | idrank, range kmin..kmax
+//   N'_w rt >= 0 ordered by (D, id)    -> counted (key range kmin..kmax); the head
+//                                         (key < thr) is appended to cand[]
+// The planner's 64-byte views are written for the running, critical, blown
+// and candidate requests only: a waiting request outside the head costs one
+// state byte and one key read per step.
 __global__ void __launch_bounds__(256) k_classify(Dev d) {
     pdl_enter();
     __shared__ int32_t sc[32];
@@ -110,7 +115,7 @@ __global__ void __launch_bounds__(256) k_classify(Dev d) {
     const Ctl& c = *d.ctl;
     if (!c.active) return;
     const int64_t now = c.now, ti = c.t_i, eps = d.eps;
-    const int ib = d.idbits;
+    const uint64_t thr = c.thr;
     const int32_t hi_live = c.next_pending;
     const int32_t alo = c.adm_lo, ahi = c.adm_hi;
     const int64_t ev0 = c.ev_count - (ahi - alo);
@@ -120,60 +125,48 @@ __global__ void __launch_bounds__(256) k_classify(Dev d) {
     uint64_t kmin = ~0ull, kmax = 0;
     for (int32_t c0 = lo; c0 < hi; c0 += 256) {
         const int32_t i = c0 + (int32_t)threadIdx.x;
-        int32_t is_run = 0, is_blown = 0;
+        int32_t is_run = 0, is_blown = 0, is_cand = 0;
         if (i < hi) {
             if (i >= alo && i < ahi) admit_one(d, i, alo, ev0);
-            int32_t f0 = -1;
             if (i < hi_live) {
                 const int8_t s = d.state[i];
-                if (s >= ST_WAITING && s <= ST_PREEMPTED) {
+                bool view = false;
+                if (s == ST_WAITING || s == ST_PREEMPTED) {
+                    const uint64_t k = d.key0[i];
+                    const int32_t wc = wait_class(d, s, k, now, ti, eps);
+                    if (wc == WC_CRIT) {
+                        d.crit_idx[atomicAdd(&d.ctl->cnt_nw, 1)] = i;
+                        ncrit++;
+                        view = true;
+                    } else if (wc == WC_BLOWN) {
+                        is_blown = 1;  // queue key (1, arrival, id)
+                        view = true;
+                    } else {
+                        nf0++;
+                        kmin = k < kmin ? k : kmin;
+                        kmax = k > kmax ? k : kmax;
+                        if (k < thr) { is_cand = 1; view = true; }
+                    }
+                } else if (s == ST_RUNNING) {
+                    is_run = 1;
+                    view = true;
+                }
+                if (view) {
                     const PV v = make_pv(d, i, now);  // the planner's snapshot view
                     uint4* dst = reinterpret_cast<uint4*>(d.views + i);
                     const uint4* src = reinterpret_cast<const uint4*>(&v);
                     dst[0] = src[0]; dst[1] = src[1]; dst[2] = src[2]; dst[3] = src[3];
                 }
-                if ((s == ST_WAITING || s == ST_PREEMPTED) && d.policy != CO_POLICY_CACHEOPT) {
-                    // baseline planners (scheduler.py:760-766, 869-873): FCFS by
-                    // (arrival, id) = id rank with preempted requests first (the
-                    // block-ordered blown list), or rlp's (bucket, arrival, id)
-                    uint64_t k;
-                    if (d.policy == CO_POLICY_RLP) {
-                        const int32_t r = d.pred[i] - d.gen[i];
-                        k = ((uint64_t)((r > 1 ? r : 1) / 50) << ib) | (uint64_t)d.idrank[i];
-                    } else {
-                        k = (uint64_t)d.idrank[i];
-                    }
-                    if (s == ST_PREEMPTED && d.policy != CO_POLICY_RLP) {
-                        is_blown = 1;
-                    } else {
-                        d.key0[i] = k;
-                        f0 = -2;
-                        nf0++;
-                        kmin = k < kmin ? k : kmin;
-                        kmax = k > kmax ? k : kmax;
-                    }
-                } else if (s == ST_WAITING || s == ST_PREEMPTED) {
-                    // every waiting view is ready (engine.py:311-312); rt = D - now
-                    const int64_t D = d.first_tok[i] < 0 ? d.arr[i] + d.slo_ttft[i] : d.last_tok[i] + d.slo_tbt[i];
-                    const int64_t rt = D - now;
-                    if (rt >= -eps && rt - ti < eps) {
-                        d.crit_idx[atomicAdd(&d.ctl->cnt_nw, 1)] = i;
-                        ncrit++;
-                    } else if (rt < 0) {
-                        is_blown = 1;  // queue key (1, arrival, id)
-                    } else {
-                        const uint64_t k = ((uint64_t)D << ib) | (uint64_t)d.idrank[i];  // (0, rt, id)
-                        d.key0[i] = k;
-                        f0 = -2;
-                        nf0++;
-                        kmin = k < kmin ? k : kmin;
-                        kmax = k > kmax ? k : kmax;
-                    }
-                } else if (s == ST_RUNNING) {
-                    is_run = 1;
-                }
             }
-            d.f0_bin[i] = f0;
+        }
+        // the head candidates: one atomic per warp
+        const unsigned cb = __ballot_sync(0xffffffffu, is_cand);
+        if (cb) {
+            int32_t base = 0;
+            if (lane == 0) base = atomicAdd(&d.ctl->cnt_cand, __popc(cb));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            const int32_t pos = base + __popc(cb & ((1u << lane) - 1));
+            if (is_cand && pos < CAND_CAP) d.cand[pos] = i;
         }
         // order-preserving block compaction of the running and blown flags
         int32_t packed = is_run | (is_blown << 16), x = packed;
@@ -230,79 +223,6 @@ __global__ void __launch_bounds__(256) k_classify(Dev d) {
         if (blown_base) atomicAdd(&cm->cnt_blown, blown_base);
         d.blk_cnt[2 * blockIdx.x] = run_base;
         d.blk_cnt[2 * blockIdx.x + 1] = blown_base;
-    }
-}
-
-__device__ __forceinline__ int bin_shift(uint64_t range) {
-    const int bits = range ? 64 - __clzll((long long)range) : 0;
-    return bits > 12 ? bits - 12 : 0;  // (key - kmin) >> shift < NBIN
-}
-
-// histogram of the non-blown N'_w keys over NBIN range-adaptive buckets
-__global__ void __launch_bounds__(256) k_bins(Dev d) {
-    pdl_enter();
-    __shared__ int32_t h[NBIN];
-    const Ctl& c = *d.ctl;
-    if (!c.active || c.cnt_nwp == 0) return;
-    const uint64_t kmin = c.kmin;
-    const int sh = bin_shift(c.kmax - kmin);
-    for (int k = threadIdx.x; k < NBIN; k += blockDim.x) h[k] = 0;
-    __syncthreads();
-    const int32_t n = c.next_pending;
-    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        if (d.f0_bin[i] == -2) {
-            const int32_t b = (int32_t)((d.key0[i] - kmin) >> sh);
-            d.f0_bin[i] = b;
-            atomicAdd(&h[b], 1);
-        }
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < NBIN; k += blockDim.x)
-        if (h[k]) atomicAdd(&d.hist[k], h[k]);
-}
-
-// scatter into bucket order (unordered within a bucket; the planner sorts
-// each bucket group by key when it first needs it)
-__global__ void __launch_bounds__(256) k_scatter(Dev d) {
-    pdl_enter();
-    __shared__ int32_t off[NBIN];
-    __shared__ int32_t wsum[8];
-    const Ctl& c = *d.ctl;
-    if (!c.active || c.cnt_nwp == 0) return;
-    // exclusive prefix of the histogram (16 bins per thread)
-    constexpr int PER = NBIN / 256;
-    int32_t loc[PER], t = 0;
-    for (int q = 0; q < PER; q++) { loc[q] = d.hist[threadIdx.x * PER + q]; t += loc[q]; }
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    int32_t x = t;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) wsum[w] = x;
-    __syncthreads();
-    int32_t wbase = 0;
-    for (int k = 0; k < w; k++) wbase += wsum[k];
-    int32_t run = wbase + x - t;
-    for (int q = 0; q < PER; q++) { off[threadIdx.x * PER + q] = run; run += loc[q]; }
-    __syncthreads();
-    if (blockIdx.x == 0) {
-        for (int k = threadIdx.x; k < NBIN; k += blockDim.x) d.bin_off[k] = off[k];
-        if (threadIdx.x == 0) d.bin_off[NBIN] = c.cnt_nwp;
-        // group ends for the planner's lazy materialization: grp_end[j] is the
-        // first bucket boundary at or after (j+1)*GRP (capped at the total)
-        const int32_t tot = c.cnt_nwp;
-        for (int k = threadIdx.x; k < NBIN; k += blockDim.x) {
-            const int32_t lo = off[k], hi = k + 1 < NBIN ? off[k + 1] : tot;
-            for (int32_t j = lo / GRP; j < hi / GRP; j++) d.grp_end[j] = hi;
-        }
-        if (threadIdx.x == 0 && tot % GRP) d.grp_end[tot / GRP] = tot;
-    }
-    const int32_t n = c.next_pending;
-    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int32_t b = d.f0_bin[i];
-        if (b >= 0) d.bucket[off[b] + atomicAdd(&d.fill[b], 1)] = i;
     }
 }
 

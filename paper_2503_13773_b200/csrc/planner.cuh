@@ -40,7 +40,91 @@ struct PlanSh {
     int64_t f_total, a_total, f_supply, a_supply, tbt_floor, lim, resid;
     int32_t rsvb, n_mem, n_act, n_pre, n_cl, n_def, n_gm, n_pend, n_mready, n_part;
     int32_t k_sel, search, cur, pos, stop, sated, overflow, g_nlive, g_left;
+    // the keyed N'_w materialized so far: l_nwp[0..mat) in key order holds
+    // every keyed item with key < lo_key (then the blown tail)
+    uint64_t lo_key;
+    int32_t cand_done, xcnt, xbest;
+    int32_t xh[XNB];
 };
+
+// Appends to l_nwp[S.mat..) the next keyed N'_w items in key order: every
+// item with key in [S.lo_key, hi), hi chosen from a histogram so that about
+// `want` (at most XCHUNK) items come in.  A block-wide pass over the live
+// slots re-derives membership with k_classify's own wait_class; used when
+// the step needs more of the queue than k_classify's candidate head.
+__device__ int32_t nwp_extend(const Dev& d, PlanSh& S, int32_t want, int64_t now, int64_t ti, int64_t eps) {
+    const Ctl& c = *d.ctl;
+    const int tid = threadIdx.x, bd = (int)blockDim.x;
+    const uint64_t lo = S.lo_key;
+    if (c.cnt_nwp == 0 || lo > c.kmax) return 0;
+    const int32_t n = c.next_pending;
+    uint64_t top = c.kmax, hi;
+    auto keyed = [&](int32_t i, uint64_t& k) -> bool {
+        const int8_t s = d.state[i];
+        if (s != ST_WAITING && s != ST_PREEMPTED) return false;
+        k = d.key0[i];
+        return wait_class(d, s, k, now, ti, eps) == WC_KEYED;
+    };
+    while (true) {
+        const uint64_t range = top - lo;
+        const int bits = range ? 64 - __clzll((long long)range) : 0;
+        const int sh = bits > 11 ? bits - 11 : 0;  // (range >> sh) < XNB
+        for (int k = tid; k < XNB; k += bd) S.xh[k] = 0;
+        __syncthreads();
+        for (int32_t i = tid; i < n; i += bd) {
+            uint64_t k;
+            if (keyed(i, k) && k >= lo && k <= top) atomicAdd(&S.xh[(k - lo) >> sh], 1);
+        }
+        __syncthreads();
+        const int32_t total = blk_scan_smem(S.xh, XNB, S.b);  // exclusive prefix in place
+        uint64_t bst = ~0ull;
+        for (int b = tid; b < XNB; b += bd) {
+            const int32_t incl = b + 1 < XNB ? S.xh[b + 1] : total;
+            if (incl >= want && (uint64_t)b < bst) bst = (uint64_t)b;
+        }
+        bst = blk_min(bst, S.b);
+        const int bs_ = bst == ~0ull ? XNB - 1 : (int)bst;
+        const int32_t incl = bs_ + 1 < XNB ? S.xh[bs_ + 1] : total, excl = S.xh[bs_];
+        __syncthreads();
+        if (incl <= XCHUNK) {
+            hi = bs_ == XNB - 1 ? top + 1 : lo + ((uint64_t)(bs_ + 1) << sh);
+            break;
+        }
+        if (excl > 0) { hi = lo + ((uint64_t)bs_ << sh); break; }
+        top = lo + ((uint64_t)(bs_ + 1) << sh) - 1;  // everything below is empty: refine inside this bin
+    }
+    if (tid == 0) S.xcnt = 0;
+    __syncthreads();
+    const int32_t m0 = S.mat;
+    for (int32_t i = tid; i < n; i += bd) {
+        uint64_t k;
+        if (keyed(i, k) && k >= lo && k < hi) {
+            d.l_nwp[m0 + atomicAdd(&S.xcnt, 1)] = i;
+            const PV v = make_pv(d, i, now);  // its view, as k_classify writes the head's
+            uint4* dst = reinterpret_cast<uint4*>(d.views + i);
+            const uint4* src = reinterpret_cast<const uint4*>(&v);
+            dst[0] = src[0]; dst[1] = src[1]; dst[2] = src[2]; dst[3] = src[3];
+        }
+    }
+    __syncthreads();
+    const int32_t got = S.xcnt;
+    blk_sort_u64(d.l_nwp + m0, got, [&](int32_t i) { return d.key0[i]; }, d, S.b);
+    if (tid == 0) { S.mat = m0 + got; S.lo_key = hi; }
+    __syncthreads();
+    return got;
+}
+
+// the candidate bound for the next step: the key just above the first
+// CAND_TARGET keyed items of this step's queue (thread 0, end of the plan)
+__device__ __forceinline__ void set_next_threshold(const Dev& d, const PlanSh& S, int32_t n_f0) {
+    if (!S.cand_done) return;
+    const int32_t keyed = S.mat < n_f0 ? S.mat : n_f0;
+    uint64_t t;
+    if (keyed >= CAND_TARGET) t = d.key0[d.l_nwp[CAND_TARGET - 1]] + 1;
+    else if (S.lo_key > d.ctl->kmax) t = ~0ull;  // the whole keyed queue is the head
+    else t = S.lo_key;
+    d.ctl->thr = t;
+}
 
 __device__ __forceinline__ void push_act(const Dev& d, PlanSh& S, int32_t kind, int32_t i, int64_t tok,
                                          int32_t nb = 0, int32_t h = -1, int64_t start = 0) {
@@ -492,16 +576,14 @@ __device__ void plan_baseline(const Dev& d, PlanSh& S, const int32_t* RUN, int32
         P.overflow = S.batch_now > d.token_budget ? 1 : 0;
         P.sated = 0;
         P.k_sel = 0;
+        set_next_threshold(d, S, n_f0);
     }
-    for (int32_t k = tid; k < NBIN; k += (int)blockDim.x) { d.hist[k] = 0; d.fill[k] = 0; }
 }
 
-__global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
-    pdl_enter();
-    extern __shared__ __align__(16) uint8_t plan_smem[];
-    PlanSh& S = *reinterpret_cast<PlanSh*>(plan_smem);
+// the planner body (run by k_serial, csrc/cacheopt.cu); all threads call it
+// when the step is active
+__device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
     const Ctl& c = *d.ctl;
-    if (!c.active) return;
     const int tid = threadIdx.x;
     const int64_t now = c.now, ti = c.t_i, eps = d.eps;
     const int32_t sid = c.sid;
@@ -527,7 +609,6 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         S.blkoff[1][b] = d.blk_cnt[2 * b + 1];
     }
     if (tid == 0) {
-        S.mat = 0;
         S.blkoff[0][d.nblk] = 0; S.blkoff[1][d.nblk] = 0;
     }
     __syncthreads();
@@ -548,20 +629,37 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
     blk_sort(d.crit_idx, n_nw, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
         k0 = (uint64_t)(view_of(d, i).rt + (1ll << 62)); k1 = (uint64_t)d.idrank[i]; k2 = 0;
     }, d, S.b);
-    // N'_w (scheduler.py:151-160): rt >= 0 by (D, id) from the buckets, whole
-    // buckets at a time (k_scatter's group ends), then the blown requests in
-    // arrival order.  S.mat is always a bucket boundary below n_f0.
+    // N'_w (scheduler.py:151-160): rt >= 0 by (D, id) -- k_classify's
+    // candidate head sorted on first use, then extensions -- followed by the
+    // blown requests in arrival order.  l_nwp[0..S.mat) is always exact.
+    if (tid == 0) { S.cand_done = 0; S.lo_key = 0; S.mat = 0; }
+    __syncthreads();
     auto ensure = [&](int32_t target) {
         if (target > n_nwp) target = n_nwp;
+        if (S.mat >= target) return;
+        if (!S.cand_done) {
+            const int32_t nc = c.cnt_cand;
+            if (nc <= CAND_CAP) {
+                for (int32_t k = tid; k < nc; k += (int)blockDim.x) d.l_nwp[k] = d.cand[k];
+                __syncthreads();
+                blk_sort_u64(d.l_nwp, nc, [&](int32_t i) { return d.key0[i]; }, d, S.b);
+                if (tid == 0) { S.mat = nc; S.lo_key = c.thr; }
+            }  // (an overflowed head is ignored: extensions start from key 0)
+            if (tid == 0) S.cand_done = 1;
+            __syncthreads();
+        }
         while (S.mat < target) {
             const int32_t m0 = S.mat;
             if (m0 < n_f0) {
-                const int32_t want = target < n_f0 ? target : n_f0;
-                const int32_t end = d.grp_end[(want - 1) / GRP], g = end - m0;
-                for (int32_t k = tid; k < g; k += (int)blockDim.x) d.l_nwp[m0 + k] = d.bucket[m0 + k];
-                __syncthreads();
-                blk_sort_u64(d.l_nwp + m0, g, [&](int32_t i) { return d.key0[i]; }, d, S.b);
-                if (tid == 0) S.mat = end;
+                int32_t want = target - m0;
+                const int32_t geo = m0 > CAND_TARGET ? m0 : CAND_TARGET;  // geometric growth
+                want = want > geo ? want : geo;
+                want = want < XCHUNK ? want : XCHUNK;
+                if (nwp_extend(d, S, want, now, ti, eps) == 0) {
+                    if (tid == 0) { d.ctl->error = 10; d.ctl->err_info[0] = m0; d.ctl->err_info[1] = n_f0; }
+                    __syncthreads();
+                    return;
+                }
             } else {
                 for (int32_t k = tid; k < n_blown; k += (int)blockDim.x) d.l_nwp[m0 + k] = d.l_blown[k];
                 if (tid == 0) S.mat = m0 + n_blown;
@@ -1112,7 +1210,20 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
             };
             int f = 0;
             for (int32_t k = k_sel + tid; k < S.mat; k += (int)blockDim.x) f |= feas(NWP[k]);
-            for (int32_t k = S.mat + tid; k < n_f0; k += (int)blockDim.x) f |= feas(d.bucket[k]);
+            if (S.mat < n_f0) {
+                // the keyed items not materialized yet (key >= lo_key): no views
+                // were written for them, so they are derived on the spot
+                const uint64_t lo = S.lo_key;
+                for (int32_t i = tid; i < c.next_pending; i += (int)blockDim.x) {
+                    const int8_t s = d.state[i];
+                    if (s != ST_WAITING && s != ST_PREEMPTED) continue;
+                    const uint64_t k = d.key0[i];
+                    if (k < lo || wait_class(d, s, k, now, ti, eps) != WC_KEYED) continue;
+                    const PV v = make_pv(d, i, now);
+                    const int64_t t = (int64_t)v.target - v.eff;
+                    f |= t > 0 && pv_cost(v, t, bs) <= room0;
+                }
+            }
             if (S.mat <= n_f0)
                 for (int32_t k = tid; k < n_blown; k += (int)blockDim.x) f |= feas(d.l_blown[k]);
             if (!__syncthreads_or(f) && tid == 0) S.stop = 1;
@@ -1163,8 +1274,8 @@ __global__ void __launch_bounds__(NT, 1) k_plan(Dev d) {
         P.overflow = (S.overflow || S.batch_now > d.token_budget) ? 1 : 0;
         P.sated = S.sated;
         P.k_sel = k_sel;
+        set_next_threshold(d, S, n_f0);
     }
-    for (int32_t k = tid; k < NBIN; k += (int)blockDim.x) { d.hist[k] = 0; d.fill[k] = 0; }
     prof_mark(d, 15);
 }
 

@@ -213,6 +213,7 @@ __device__ __forceinline__ bool live_state(int8_t s) { return s >= ST_WAITING &&
 __device__ void do_preempt(const Dev& d, int i, int32_t strat, int64_t now, int32_t cause) {
     if (d.state[i] != ST_RUNNING) return;
     d.state[i] = ST_PREEMPTED;
+    d.key0[i] = wait_key(d, i);  // its waiting-queue key (D = last token + TBT SLO)
     d.pcount[i] += 1;
     d.last_strat[i] = (int8_t)strat;
     int32_t u = d.used[i];
