@@ -84,14 +84,6 @@ static int fail(int code, const std::string& msg) {
 __global__ void k_preempt_one(Dev d, int32_t i, int32_t strat, int64_t now, int32_t cause) {
     if (threadIdx.x == 0 && blockIdx.x == 0) do_preempt(d, i, strat, now, cause);
 }
-// N4: this instance's [free_tokens, reserved_blocks_current] (kvc.py:92-98,
-// :79) into the all-reduce send buffer, every step whether or not it ran
-__global__ void k_reserve_pack(Dev d, int64_t* send) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        send[0] = free_tokens(d);
-        send[1] = d.ctl->rsv_cur;
-    }
-}
 __global__ void k_reset_drained(Dev d, int64_t ev, int64_t mem, int64_t smp) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         d.ctl->ev_count -= ev;
@@ -126,8 +118,11 @@ __device__ __forceinline__ void mirror_body(const Dev& d, LogMirror* m) {
 // per-stage timing replay), 2 = planner then apply in one launch; then, when
 // `mir` is set (the step() graph), the control block and the append log into
 // mapped pinned memory.
+// `pack` (a communicator is attached): N4's send slot for this step, filled
+// with the instance's [free_tokens, reserved_blocks_current] (kvc.py:92-98,
+// :79) after apply, every step whether or not it ran.
 template <int MODE>
-__global__ void __launch_bounds__(NT, 1) k_serial(Dev d, LogMirror* mir) {
+__global__ void __launch_bounds__(NT, 1) k_serial(Dev d, LogMirror* mir, int64_t* pack) {
     pdl_enter();
     extern __shared__ __align__(16) uint8_t serial_smem[];
     if (d.ctl->active) {
@@ -135,10 +130,12 @@ __global__ void __launch_bounds__(NT, 1) k_serial(Dev d, LogMirror* mir) {
         if (MODE == 2) __syncthreads();
         if (MODE != 0) apply_body(d, *reinterpret_cast<ApplySh*>(serial_smem));
     }
-    if (mir) {
-        __syncthreads();
-        mirror_body(d, mir);
+    if (mir || (pack && MODE != 0)) __syncthreads();
+    if (pack && MODE != 0 && threadIdx.x == 0) {
+        pack[0] = free_tokens(d);
+        pack[1] = d.ctl->rsv_cur;
     }
+    if (mir) mirror_body(d, mir);
 }
 
 struct co_engine {
@@ -164,8 +161,10 @@ struct co_engine {
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0;
     cudaStream_t side = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
-    int64_t* red = nullptr;  // [send 2][recv 2]
+    cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
+    int64_t* red = nullptr;  // two slots of [send 2][recv 2]; step j of a sequence uses slot j & 1
+    int join_pending = -1;   // slot whose all-reduce the compute stream has not joined yet
+    int last_slot = 0;       // slot of the last all-reduce enqueued (co_global_reserve)
     int64_t reduce_calls = 0;
     CUtensorMap kvmap;
     cudaGraphExec_t graph1 = nullptr;   // one step, step() semantics
@@ -249,10 +248,20 @@ static void launch_coop(void (*kern)(KArgs...), int grid, int block, cudaStream_
     cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// N4's all-reduce runs on the side stream; with `defer` the compute stream
+// joins it only at the end of the NEXT step (the totals never
+// feed a decision), so a step's collective latency hides behind the next
+// step.  Every sequence ends with flush_join (a capture must rejoin its fork).
+static void flush_join(co_engine* E) {
+    if (E->comm && E->join_pending >= 0) cudaStreamWaitEvent(E->stream, E->join[E->join_pending], 0);
+    E->join_pending = -1;
+}
+
 static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr, int32_t reset = 0,
-                       LogMirror* mir = nullptr) {
+                       LogMirror* mir = nullptr, int slot = 0, bool defer = false) {
     Dev& d = E->d;
     cudaStream_t s = E->stream;
+    int64_t* pack = E->comm ? E->red + 4 * slot : nullptr;
     if (ev) mark(ev[0], s);
     k_begin<<<1, 32, 0, s>>>(d, guard, reset);
     if (ev) mark(ev[1], s);
@@ -263,22 +272,23 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr, i
     if (ev) mark(ev[2], s);
     if (ev) mark(ev[3], s);  // (no bucket stage: k_classify collects the N'_w head)
     if (ev) {
-        launch_pdl(false, k_serial<0>, 1, E->plan_threads, sizeof(PlanSh), s, d, (LogMirror*)nullptr);
+        launch_pdl(false, k_serial<0>, 1, E->plan_threads, sizeof(PlanSh), s, d, (LogMirror*)nullptr,
+                   (int64_t*)nullptr);
         mark(ev[4], s);
-        launch_pdl(false, k_serial<1>, 1, E->plan_threads, sizeof(PlanSh), s, d, (LogMirror*)nullptr);
+        launch_pdl(false, k_serial<1>, 1, E->plan_threads, sizeof(PlanSh), s, d, (LogMirror*)nullptr, pack);
         mark(ev[5], s);
     } else {
-        launch_pdl(pdl, k_serial<2>, 1, E->plan_threads, sizeof(PlanSh), s, d, mir);
+        launch_pdl(pdl, k_serial<2>, 1, E->plan_threads, sizeof(PlanSh), s, d, mir, pack);
     }
     if (ev) mark(ev[6], s);  // (the validate_every check runs inside k_apply)
     if (E->comm) {
         // global reserve telemetry: overlaps the data plane on a side stream
         cudaEventRecord(E->fork, s);
         cudaStreamWaitEvent(E->side, E->fork, 0);
-        k_reserve_pack<<<1, 32, 0, E->side>>>(d, E->red);
-        ncclResult_t nr = nccl().allReduce(E->red, E->red + 2, 2, ncclInt64, ncclSum, E->comm, E->side);
+        ncclResult_t nr = nccl().allReduce(pack, pack + 2, 2, ncclInt64, ncclSum, E->comm, E->side);
         if (nr != ncclSuccess) return fail(CO_ECUDA, std::string("ncclAllReduce: ") + nccl().errorString(nr));
-        cudaEventRecord(E->join, E->side);
+        cudaEventRecord(E->join[slot], E->side);
+        E->last_slot = slot;
     }
     if (d.dp.on) {
         launch_coop(k_data, E->sms, 512, s, d, d.dp, d.dctl, 0);
@@ -299,7 +309,11 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr, i
         mark(ev[7], s);
         mark(ev[8], s);
     }
-    if (E->comm) cudaStreamWaitEvent(s, E->join, 0);
+    if (E->comm) {
+        flush_join(E);  // the previous step's collective (deferred) ...
+        E->join_pending = slot;
+        if (!defer) flush_join(E);  // ... and this one's unless deferred to the next step
+    }
     return CO_OK;
 }
 
@@ -411,7 +425,8 @@ int co_destroy(co_engine* E) {
     if (E->comm) nccl().commDestroy(E->comm);
     if (E->side) cudaStreamDestroy(E->side);
     if (E->fork) cudaEventDestroy(E->fork);
-    if (E->join) cudaEventDestroy(E->join);
+    for (cudaEvent_t j : E->join)
+        if (j) cudaEventDestroy(j);
     if (E->red) cudaFree(E->red);
     if (E->d.prof) cudaFree(E->d.prof);
     for (void* p : E->allocs) cudaFree(p);
@@ -781,7 +796,11 @@ static int ensure_step_graph(co_engine* E) {
         CK(cudaStreamBeginCapture(E->stream, cudaStreamCaptureModeThreadLocal));
         // the control block and the step's log come back inside the graph
         // (k_serial's tail): one launch + one sync per step
-        if ((r = launch_step(E, 0, nullptr, reset, E->mir_dev))) { cudaStreamEndCapture(E->stream, &g); return r; }
+        if ((r = launch_step(E, 0, nullptr, reset, E->mir_dev))) {
+            flush_join(E);
+            cudaStreamEndCapture(E->stream, &g);
+            return r;
+        }
         CK(cudaStreamEndCapture(E->stream, &g));
         CK(cudaGraphInstantiate(&ge, g, 0));
         cudaGraphDestroy(g);
@@ -795,6 +814,7 @@ static int launch_step1(co_engine* E) {
     touch(E);
     if (E->timing) CK(cudaEventRecord(E->ev0, E->stream));
     CK(cudaGraphLaunch(E->reset_pending ? E->graph1r : E->graph1, E->stream));
+    E->last_slot = 0;
     E->reset_pending = false;
     if (E->comm) E->reduce_calls += 1;
     if (E->timing) CK(cudaEventRecord(E->ev1, E->stream));
@@ -892,8 +912,13 @@ int co_run(co_engine* E, int64_t max_steps, int32_t K, int64_t* steps_done) {
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(E->stream, cudaStreamCaptureModeThreadLocal));
         for (int k = 0; k < K; k++) {
-            if ((r = launch_step(E, 1))) { cudaStreamEndCapture(E->stream, &g); return r; }
+            if ((r = launch_step(E, 1, nullptr, 0, nullptr, k & 1, true))) {
+                flush_join(E);
+                cudaStreamEndCapture(E->stream, &g);
+                return r;
+            }
         }
+        flush_join(E);
         CK(cudaStreamEndCapture(E->stream, &g));
         CK(cudaGraphInstantiate(&E->graph, g, 0));
         cudaGraphDestroy(g);
@@ -914,6 +939,7 @@ int co_run(co_engine* E, int64_t max_steps, int32_t K, int64_t* steps_done) {
             launched += 1;
         } else {
             CK(cudaGraphLaunch(E->graph, E->stream));
+            E->last_slot = (K - 1) & 1;
             launched += K;
         }
         if (E->comm) E->reduce_calls += single ? 1 : K;
@@ -1163,17 +1189,19 @@ int co_time_steps(co_engine* E, int32_t k, int64_t flush_bytes, double* step_ms,
         if (flush) cudaMemsetAsync(flush, j & 0xff, flush_bytes, E->stream);
         cudaEvent_t* e = evs.data() + (size_t)j * NE;
         if (stages) {
-            r = launch_step(E, 1, e);
+            r = launch_step(E, 1, e, 0, nullptr, j & 1, true);
         } else {
             mark(e[0], E->stream);
-            r = launch_step(E, 1, nullptr);
+            r = launch_step(E, 1, nullptr, 0, nullptr, j & 1, true);
             mark(e[NE - 1], E->stream);
         }
     }
+    flush_join(E);  // (the last step's collective is joined after its end event)
     CK(cudaStreamEndCapture(E->stream, &g));
     if (!r) {
         CK(cudaGraphInstantiate(&ge, g, 0));
         CK(cudaGraphLaunch(ge, E->stream));
+        E->last_slot = (k - 1) & 1;
         if (E->comm) E->reduce_calls += k;
         CK(cudaStreamSynchronize(E->stream));
         if (stages)
@@ -1397,9 +1425,10 @@ int co_attach_nccl(co_engine* E, const uint8_t* uid, int32_t nranks, int32_t ran
     }
     CK(cudaStreamCreateWithFlags(&E->side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&E->fork, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&E->join, cudaEventDisableTiming));
-    CK(cudaMalloc(&E->red, 4 * sizeof(int64_t)));
-    CK(cudaMemset(E->red, 0, 4 * sizeof(int64_t)));
+    CK(cudaEventCreateWithFlags(&E->join[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&E->join[1], cudaEventDisableTiming));
+    CK(cudaMalloc(&E->red, 8 * sizeof(int64_t)));
+    CK(cudaMemset(E->red, 0, 8 * sizeof(int64_t)));
     E->nranks = nranks;
     E->rank = rank;
     if (E->graph) { cudaGraphExecDestroy(E->graph); E->graph = nullptr; }  // recapture with the collective
@@ -1412,7 +1441,7 @@ int co_global_reserve(co_engine* E, int64_t* out, int64_t* calls) {
     if (!E || !out) return fail(CO_EINVAL, "null argument");
     if (!E->comm) return fail(CO_EINVAL, "no communicator attached");
     CK(cudaStreamSynchronize(E->side));
-    CK(cudaMemcpy(out, E->red + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out, E->red + 4 * E->last_slot + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
     if (calls) *calls = E->reduce_calls;
     return CO_OK;
 }
