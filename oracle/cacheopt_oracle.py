@@ -1156,6 +1156,12 @@ class CacheOptOracle:
                     actions.append(("grow" if self.holds[i] else "allocate", i, int(needs[x]), 0, -1, 0))
                     free -= int(costs[x])
                     pos = x + 1
+        if getattr(self, "debug_sizes", None) is not None:  # development aid: per-step set sizes
+            self.debug_sizes.append(dict(
+                running=len(running_all), n_w=len(n_w), n_r=len(n_r), n_rp=len(n_rp), triples=len(triples),
+                n_wp=len(n_wp_arr), pending=len(pending_nw), victims=len(preempt), deferred=len(deferred),
+                selected=len(selected), parts=len(parts), pro=len(pro), fulfilled=len(fulfilled), sated=sated,
+                claims=len(claims), actions=len(actions), members=len(members), granted_members=len(granted_members)))
         return dict(members=members, preempt=preempt, actions=actions, claims=claims,
                     deferred=deferred, overflow=overflow or sum(t for _, t in members) > budget,
                     batch_tokens=sum(t for _, t in members))

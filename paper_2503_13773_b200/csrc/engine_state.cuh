@@ -209,12 +209,17 @@ __device__ __forceinline__ int32_t strategy_of(const Dev& d, int i) {
 __device__ __forceinline__ int64_t lut(const int64_t* t, int64_t s, int64_t smax) {
     return t[s < smax ? s : smax];
 }
+// %globaltimer phase stamps (tools/phase_timeline.py); compiled in only for
+// development builds (CACHEOPT_NVCC_EXTRA=-DCO_PHASE_PROF): every stamp site
+// is executed code the step fetches after an L2 flush
 __device__ __forceinline__ void prof_mark(const Dev& d, int slot) {
+#ifdef CO_PHASE_PROF
     if (d.prof && threadIdx.x == 0) {
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         d.prof[slot] = (int64_t)t;
     }
+#endif
 }
 // costmodel.py:51-55 iteration_latency in IEEE double, no contraction
 __device__ __forceinline__ double iter_ms(const Dev& d, int64_t tokens) {

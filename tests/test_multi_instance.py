@@ -81,6 +81,8 @@ def test_one_rank_nccl_reserve_matches_instance(cuda_ok):
     for _ in range(200):
         orc.step()
     assert eng.events == orc.events  # telemetry never changes a decision
+    # the multi-step graph's deferred joins: the last slot holds the last step's totals
+    assert eng.global_reserve()[:2] == (orc.free_tokens(), orc.rsv_cur)
     assert eng.global_reserve()[2] > 0
 
 
@@ -99,5 +101,6 @@ def test_collective_mode_runs_fixed_step_counts_past_the_end(cuda_ok):
     eng.run_steps(total + 100)
     free, rsv, calls = eng.global_reserve()
     assert calls >= total + 100
+    assert (free, rsv) == (orc.free_tokens(), orc.rsv_cur)
     assert eng.events == orc.events
     assert eng.step_result()[0] is False  # finished, and still enqueues its collective
