@@ -28,6 +28,7 @@ extern "C" {
 #define CO_EINVAL 1
 #define CO_ECUDA 2
 #define CO_EDEVICE 3
+#define CO_EAGAIN 4  /* caller buffers too small; the sizes needed were returned */
 
 /* lifecycle codes (core.py:26-30); PENDING = not yet arrived */
 #define CO_PENDING 0
@@ -215,12 +216,22 @@ int co_preempt(co_engine* eng, int64_t idx, int32_t strategy, int64_t now_us, in
 /* Blocking readbacks into caller-owned host buffers. */
 int co_get_scalars(co_engine* eng, co_scalars* out);
 int co_read_field(co_engine* eng, int32_t field, int64_t* out /* n values */);
+/* Undrained append-log sizes in one call: out[0] events, out[1] iteration
+ * members, out[2] utilization samples (the counts co_pending_events and
+ * co_get_scalars' n_samples report). */
+int co_pending_log(co_engine* eng, int64_t* out /* 3 */);
 /* Drains up to max_events events (and their iter member streams) into the
  * caller's buffers; returns counts.  members: (idx, tokens) int32 pairs. */
 int co_drain_events(co_engine* eng, co_event* events, int64_t max_events,
                     int32_t* members, int64_t max_members,
                     int64_t* n_events, int64_t* n_members);
 int co_pending_events(co_engine* eng, int64_t* n_events, int64_t* n_members);
+/* The whole append log in one call: events (+ their iteration members) and
+ * utilization samples.  counts[3] = {events, members, samples} drained; if a
+ * buffer is too small nothing is drained, counts holds the sizes needed and
+ * the return is CO_EAGAIN. */
+int co_drain_log(co_engine* eng, co_event* events, int64_t max_events, int32_t* members, int64_t max_members,
+                 int64_t* samples, int64_t max_samples, int64_t* counts);
 /* per-iteration (footprint, used) samples (engine.py:636), drained */
 int co_drain_samples(co_engine* eng, int64_t* out /* 2 per sample */, int64_t max, int64_t* n);
 /* token timestamps: offsets[n+1] and the Σ true_output_len slab; callers

@@ -17,6 +17,7 @@ NSTAGES = 8
 STAGES = ("begin+admit", "classify", "bucket", "plan", "apply", "check", "data", "decode")
 
 EV_ARRIVE, EV_ADMIT, EV_ITER, EV_PREEMPT, EV_READMIT, EV_COMPLETE = range(6)
+CO_EAGAIN = 4  # co_drain_log: buffers too small, sizes returned
 CAUSES = ("plan", "squeeze", "collision")
 
 FIELDS = ("STATE GENERATED USED KV_NEED PREFILL_DONE PREEMPTION_COUNT PREEMPTION_TIME "
@@ -82,7 +83,7 @@ class CoEvent(C.Structure):
 
 EXPORTS = (
     "co_create", "co_destroy", "co_step", "co_run", "co_preempt", "co_get_scalars", "co_read_field",
-    "co_drain_events", "co_pending_events", "co_drain_samples", "co_read_token_times",
+    "co_drain_events", "co_pending_events", "co_pending_log", "co_drain_log", "co_drain_samples", "co_read_token_times",
     "co_check_invariants", "co_last_device_ms", "co_kernels_per_step", "co_time_steps", "co_last_error",
     "co_version", "co_read_block_tables", "co_data_stats", "co_kv_verify", "co_read_decode", "co_host_link_gbs",
     "co_set_decode", "co_swap_bench", "co_nccl_unique_id", "co_attach_nccl", "co_global_reserve",
@@ -144,6 +145,8 @@ def load() -> C.CDLL:
         "co_read_field": (C.c_int, [V, C.c_int32, I64P]),
         "co_drain_events": (C.c_int, [V, C.POINTER(CoEvent), C.c_int64, I32P, C.c_int64, I64P, I64P]),
         "co_pending_events": (C.c_int, [V, I64P, I64P]),
+        "co_pending_log": (C.c_int, [V, I64P]),
+        "co_drain_log": (C.c_int, [V, C.POINTER(CoEvent), C.c_int64, I32P, C.c_int64, I64P, C.c_int64, I64P]),
         "co_drain_samples": (C.c_int, [V, I64P, C.c_int64, I64P]),
         "co_read_token_times": (C.c_int, [V, I64P, I64P]),
         "co_check_invariants": (C.c_int, [V]),

@@ -54,6 +54,7 @@ struct Ctl {
     int32_t free_top;                                 // N1: pages on the free stack
     int32_t chunk_top;                                // N1: free table chunks
     int32_t err_info[4];
+    uint64_t mir_seq;                                 // step mirrors written (mapped completion flag)
 };
 
 // The plan of one step (scheduler.py:295-323 BatchPlan) as device lists.

@@ -26,6 +26,7 @@ from .hostprep import (bin_of, charge_luts, iteration_us, run_confidence, run_pa
                        sweet_spot)
 
 STRATEGY_CODE = {Strategy.SWAP: 0, Strategy.RECOMPUTE: 1}
+
 CAUSE_CODE = {"plan": 0, "squeeze": 1, "collision": 2}
 
 
@@ -390,6 +391,10 @@ class Engine:
         self.pool = PoolView(self)
         self._resbuf = None
         self._evbuf = self._membuf = self._sbuf = None
+        self._drain_args = None
+        self._rid_np = np.array(self._rid, dtype=np.int64)
+        self._pend = np.zeros(3, dtype=np.int64)
+        self._pend_p = _ptr(self._pend, C.c_int64)
 
     # -- lifecycle -----------------------------------------------------------
 
@@ -446,7 +451,6 @@ class Engine:
         (step()'s bool, int32 array [m, 2] of (req_id, tokens) that ran, end_us)."""
         if self._resbuf is None:
             self._resbuf = np.empty(2 * (3 * self._n + 64), dtype=np.int32)
-            self._rid_np = np.array(self._rid, dtype=np.int64)
             self._sr_out = (C.c_int32(), C.c_int64(), C.c_int64())
             r, n, end = self._sr_out
             self._sr_args = (self._h, C.byref(r), _ptr(self._resbuf, C.c_int32), len(self._resbuf) // 2,
@@ -618,51 +622,58 @@ class Engine:
 
     def _drain(self) -> None:
         """Move the device append log (events, iteration members, utilization
-        samples) into the host lists.  After a step() the library serves it
-        from the step graph's pinned mirror, so this is host-only work."""
-        ne, nm = C.c_int64(), C.c_int64()
-        N.check(self._lib.co_pending_events(self._h, C.byref(ne), C.byref(nm)), "co_pending_events")
-        if ne.value:
-            if self._evbuf is None or len(self._evbuf) < ne.value or len(self._membuf) < 2 * max(nm.value, 1):
-                self._evbuf = (N.CoEvent * max(ne.value, 1024))()
-                self._membuf = np.empty(2 * max(nm.value, 16384), dtype=np.int32)
-            got_e, got_m = C.c_int64(), C.c_int64()
-            N.check(self._lib.co_drain_events(self._h, self._evbuf, len(self._evbuf), _ptr(self._membuf, C.c_int32),
-                                              len(self._membuf) // 2, C.byref(got_e), C.byref(got_m)),
-                    "co_drain_events")
-            self._events.extend(self._convert(self._evbuf, got_e.value, self._membuf))
-        self._sc = None
-        s = self._scalars()
-        if s.n_samples:
-            if self._sbuf is None or len(self._sbuf) < 2 * s.n_samples:
-                self._sbuf = np.empty(2 * max(s.n_samples, 1024), dtype=np.int64)
-            got = C.c_int64()
-            N.check(self._lib.co_drain_samples(self._h, _ptr(self._sbuf, C.c_int64), len(self._sbuf) // 2,
-                                               C.byref(got)), "co_drain_samples")
-            k = got.value
-            self._samples.extend(zip(self._sbuf[0:2 * k:2].tolist(), self._sbuf[1:2 * k:2].tolist()))
+        samples) into the host lists in one library call.  After a step() the
+        library serves it from the step graph's pinned mirror, so this is
+        host-only work."""
+        cnt = self._pend
+        while True:
+            if self._evbuf is None:
+                ne, nm, ns = (max(1024, int(x)) for x in cnt)
+                self._evbuf = (N.CoEvent * ne)()
+                self._membuf = np.empty(2 * max(nm, 16384), dtype=np.int32)
+                self._sbuf = np.empty(2 * ns, dtype=np.int64)
+                self._drain_args = (self._h, self._evbuf, len(self._evbuf), _ptr(self._membuf, C.c_int32),
+                                    len(self._membuf) // 2, _ptr(self._sbuf, C.c_int64), len(self._sbuf) // 2,
+                                    self._pend_p)
+            rc = self._lib.co_drain_log(*self._drain_args)
+            if rc != N.CO_EAGAIN:
+                break
+            self._evbuf = None  # grow to the sizes returned in cnt and retry
+        N.check(rc, "co_drain_log")
+        ne, ns = int(cnt[0]), int(cnt[2])
+        if ne:
+            self._events.extend(self._convert(ne, self._membuf))
+        if ns:
+            it = iter(self._sbuf[:2 * ns].tolist())
+            self._samples.extend(zip(it, it))
         self._sc = None
 
-    def _convert(self, evs, n: int, mem: np.ndarray) -> Iterator[dict]:
+    def _convert(self, n: int, mem: np.ndarray) -> List[dict]:
+        """Device event records -> the reference's event dicts (engine.py:
+        353, 376-383, 407, 512-518, 533)."""
         rid = self._rid
+        evs = self._evbuf
+        out = []
+        app = out.append
         for k in range(n):
             e = evs[k]
             kind = e.kind
-            if kind == N.EV_ARRIVE:
-                yield {"ev": "arrive", "t": e.t, "req": rid[e.idx]}
-            elif kind == N.EV_ITER:
-                m = mem[2 * e.c: 2 * (e.c + e.idx)].tolist()
-                yield {"ev": "iter", "t": e.t, "end": e.a, "tokens": e.b,
-                       "members": [[rid[m[j]], m[j + 1]] for j in range(0, len(m), 2)]}
+            if kind == N.EV_ITER:
+                lo = 2 * e.c
+                it = iter(mem[lo:lo + 2 * e.idx].tolist())
+                app({"ev": "iter", "t": e.t, "end": e.a, "tokens": e.b, "members": [[rid[x], y] for x, y in zip(it, it)]})
+            elif kind == N.EV_ARRIVE:
+                app({"ev": "arrive", "t": e.t, "req": rid[e.idx]})
             elif kind == N.EV_ADMIT:
-                yield {"ev": "admit", "t": e.t, "req": rid[e.idx]}
+                app({"ev": "admit", "t": e.t, "req": rid[e.idx]})
             elif kind == N.EV_PREEMPT:
-                yield {"ev": "preempt", "t": e.t, "req": rid[e.idx],
-                       "strategy": STRATEGY_FROM_CODE[e.b].value, "kv": e.a, "cause": N.CAUSES[e.c]}
+                app({"ev": "preempt", "t": e.t, "req": rid[e.idx],
+                     "strategy": STRATEGY_FROM_CODE[e.b].value, "kv": e.a, "cause": N.CAUSES[e.c]})
             elif kind == N.EV_READMIT:
-                yield {"ev": "readmit", "t": e.t, "req": rid[e.idx], "ready_at": e.a}
+                app({"ev": "readmit", "t": e.t, "req": rid[e.idx], "ready_at": e.a})
             else:
-                yield {"ev": "complete", "t": e.t, "req": rid[e.idx]}
+                app({"ev": "complete", "t": e.t, "req": rid[e.idx]})
+        return out
 
     @property
     def events(self) -> List[dict]:
