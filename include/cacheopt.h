@@ -64,7 +64,7 @@ extern "C" {
 typedef struct co_config {
     int64_t capacity_tokens;        /* engine.py:67 */
     int32_t reserved_blocks;        /* engine.py:68 */
-    int32_t allow_stacking;         /* engine.py:69; must be 0 (EINVAL otherwise) */
+    int32_t allow_stacking;         /* engine.py:69, kvc.py:64: several guests per host */
     int32_t block_size;             /* small_block_b, engine.py:236 */
     int32_t buffer_b;               /* scheduler.py:41 */
     int32_t token_budget;           /* scheduler.py:39 */
@@ -369,6 +369,73 @@ int co_gen_predictor(int64_t n, const co_predictor_spec* spec, uint64_t seed, in
 
 const char* co_last_error(void);
 const char* co_version(void);
+
+/* ---- kvc.BlockPool on the device (kvc.py:55-375) ---------------------------
+ * A standalone record table in HBM driven by the engine's own pool functions
+ * (csrc/pool_api.cuh); records are addressed by slot (the host maps request
+ * ids to slots).  co_pool_op: op = CO_POOL_*, a/b/c as listed; out[3]:
+ * out[0] > 0 Grant(out[1] tokens, out[2] footprint) or release's net tokens
+ * in out[1]; out[0] == 0 Shortfall(missing = out[1]); out[0] < 0 the
+ * contract violation -CO_PV_* (the reference's ValueError). */
+typedef struct co_pool co_pool;
+enum { CO_POOL_ALLOCATE = 0,        /* a = n_tokens                       kvc.py:156 */
+       CO_POOL_EMBED = 1,           /* a = n_tokens, b = host slot, c = start_offset  :202 */
+       CO_POOL_DRAW_RESERVED = 2,   /* a = n_blocks                       :229 */
+       CO_POOL_GROW = 3,            /* a = n_tokens                       :251 */
+       CO_POOL_PROMOTE = 4,         /*                                    :283 */
+       CO_POOL_RELEASE = 5,         /* out[1] = net tokens returned       :299 */
+       CO_POOL_SET_USED = 6,        /* a = used_tokens                    :326 */
+       CO_POOL_NET_RELEASE_GAIN = 7 /* out[1]                             :142 */ };
+enum { CO_PV_TOKENS = 1,            /* "n_tokens must be >= 1" */
+       CO_PV_HOLDS = 2,             /* "request {id} already holds an allocation" */
+       CO_PV_NO_RECORD = 3,         /* "no allocation for request {id}" */
+       CO_PV_NO_RECORD_HOST = 4,    /* "no allocation for request {host}" */
+       CO_PV_HOST_EMBEDDED = 5,     /* "host {host} is itself embedded" */
+       CO_PV_SELF_HOST = 6,         /* "a request cannot host itself" */
+       CO_PV_HAS_GUEST = 7,         /* "host {host} already has a guest" */
+       CO_PV_EMBED_RANGE = 8,       /* "embed region exceeds host allocation" */
+       CO_PV_EMBED_OVERLAP = 9,     /* "embed region overlaps an existing guest" */
+       CO_PV_BLOCKS = 10,           /* "n_blocks must be >= 1" */
+       CO_PV_GUEST_RESERVE = 11,    /* "guests cannot draw from the reserve" */
+       CO_PV_NOT_EMBEDDED = 12,     /* "request {id} is not embedded" */
+       CO_PV_USED_RANGE = 13        /* "request {id}: used {u} outside [0, {granted}]" (out[1] = granted) */ };
+int co_pool_create(int64_t capacity, int32_t block_size, int32_t reserved_blocks, int32_t buffer_b,
+                   int32_t allow_stacking, int32_t max_records, int32_t device, co_pool** out);
+int co_pool_destroy(co_pool* pool);
+int co_pool_op(co_pool* pool, int32_t op, int32_t slot, int64_t a, int64_t b, int64_t c, int64_t* out /* 3 */);
+/* kvc.py:169-200: triples[4n] = (host slot or -1, request id, allocated a_j,
+ * used u_j); out[4] = {found, host slot, start_offset, feasible_slack} */
+int co_pool_find_host(co_pool* pool, int32_t n, const int64_t* triples, int64_t cand_prompt, int64_t cand_out,
+                      int64_t buffer_b, int64_t* out);
+/* scalars[6] = {free, footprint, granted, used, reserved_current, free pages};
+ * records (optional) [max_records][9] = {holds, granted, host slot, offset,
+ * reserved drawn, first guest slot, next guest slot, used, creation seq} */
+int co_pool_state(co_pool* pool, int64_t* scalars, int64_t* records);
+int co_pool_check(co_pool* pool);  /* kvc.py:336-375 + N1 page conservation */
+int co_pool_read_tables(co_pool* pool, int32_t* lens, int32_t* pages, int64_t max_pages, int32_t* free_pages,
+                        int32_t* n_free);
+
+/* ---- the reference's pure scheduling ops on the device -------------------
+ * (scheduler.py:129-279, preemption.py:46-75) through the planner's own
+ * device code (csrc/sched_ops.cuh).  rows: int64 [n][8]; column 0 is always
+ * the row's rank in ascending req_id order (the ids' tie-break).
+ *   CLASSIFY           rows (rank, list 0 waiting / 1 running, rt, returned, arrival)
+ *                      params (t_i_max_us, epsilon_us); out = 4 counts, then the
+ *                      row indices of n_w, n_r, n_w', n_r' in the reference's order
+ *   FILL_BUDGET        rows (chunk); params (token_budget, consumed); out (k, overflow)
+ *   ALLOCATE_REMAINING rows (rank, m_tokens, rt_us, prompt_len), n <= 1024;
+ *                      params (a_prime); out[k] = grant, -1 for m_tokens <= 0
+ *   PAIR_RELEASE       rows (rank, est_remaining_iters, release_gain);
+ *                      params (residual_tokens, runway_iters); out[0] = row or -1
+ *   ORDER_VICTIMS      rows (rank, slo_tbt_us, remaining_tokens, occupancy);
+ *                      params (token_step, n_edges <= 6, edges...); out = order
+ *   PROACTIVE_INCLUDE  rows (rank, returned, allocated, target_alloc, est_remaining);
+ *                      params (m); out = count, then the rows in order
+ * out holds 2n + 8 values. */
+enum { CO_SOP_CLASSIFY = 0, CO_SOP_FILL_BUDGET = 1, CO_SOP_ALLOCATE_REMAINING = 2, CO_SOP_PAIR_RELEASE = 3,
+       CO_SOP_ORDER_VICTIMS = 4, CO_SOP_PROACTIVE_INCLUDE = 5 };
+int co_sched_op(int32_t op, int32_t n, const int64_t* rows, const int64_t* params /* 16 */, int64_t* out,
+                int32_t device);
 
 #ifdef __cplusplus
 }

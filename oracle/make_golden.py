@@ -29,6 +29,7 @@ OUT = os.path.join(ROOT, "tests", "golden")
 sys.path.insert(0, ROOT)
 
 SEEDS = [0, 1, 2, 5, 9, 13, 21, 34]
+STACK_SEEDS = [8, 13, 57]  # regimes where a host carries up to 3-4 stacked guests (allow_stacking=True)
 BASELINE_CASES = [("vllm_block", 5), ("vllm_block", 13), ("sarathi_chunked", 13), ("sarathi_chunked", 9),
                   ("rlp", 6), ("s3", 2), ("s3", 13)]
 
@@ -59,7 +60,8 @@ def ref_build(params):
                        sched=SchedulerConfig(**{"policy": "cacheopt", **params["sched"]}),
                        predictor=PredictorConfig(**params["pred"]), truth=truth, seed=seed,
                        fixed_confidence=params["fixed_confidence"],
-                       validate_every=params["validate_every"])
+                       validate_every=params["validate_every"],
+                       allow_stacking=params.get("allow_stacking", False))
     return reqs, cfg
 
 
@@ -127,6 +129,15 @@ def main():
         p = case_params(s)
         reqs, cfg = ref_build(p)
         run_and_store(f"case{s:02d}", p, reqs, cfg)
+    # allow_stacking=True (kvc.py:187-192, :212): several guests per host
+    for s in STACK_SEEDS:
+        name = f"stack_case{s:02d}"
+        if only and name not in only:
+            continue
+        p = case_params(s)
+        p["allow_stacking"] = True
+        reqs, cfg = ref_build(p)
+        run_and_store(name, p, reqs, cfg)
     # the four baseline planners (scheduler.py:760-936) on regimes that preempt
     for pol, s in BASELINE_CASES:
         name = f"base_{pol}_case{s:02d}"

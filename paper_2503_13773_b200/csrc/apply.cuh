@@ -23,13 +23,21 @@ __device__ void check_pool(const Dev& d, BlkShared& sb) {
         int32_t h = d.host[i];
         if (h >= 0) {
             if (d.guest[i] >= 0) bad |= 2;
-            if (!d.holds[h] || d.guest[h] != i) bad |= 4;
+            bool listed = false;
+            if (d.holds[h])
+                for (int32_t g = d.guest[h]; g >= 0 && !listed; g = d.gnext[g]) listed = g == i;
+            if (!listed) bad |= 4;
             else if (d.off[i] < 0 || (int64_t)d.off[i] + d.granted[i] > d.granted[h]) bad |= 8;
         } else if (d.tab_len[i] * (int64_t)d.bs != fp_tokens(d.granted[i], d.bs)) {
             bad |= 32;  // N1: the table covers exactly the footprint
         }
-        int32_t g = d.guest[i];
-        if (g >= 0 && d.off[g] < d.used[i]) bad |= 16;
+        // guest spans above the host's used region, pairwise disjoint (kvc.py:365-375)
+        for (int32_t g = d.guest[i]; g >= 0; g = d.gnext[g]) {
+            if (d.off[g] < d.used[i]) bad |= 16;
+            for (int32_t q = d.gnext[g]; q >= 0; q = d.gnext[q])
+                if (!((int64_t)d.off[g] + d.granted[g] <= d.off[q] || (int64_t)d.off[q] + d.granted[q] <= d.off[g]))
+                    bad |= 16;
+        }
     }
     fp = blk_sum(fp, sb);
     bad = blk_sum(bad ? 1 : 0, sb);
@@ -368,8 +376,9 @@ __device__ __forceinline__ void apply_body(const Dev& d, ApplySh& S) {
     // ---- collisions (engine.py:573-591), hosts in record-creation order ----
     const int32_t n_coll = blk_compact(RUN, n_run, d.l_coll, [&](int32_t h) {
         if (d.state[h] != ST_RUNNING || !d.holds[h] || d.host[h] >= 0) return false;
-        int32_t g = d.guest[h];
-        return g >= 0 && d.used[h] >= d.off[g];
+        for (int32_t g = d.guest[h]; g >= 0; g = d.gnext[g])
+            if (d.used[h] >= d.off[g]) return true;
+        return false;
     }, S.b);
     blk_sort(d.l_coll, n_coll, [&](int32_t h, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
         k0 = (uint64_t)d.rec_seq[h]; k1 = 0; k2 = 0;
@@ -378,10 +387,22 @@ __device__ __forceinline__ void apply_body(const Dev& d, ApplySh& S) {
         for (int32_t k = 0; k < n_coll; k++) {
             int32_t h = d.l_coll[k];
             if (d.state[h] != ST_RUNNING || !d.holds[h]) continue;
-            int32_t g = d.guest[h];
-            if (g < 0 || d.used[h] < d.off[g]) continue;
-            if (pool_promote(d, g)) continue;
-            if (d.state[g] == ST_RUNNING) do_preempt(d, g, strategy_of(d, g), end, CO_CAUSE_COLLISION);
+            // the host's guests by offset ascending (engine.py:585), a copy:
+            // promotions and preemptions unlink them as the loop goes
+            constexpr int MAXG = 32;
+            int32_t gl[MAXG];
+            int32_t ng = 0;
+            for (int32_t g = d.guest[h]; g >= 0 && ng < MAXG; g = d.gnext[g]) {
+                int32_t p = ng++;
+                while (p > 0 && d.off[gl[p - 1]] > d.off[g]) { gl[p] = gl[p - 1]; p--; }
+                gl[p] = g;
+            }
+            for (int32_t q = 0; q < ng; q++) {
+                const int32_t g = gl[q];
+                if (d.used[h] < d.off[g]) continue;
+                if (pool_promote(d, g)) continue;
+                if (d.state[g] == ST_RUNNING) do_preempt(d, g, strategy_of(d, g), end, CO_CAUSE_COLLISION);
+            }
         }
         if (d.dp.on) {
             // standalone members' KV at their final pages, then this

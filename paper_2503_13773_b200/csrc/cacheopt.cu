@@ -15,6 +15,8 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <type_traits>
+#include <climits>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -457,7 +459,6 @@ int co_destroy(co_engine* E) {
 int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int device, co_engine** out) {
     if (!cfg || !tr || !lu || !out) return fail(CO_EINVAL, "null argument");
     *out = nullptr;
-    if (cfg->allow_stacking) return fail(CO_EINVAL, "allow_stacking=True is not supported by the device pool");
     if (cfg->block_size < 1 || cfg->buffer_b < 0 || cfg->token_budget < 1 || cfg->preallocate_m < 0 ||
         cfg->decode_runway_iters < 0 || cfg->epsilon_us < 0 || cfg->token_step < 1 || cfg->capacity_tokens < 1 ||
         cfg->reserved_blocks < 0 || cfg->n_slo_edges < 0 || cfg->n_slo_edges > CO_MAX_SLO_EDGES)
@@ -555,6 +556,7 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
 
     Dev& d = E->d;
     d.n = (int32_t)n; d.bs = cfg->block_size; d.B = cfg->block_size; d.buffer_b = cfg->buffer_b;
+    d.stacking = cfg->allow_stacking ? 1 : 0;
     d.token_budget = cfg->token_budget; d.prealloc_m = cfg->preallocate_m; d.runway_iters = cfg->decode_runway_iters;
     d.fcfs = cfg->victim_rule_fcfs; d.record_events = cfg->record_events; d.validate_every = cfg->validate_every;
     d.pad = cfg->padding; d.idbits = idbits; d.key_bits = key_bits; d.n_edges = cfg->n_slo_edges; d.token_step = cfg->token_step;
@@ -585,7 +587,7 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     AL(d.first_tok, n); AL(d.last_tok, n); AL(d.max_tbt, n); AL(d.ready_at, n); AL(d.pstart, n);
     AL(d.swap_done, n); AL(d.first_start, n); AL(d.completion, n); AL(d.ptime, n);
     AL(d.tok_times, E->tok_total);
-    AL(d.holds, n); AL(d.granted, n); AL(d.host, n); AL(d.off, n); AL(d.rsv, n); AL(d.guest, n); AL(d.rec_seq, n);
+    AL(d.holds, n); AL(d.granted, n); AL(d.host, n); AL(d.off, n); AL(d.rsv, n); AL(d.guest, n); AL(d.gnext, n); AL(d.rec_seq, n);
     AL(d.claim_w, n); AL(d.claim_ep, n); AL(d.epoch, n);
     AL(d.chunk_pool, n_chunks * TCHUNK); AL(d.chunk_stack, n_chunks); AL(d.dir, (int64_t)n * dir_w);
     AL(d.tab_len, n); AL(d.free_stack, n_pages);
@@ -646,7 +648,10 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
         void* hdev = nullptr;
         cudaHostGetDevicePointer(&hdev, E->host_pool, 0);
         x.hkv = static_cast<uint16_t*>(hdev);
-        x.stage_tokens = max_s + 1;
+        // every guest moves at most once per step and all their KV fits the
+        // pool, so with stacking the whole step's MOVE group fits `capacity`
+        x.group_moves = cfg->allow_stacking ? 1 : 0;
+        x.stage_tokens = cfg->allow_stacking ? std::max<int64_t>(max_s, cfg->capacity_tokens) + 1 : max_s + 1;
         AL(x.stage, x.stage_tokens * x.rows * x.D);
         x.op_cap = 8 * n + 4096;
         x.snap_cap = 16 * (int64_t)n_pages + 8 * n + 65536;
@@ -712,7 +717,7 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     for (int32_t* p : {d.gen, d.used, d.prefill, d.pcount, d.pred, d.est, d.alloc_kvc, d.granted, d.off, d.rsv,
                        d.claim_ep, d.epoch})
         memset_all(p, 0, n4);
-    for (int32_t* p : {d.host, d.guest, d.claim_w}) memset_all(p, 0xff, n4);
+    for (int32_t* p : {d.host, d.guest, d.gnext, d.claim_w}) memset_all(p, 0xff, n4);
     for (int32_t* p : {d.st_nr, d.st_crit, d.st_removed, d.st_embedded, d.st_resumed, d.st_stalled, d.st_parts,
                        d.st_claimed, d.st_failed, d.st_acted, d.st_deferred})
         memset_all(p, 0, n4);
@@ -1776,3 +1781,6 @@ int co_gen_predictor(int64_t n, const co_predictor_spec* sp, uint64_t seed, int 
 }
 
 }  // extern "C"
+
+#include "pool_api.cuh"
+#include "sched_ops.cuh"

@@ -217,8 +217,12 @@ __global__ void __launch_bounds__(512, 1) k_data(Dev d, DataCfg x, DataCtl* dc, 
     while (a < nops) {
         const int32_t kind = x.ops[a].kind;
         int32_t b = a + 1;
-        if (kind != D_MOVE)
+        if (kind != D_MOVE) {
             while (b < nops && x.ops[b].kind == kind) b++;
+        } else if (x.group_moves) {
+            int64_t tk = x.ops[a].ntok;
+            while (b < nops && x.ops[b].kind == D_MOVE && tk + x.ops[b].ntok <= x.stage_tokens) tk += x.ops[b++].ntok;
+        }
         // ops [a, b): independent, same kind; flat work over their units
         int64_t total = 0;
         for (int32_t o = a; o < b; o++) total += (int64_t)x.ops[o].ntok * units_per_tok;
@@ -251,14 +255,15 @@ __global__ void __launch_bounds__(512, 1) k_data(Dev d, DataCfg x, DataCtl* dc, 
                 }
                 const uint16_t* src;
                 uint16_t* dst;
+                const int64_t so = obase / units_per_tok + j;  // staging slot: token offset within the group
                 if (op.kind == D_MOVE && pass == 1) {
-                    src = x.stage + ((int64_t)j * x.rows + r) * x.D + ch * 8;
+                    src = x.stage + (so * x.rows + r) * x.D + ch * 8;
                 } else {
                     const uint16_t* base = op.src_where == W_HOST ? x.hkv : x.kv;
                     src = base + loc_elem(d, x, op.src_where, op.src_snap, op.src_end, op.req, tok, r) + ch * 8;
                 }
                 if (op.kind == D_MOVE && pass == 0) {
-                    dst = x.stage + ((int64_t)j * x.rows + r) * x.D + ch * 8;
+                    dst = x.stage + (so * x.rows + r) * x.D + ch * 8;
                 } else {
                     uint16_t* base = op.dst_where == W_HOST ? x.hkv : x.kv;
                     dst = base + loc_elem(d, x, op.dst_where, op.dst_snap, op.dst_end, op.req, tok, r) + ch * 8;

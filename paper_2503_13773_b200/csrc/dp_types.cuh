@@ -38,6 +38,10 @@ struct DataCfg {
     int64_t dec_item_cap;
     uint32_t* gbar;       // grid barrier {count, generation}
     int32_t on, decode_on;
+    // stacking: a host release re-homes several guests, and an earlier guest's
+    // new pages can be the pages that still hold a later guest's KV, so a run
+    // of MOVEs is staged as one group (all reads, then all writes)
+    int32_t group_moves;
 };
 
 struct DataCtl {

@@ -85,9 +85,12 @@ struct Dev {
         *completion, *ptime;
     const int64_t* tok_off;
     int64_t* tok_times;
-    // pool records (kvc.py:44-52); no stacking: at most one guest per host
+    // pool records (kvc.py:44-52).  A host's guests (kvc.py:52 `guests`, in
+    // embed order) are a singly linked list: guest[h] = first, gnext[g] =
+    // next.  Without stacking the list has at most one entry.
     uint8_t* holds;
-    int32_t *granted, *host, *off, *rsv, *guest;
+    int32_t *granted, *host, *off, *rsv, *guest, *gnext;
+    int32_t stacking;  // BlockPool.allow_stacking (kvc.py:64, 187-192, 212)
     int64_t* rec_seq;
     // N1 physical block tables (standalone records only; a guest is a view
     // into its host's pages).  Request i's k-th page is
@@ -160,11 +163,14 @@ __device__ __forceinline__ int64_t fp_tokens(int64_t t, int bs) { return ((t + b
 __device__ __forceinline__ int64_t rt_of(const Dev& d, int i, int64_t now) {
     return d.first_tok[i] < 0 ? d.slo_ttft[i] - (now - d.arr[i]) : d.slo_tbt[i] - (now - d.last_tok[i]);
 }
+// engine.py:275-282: min(granted, lowest guest offset)
 __device__ __forceinline__ int32_t eff_of(const Dev& d, int i) {
     if (!d.holds[i]) return 0;
     int32_t g = d.granted[i];
-    int32_t gu = d.guest[i];
-    if (gu >= 0) { int32_t o = d.off[gu]; return o < g ? o : g; }
+    for (int32_t gu = d.guest[i]; gu >= 0; gu = d.gnext[gu]) {
+        const int32_t o = d.off[gu];
+        g = o < g ? o : g;
+    }
     return g;
 }
 __device__ __forceinline__ bool guest_of(const Dev& d, int i) { return d.holds[i] && d.host[i] >= 0; }
@@ -196,8 +202,7 @@ __device__ __forceinline__ int64_t free_tokens(const Dev& d) {
 __device__ __forceinline__ int64_t gain_of(const Dev& d, int i) {
     if (d.host[i] >= 0) return 0;
     int64_t freed = fp_tokens(d.granted[i], d.bs);
-    int32_t g = d.guest[i];
-    if (g >= 0) freed -= fp_tokens(d.granted[g], d.bs);
+    for (int32_t g = d.guest[i]; g >= 0; g = d.gnext[g]) freed -= fp_tokens(d.granted[g], d.bs);
     int64_t room = (int64_t)d.rsv_target - d.ctl->rsv_cur;
     int64_t refill = d.rsv[i] < room ? d.rsv[i] : room;
     return freed - refill * d.bs;

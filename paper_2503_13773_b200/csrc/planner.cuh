@@ -139,9 +139,12 @@ __device__ __forceinline__ void push_mem(const Dev& d, PlanSh& S, int32_t i, int
 }
 
 // scheduler.py:432-449 try_embed + kvc.py:169-200 find_embedding_host.
-// Without stacking a host is feasible iff (a_j - u_j) >= b + need + out, so
-// with the hosts sorted by (a_j - u_j, id) the argmin is the first free entry
-// at or after a lower bound.
+// A guest-free host is feasible iff (a_j - u_j) >= b + need + out, so with
+// the hosts sorted by (a_j - u_j, id) the argmin is the first free entry at
+// or after a lower bound.  With stacking a host that already carries guests
+// places the new one below its lowest guest (end = min offset <= a_j), so it
+// additionally needs (end - u_j) >= b + need + out; every entry before the
+// lower bound is infeasible either way, so the scan stays exact.
 __device__ bool try_embed(const Dev& d, PlanSh& S, const PV& v, int32_t n_tri, int32_t sid) {
     const int32_t i = v.i;
     if (v.eff > 0 || v.pcount > 0) return false;
@@ -155,14 +158,20 @@ __device__ bool try_embed(const Dev& d, PlanSh& S, const PV& v, int32_t n_tri, i
         int32_t mid = (lo + hi) >> 1;
         if ((cached ? S.tri_key[mid] : d.l_tri_key[mid]) < thr) lo = mid + 1; else hi = mid;
     }
-    if (cached) {
-        while (lo < n_tri && (S.tri_taken[lo] || d.st_removed[S.tri_idx[lo]] == sid)) lo++;
-    } else {
-        while (lo < n_tri && (d.l_tri_taken[lo] || d.st_removed[d.l_tri[lo]] == sid)) lo++;
+    int64_t end = 0;
+    for (; lo < n_tri; lo++) {
+        const int32_t hh = cached ? S.tri_idx[lo] : d.l_tri[lo];
+        if ((cached ? S.tri_taken[lo] : d.l_tri_taken[lo]) || d.st_removed[hh] == sid) continue;
+        end = (cached ? S.tri_key[lo] : d.l_tri_key[lo]) + d.used[hh];  // a_j
+        if (d.guest[hh] >= 0) {  // stacking: below the lowest guest
+            end = eff_of(d, hh);
+            if (end - d.used[hh] < thr) continue;
+        }
+        break;
     }
     if (lo >= n_tri) return false;
     int32_t h = cached ? S.tri_idx[lo] : d.l_tri[lo];
-    push_act(d, S, A_EMBED, i, need, 0, h, (cached ? S.tri_key[lo] : d.l_tri_key[lo]) + d.used[h] - need);
+    push_act(d, S, A_EMBED, i, need, 0, h, end - need);
     d.st_embedded[i] = sid;
     if (cached) S.tri_taken[lo] = 1; else d.l_tri_taken[lo] = 1;  // one guest per host per plan (scheduler.py:446-448)
     return true;
@@ -712,7 +721,7 @@ __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
     for (int32_t k = tid; k < n_tri; k += (int)blockDim.x) {
         int32_t h = d.l_tri[k];
         const int64_t key = (int64_t)d.granted[h] - d.used[h];
-        const int32_t taken = d.guest[h] >= 0 ? 1 : 0;  // already hosting: skipped without stacking
+        const int32_t taken = (d.guest[h] >= 0 && !d.stacking) ? 1 : 0;  // already hosting: skipped without stacking
         if (tri_cached) {
             S.tri_key[k] = key; S.tri_idx[k] = h; S.tri_taken[k] = taken;
         } else {

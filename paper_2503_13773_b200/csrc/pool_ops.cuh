@@ -54,6 +54,7 @@ __device__ __forceinline__ void new_record(const Dev& d, int i, int32_t granted,
     d.off[i] = off;
     d.rsv[i] = 0;
     d.guest[i] = -1;
+    d.gnext[i] = -1;
     d.rec_seq[i] = ++d.ctl->seq;  // dict insertion order (kvc.py:82)
 }
 __device__ __forceinline__ void drop_record(const Dev& d, int i) {
@@ -73,14 +74,28 @@ __device__ bool pool_allocate(const Dev& d, int i, int64_t n) {
     return true;
 }
 
-// kvc.py:202-227 (no stacking)
+// unlink guest i from host h's list (kvc.py:294 / :306 `host.guests.remove`)
+__device__ __forceinline__ void guest_unlink(const Dev& d, int h, int i) {
+    int32_t prev = -1;
+    for (int32_t g = d.guest[h]; g >= 0; prev = g, g = d.gnext[g]) {
+        if (g != i) continue;
+        if (prev < 0) d.guest[h] = d.gnext[g]; else d.gnext[prev] = d.gnext[g];
+        d.gnext[g] = -1;
+        return;
+    }
+}
+
+// kvc.py:202-227
 __device__ bool pool_embed(const Dev& d, int i, int64_t n, int h, int64_t start) {
     if (n < 1 || d.holds[i] || !d.holds[h]) return false;
     if (d.host[h] >= 0 || i == h) return false;
-    if (d.guest[h] >= 0) return false;
+    if (d.guest[h] >= 0 && !d.stacking) return false;
     if (start < 0 || start + n > d.granted[h]) return false;
+    int32_t tail = -1;
+    for (int32_t g = d.guest[h]; g >= 0; tail = g, g = d.gnext[g])  // no overlap with an existing guest
+        if (!(start + n <= d.off[g] || (int64_t)d.off[g] + d.granted[g] <= start)) return false;
     new_record(d, i, (int32_t)n, h, (int32_t)start);
-    d.guest[h] = i;
+    if (tail < 0) d.guest[h] = i; else d.gnext[tail] = i;  // guests.append
     d.ctl->granted_sum += n;
     return true;
 }
@@ -119,9 +134,14 @@ __device__ bool pool_grow(const Dev& d, int i, int64_t n) {
         pop_pages(d, i, delta / d.bs);
         return true;
     }
-    // guests grow downward to the host's used region plus the buffer; with
-    // stacking disabled there is no lower guest
+    // guests grow downward to the host's used region plus the buffer, or to
+    // the top of the guest below them
     int64_t floor_ = (int64_t)d.used[h] + d.buffer_b;
+    for (int32_t g = d.guest[h]; g >= 0; g = d.gnext[g])
+        if (g != i && d.off[g] < d.off[i]) {
+            const int64_t top = (int64_t)d.off[g] + d.granted[g];
+            floor_ = top > floor_ ? top : floor_;
+        }
     if (n > (int64_t)d.off[i] - floor_) return false;
     d.off[i] -= (int32_t)n;
     d.granted[i] = (int32_t)(g + n);
@@ -138,7 +158,7 @@ __device__ bool pool_promote(const Dev& d, int i) {
     int32_t vend = 0;
     const int32_t gused = d.used[i];
     if (d.dp.on && gused > 0) vsnap = snap_view(d, d.dp, h, d.off[i] + d.granted[i], gused, &vend);
-    d.guest[h] = -1;
+    guest_unlink(d, h, i);
     d.host[i] = -1;
     d.off[i] = 0;
     d.ctl->fp_sum += fp;
@@ -152,29 +172,39 @@ __device__ void pool_release(const Dev& d, int i) {
     Ctl& c = *d.ctl;
     int32_t h = d.host[i];
     if (h >= 0) {
-        if (d.holds[h] && d.guest[h] == i) d.guest[h] = -1;
+        if (d.holds[h]) guest_unlink(d, h, i);
         c.granted_sum -= d.granted[i];
         d.host[i] = -1;
         drop_record(d, i);
         return;
     }
-    int32_t g = d.guest[i];
-    int64_t vsnap = 0;
-    int32_t vend = 0, gused = 0;
-    if (g >= 0 && d.dp.on) {
-        gused = d.used[g];
-        if (gused > 0) vsnap = snap_view(d, d.dp, i, d.off[g] + d.granted[g], gused, &vend);
+    // every guest is re-homed (kvc.py:311-317), in embed order, into pages
+    // of its own; their views are snapshotted before the host's pages go back
+    constexpr int MAXG = 32;
+    int64_t vsnap[MAXG];
+    int32_t vend[MAXG], gused[MAXG];
+    int32_t ng = 0;
+    for (int32_t g = d.guest[i]; g >= 0; g = d.gnext[g], ng++) {
+        if (ng == MAXG) { c.error = 11; c.err_info[0] = i; return; }
+        gused[ng] = d.used[g];
+        vsnap[ng] = 0;
+        vend[ng] = 0;
+        if (d.dp.on && gused[ng] > 0) vsnap[ng] = snap_view(d, d.dp, i, d.off[g] + d.granted[g], gused[ng], &vend[ng]);
     }
     push_table(d, i);
-    if (g >= 0) {  // the guest is re-homed (kvc.py:311-317) into pages of its own
+    int32_t k = 0;
+    for (int32_t g = d.guest[i]; g >= 0; k++) {
+        const int32_t nx = d.gnext[g];
         d.host[g] = -1;
         d.off[g] = 0;
+        d.gnext[g] = -1;
         const int64_t gfp = fp_tokens(d.granted[g], d.bs);
         c.fp_sum += gfp;
-        d.guest[i] = -1;
         pop_pages(d, g, gfp / d.bs);
-        if (d.dp.on && gused > 0) log_move(d, d.dp, g, gused, vsnap, vend);
+        if (d.dp.on && gused[k] > 0) log_move(d, d.dp, g, gused[k], vsnap[k], vend[k]);
+        g = nx;
     }
+    d.guest[i] = -1;
     c.fp_sum -= fp_tokens(d.granted[i], d.bs);
     c.granted_sum -= d.granted[i];
     int64_t room = (int64_t)d.rsv_target - c.rsv_cur;

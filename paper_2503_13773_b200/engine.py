@@ -268,10 +268,14 @@ class PoolView:
         return int(self._f("RESERVED_DRAWN")[self._idx(rid)])
 
     def guests_of(self, rid: int) -> List[int]:
+        """kvc.py:124-125: the host's guests in embed order (= their records'
+        creation order: a guest record is created by the embed)."""
         k = self._idx(rid)
         host = self._f("HOST")
         holds = self._f("HOLDS")
-        return [self._e._rid[g] for g in np.nonzero((host == k) & (holds == 1))[0]]
+        seq = self._f("RECORD_SEQ")
+        g = np.nonzero((host == k) & (holds == 1))[0]
+        return [self._e._rid[x] for x in g[np.argsort(seq[g], kind="stable")]]
 
     def owners(self) -> List[int]:
         holds = self._f("HOLDS")
@@ -297,8 +301,6 @@ class Engine:
                              f"(device policies: {DEVICE_POLICIES})")
         if cfg.sched.invert_amortization:
             raise ValueError("invert_amortization=True is not supported by the device planner")
-        if cfg.allow_stacking:
-            raise ValueError("allow_stacking=True is not supported by the device pool")
         self.cfg = cfg
         # the caller's Request objects, kept current like the reference's
         # in-step transitions (core.py:113-130): refreshed lazily on access

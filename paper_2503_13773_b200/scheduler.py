@@ -1,0 +1,256 @@
+"""The reference's pure scheduling ops (scheduler.py:71-279) and victim
+ordering (preemption.py:38-75) with their names and argument meaning.
+
+The ops that make decisions -- classify_critical, fill_token_budget,
+allocate_remaining, pair_release, proactive_include, order_victims -- run on
+the GPU through the planner's own device code (csrc/sched_ops.cuh via
+co_sched_op): the same criticality predicate, queue keys, block compaction,
+rank sort, budget prefix, exact integer amortization and argmins k_plan uses
+inside the engine step.  The closed-form demand helpers are host arithmetic,
+as in the reference.  The engine never calls this module (its planner reads
+the resident request pool); it exists so callers and the reference's own
+tests can drive the device ops on snapshot views."""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import Dict, Iterable, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _native as N
+from .config import BucketConfig
+from .core import Lifecycle
+
+SOP_CLASSIFY, SOP_FILL_BUDGET, SOP_ALLOCATE_REMAINING, SOP_PAIR_RELEASE, SOP_ORDER_VICTIMS, \
+    SOP_PROACTIVE_INCLUDE = range(6)
+_DEVICE = 0
+
+
+def set_device(device: int) -> None:
+    """CUDA device the ops run on (default 0)."""
+    global _DEVICE
+    _DEVICE = int(device)
+
+
+@dataclass(frozen=True)
+class ReqView:
+    """scheduler.py:71-96: the per-request snapshot handed to the planner."""
+    req_id: int
+    arrival_us: int
+    state: Lifecycle
+    kv_need: int
+    generated: int
+    estimated_total: int
+    predicted_total: int
+    allocated: int
+    used: int
+    slo_ttft_us: int
+    slo_tbt_us: int
+    remaining_ttft_us: Optional[int]
+    remaining_tbt_us: Optional[int]
+    ready: bool = True
+    prefill_done: int = 0
+    preemption_count: int = 0
+    is_guest: bool = False
+    tbt_blown: bool = False
+
+
+def est_remaining(v: ReqView) -> int:
+    return max(0, v.estimated_total - v.generated)
+
+
+def target_alloc(v: ReqView) -> int:
+    return max(v.used, v.kv_need) + est_remaining(v)
+
+
+def rt_us(v: ReqView) -> int:
+    if v.remaining_ttft_us is not None:
+        return v.remaining_ttft_us
+    if v.remaining_tbt_us is None:
+        raise AssertionError("a view needs remaining_ttft_us or remaining_tbt_us")
+    return v.remaining_tbt_us
+
+
+def is_returned(v: ReqView) -> bool:
+    return v.state is Lifecycle.RUNNING and v.allocated < v.used + 1
+
+
+@dataclass
+class CriticalSets:
+    n_w: List[ReqView]
+    n_r: List[ReqView]
+    n_w_prime: List[ReqView]
+    n_r_prime: List[ReqView]
+
+
+@dataclass(frozen=True)
+class AllocDemand:
+    req_id: int
+    m_tokens: int
+    rt_us: int
+    prompt_len: int
+
+
+@dataclass(frozen=True)
+class PairCandidate:
+    req_id: int
+    est_remaining_iters: int
+    release_gain: int
+
+
+@dataclass(frozen=True)
+class VictimInfo:
+    req_id: int
+    slo_tbt_us: int
+    remaining_tokens: int
+    occupancy_tokens: int
+
+
+def _ranks(ids: Sequence[int]) -> np.ndarray:
+    order = np.argsort(np.asarray(ids, dtype=np.int64), kind="stable")
+    r = np.empty(len(ids), dtype=np.int64)
+    r[order] = np.arange(len(ids))
+    return r
+
+
+def _run(op: int, rows: np.ndarray, params: Sequence[int]) -> np.ndarray:
+    lib = N.load()
+    n = len(rows)
+    rows = np.ascontiguousarray(rows, dtype=np.int64).reshape(n, 8) if n else np.zeros((0, 8), dtype=np.int64)
+    prm = np.zeros(16, dtype=np.int64)
+    prm[:len(params)] = params
+    out = np.zeros(2 * max(n, 1) + 8, dtype=np.int64)
+    p = lambda a: a.ctypes.data_as(C.POINTER(C.c_int64))  # noqa: E731
+    N.check(lib.co_sched_op(op, n, p(rows), p(prm), p(out), _DEVICE), "co_sched_op")
+    return out
+
+
+# -- criticality (scheduler.py:129-163) -----------------------------------------
+
+def classify_critical(waiting: Sequence[ReqView], running: Sequence[ReqView], t_i_max_us: int,
+                      epsilon_us: int) -> CriticalSets:
+    views = list(waiting) + list(running)
+    rows = np.zeros((len(views), 8), dtype=np.int64)
+    rows[:, 0] = _ranks([v.req_id for v in views])
+    for k, v in enumerate(views):
+        run = k >= len(waiting)
+        rows[k, 1] = int(run)
+        if run:
+            ret = is_returned(v)
+            rows[k, 3] = int(ret)
+            if ret:
+                if v.remaining_tbt_us is None:
+                    raise AssertionError("a returned running view needs remaining_tbt_us")
+                rows[k, 2] = v.remaining_tbt_us
+        else:
+            rows[k, 2] = rt_us(v)
+        rows[k, 4] = v.arrival_us
+    out = _run(SOP_CLASSIFY, rows, [t_i_max_us, epsilon_us])
+    cnt = out[:4].tolist()
+    lists, base = [], 4
+    for c in cnt:
+        lists.append([views[int(x)] for x in out[base:base + c]])
+        base += c
+    return CriticalSets(n_w=lists[0], n_r=lists[1], n_w_prime=lists[2], n_r_prime=lists[3])
+
+
+# -- demand arithmetic (scheduler.py:166-179) ------------------------------------
+
+def basic_demand(sets: CriticalSets, small_block_b: int) -> int:
+    need = sum(max(0, v.kv_need + small_block_b - v.allocated) for v in sets.n_w)
+    return need + small_block_b * len(sets.n_r)
+
+
+def ensure_capacity(pool_free: int, d_kvc: int) -> int:
+    return max(0, d_kvc - pool_free)
+
+
+# -- token budget (scheduler.py:182-200) -----------------------------------------
+
+def fill_token_budget(sets: CriticalSets, waiting_ordered: Sequence[ReqView], token_budget: int,
+                      consumed_tokens: int) -> Tuple[List[ReqView], bool]:
+    q = list(waiting_ordered)
+    rows = np.zeros((len(q), 8), dtype=np.int64)
+    for k, v in enumerate(q):
+        rows[k, 0] = v.kv_need - v.prefill_done
+    out = _run(SOP_FILL_BUDGET, rows, [token_budget, consumed_tokens])
+    return q[:int(out[0])], bool(out[1])
+
+
+# -- remaining-KVC amortization (scheduler.py:211-243) ---------------------------
+
+def allocate_remaining(demands: Sequence[AllocDemand], a_prime: int, invert: bool = False) -> Dict[int, int]:
+    if a_prime < 0:
+        raise ValueError("a_prime must be >= 0")
+    if invert:
+        raise ValueError("invert=True is not supported on the device (DESIGN.md section 7)")
+    ds = list(demands)
+    if not ds:
+        return {}
+    rows = np.zeros((len(ds), 8), dtype=np.int64)
+    rows[:, 0] = _ranks([d.req_id for d in ds])
+    for k, d in enumerate(ds):
+        rows[k, 1:4] = (d.m_tokens, d.rt_us, d.prompt_len)
+    out = _run(SOP_ALLOCATE_REMAINING, rows, [a_prime])
+    return {d.req_id: int(out[k]) for k, d in enumerate(ds) if d.m_tokens > 0}
+
+
+# -- pair release and proactive inclusion (scheduler.py:253-279) -----------------
+
+def pair_release(residual_tokens: int, runway_iters: int, candidates: Sequence[PairCandidate]) -> Optional[int]:
+    cs = list(candidates)
+    if not cs:
+        return None
+    rows = np.zeros((len(cs), 8), dtype=np.int64)
+    rows[:, 0] = _ranks([c.req_id for c in cs])
+    for k, c in enumerate(cs):
+        rows[k, 1:3] = (c.est_remaining_iters, c.release_gain)
+    k = int(_run(SOP_PAIR_RELEASE, rows, [residual_tokens, runway_iters])[0])
+    return None if k < 0 else cs[k].req_id
+
+
+def proactive_include(running: Sequence[ReqView], m: int) -> List[ReqView]:
+    rs = list(running)
+    rows = np.zeros((len(rs), 8), dtype=np.int64)
+    if rs:
+        rows[:, 0] = _ranks([v.req_id for v in rs])
+    for k, v in enumerate(rs):
+        rows[k, 1:5] = (int(is_returned(v)), v.allocated, target_alloc(v), est_remaining(v))
+    out = _run(SOP_PROACTIVE_INCLUDE, rows, [m])
+    return [rs[int(x)] for x in out[1:1 + int(out[0])]]
+
+
+# -- baseline grant arithmetic (scheduler.py:282-288) ----------------------------
+
+def s3_demand(predicted: int, bucket_tokens: int, preempt_count: int) -> int:
+    buckets = max(1, math.ceil(max(1, predicted) / bucket_tokens))
+    return buckets * bucket_tokens * (2 ** preempt_count)
+
+
+def rlp_demand(predicted_remaining: int, padding: int) -> int:
+    return max(1, predicted_remaining) + padding
+
+
+# -- victim ordering (preemption.py:38-75) ----------------------------------------
+
+def victim_key(slo_tbt_us: int, remaining_tokens: int, occupancy_tokens: int, req_id: int,
+               cfg: BucketConfig) -> Tuple[int, int, int, int]:
+    slo_b = sum(1 for e in cfg.slo_edges_us if slo_tbt_us >= e)
+    return (-slo_b, -(max(0, remaining_tokens) // cfg.token_step), occupancy_tokens, req_id)
+
+
+def order_victims(candidates: Iterable[VictimInfo], cfg: BucketConfig) -> List[VictimInfo]:
+    vs = list(candidates)
+    if not vs:
+        return []
+    edges = list(cfg.slo_edges_us)
+    if len(edges) > 6:
+        raise ValueError("at most 6 SLO bucket edges on the device")
+    rows = np.zeros((len(vs), 8), dtype=np.int64)
+    rows[:, 0] = _ranks([v.req_id for v in vs])
+    for k, v in enumerate(vs):
+        rows[k, 1:4] = (v.slo_tbt_us, v.remaining_tokens, v.occupancy_tokens)
+    out = _run(SOP_ORDER_VICTIMS, rows, [cfg.token_step, len(edges)] + edges)
+    return [vs[int(x)] for x in out[:len(vs)]]

@@ -71,7 +71,7 @@ def build_product(params: dict):
         sched=P.SchedulerConfig(**{"policy": "cacheopt", **params["sched"]}),
         predictor=P.PredictorConfig(**params["pred"]), truth=truth, seed=seed,
         fixed_confidence=params["fixed_confidence"], validate_every=params["validate_every"],
-        record_events=params.get("record_events", True))
+        record_events=params.get("record_events", True), allow_stacking=params.get("allow_stacking", False))
     return reqs, cfg
 
 

@@ -96,3 +96,42 @@ def test_baseline_configs_full_run(cuda_ok, which):
     orc = CacheOptOracle(reqs, cfg)
     orc.run()
     _compare(eng, orc, which)
+
+
+# allow_stacking=True (kvc.py:187-192, :212, :263-270): hosts carry several
+# guests (up to 4 at once in these regimes); the oracle's stacking is pinned
+# to the reference by tests/golden/stack_case* and the live cross-check
+@pytest.mark.parametrize("seed", [3, 8, 13, 14, 15, 21, 49, 57])
+def test_stacking_regimes_full_run(cuda_ok, seed):
+    from paper_2503_13773_b200 import Engine
+    p = case_params(seed)
+    p["allow_stacking"] = True
+    reqs, cfg = build_product(p)
+    eng = Engine(reqs, cfg)
+    eng.run_steps(0)
+    orc = CacheOptOracle(reqs, cfg)
+    orc.run()
+    _compare(eng, orc, f"stacking seed {seed}")
+    eng.close()
+
+
+@pytest.mark.parametrize("seed", [8, 13])
+def test_stacking_guest_lists_every_step(cuda_ok, seed):
+    # the pool's guest lists (embed order) and offsets after every step
+    from paper_2503_13773_b200 import Engine
+    p = case_params(seed)
+    p["allow_stacking"] = True
+    reqs, cfg = build_product(p)
+    eng = Engine(reqs, cfg)
+    orc = CacheOptOracle(reqs, cfg)
+    most = 0
+    while True:
+        more = eng.step()
+        orc.step()
+        want = {orc.rid[h]: [orc.rid[g] for g in gl] for h, gl in orc.guests.items() if gl}
+        got = {r: eng.pool.guests_of(r) for r in want}
+        assert got == want
+        most = max([most] + [len(v) for v in want.values()])
+        if not more:
+            break
+    assert most >= 3

@@ -28,6 +28,24 @@ def test_oracle_matches_live_reference(seed):
         assert orc.token_times[k] == eng.runtimes[rid].token_times_us
 
 
+@pytest.mark.parametrize("seed", [3, 14, 15, 21, 49])
+def test_oracle_matches_live_reference_with_stacking(seed):
+    # allow_stacking=True (kvc.py:187-192, :212, :263-270): hosts carry several guests
+    sys.path.insert(0, REFERENCE_SRC)
+    from kvcsim.engine import Engine
+    from oracle.cacheopt_oracle import CacheOptOracle
+    from oracle.make_golden import ref_build
+    from tests.cases import case_params
+    p = case_params(seed)
+    p["allow_stacking"] = True
+    reqs, cfg = ref_build(p)
+    eng = Engine(copy.deepcopy(reqs), cfg)
+    eng.run()
+    orc = CacheOptOracle(reqs, cfg)
+    orc.run()
+    assert orc.events == eng.events
+
+
 def test_config_slo_baselines_match_reference_calibration():
     import copy
     sys.path.insert(0, REFERENCE_SRC)
