@@ -248,6 +248,11 @@ int co_read_block_tables(co_engine* eng, int32_t* lens, int32_t* pages, int64_t 
 int co_data_stats(co_engine* eng, int64_t* stats);
 /* counts KV elements of every holder's tokens [0, used) that differ from the
  * synthetic content (0 = the data path never lost or misplaced a byte) */
+/* Split swap I/O totals (k_swapio, the host-link half of swap-out/in, run on
+ * a side stream beside the decode): out[6] = {bytes to host, bytes from host,
+ * device ns from its first CTA in to its last CTA out, summed over launches,
+ * launches that moved data, split on (0 = copies inside k_data), CTAs}. */
+int co_swap_io_stats(co_engine* eng, int64_t* out);
 int co_kv_verify(co_engine* eng, int64_t* mismatches, int64_t* checked);
 /* the last step's paged-decode outputs: member indices (sorted order),
  * context lengths, and out[member][layer][q_head][head_dim] fp32 */

@@ -433,6 +433,8 @@ class CacheOptOracle:
             self._drop_record(i)
             return
         self._push_pages(i)
+        if len(self.guests.get(i, ())) > 1:
+            self.multi_rehomes = getattr(self, "multi_rehomes", 0) + 1  # stacked guests re-homed at once
         for gid in self.guests.get(i, ()):
             self.host[gid] = -1
             self.off[gid] = 0

@@ -2,7 +2,7 @@
 // include/cacheopt.h.  One translation unit so every device helper inlines.
 //
 // Per engine step the stream runs:
-//   k_begin (guards + admission window) -> k_classify (grid: views, classes,
+//   k_classify (grid: the step's begin evaluated per CTA, admission, views, classes,
 //   block-ordered running/blown lists, the N'_w candidate head) -> k_serial
 //   (1 CTA x 256: the planner, then plan application + the rest of the step,
 //   gated invariant check inside) [-> NCCL reserve all-reduce
@@ -138,13 +138,22 @@ __device__ __forceinline__ void mirror_body(const Dev& d, LogMirror* m) {
 // with the instance's [free_tokens, reserved_blocks_current] (kvc.py:92-98,
 // :79) after apply, every step whether or not it ran.
 template <int MODE>
-__global__ void __launch_bounds__(NT, 1) k_serial(Dev d, LogMirror* mir, int64_t* pack) {
+__global__ void __launch_bounds__(NT, 1) k_serial(Dev d, LogMirror* mir, int64_t* pack, int32_t guard,
+                                                  int32_t reset) {
     pdl_enter();
     extern __shared__ __align__(16) uint8_t serial_smem[];
+    if (MODE != 1) {  // the step's begin (engine.py:606-614), evaluated read-only by k_classify
+        if (threadIdx.x == 0) begin_commit(d, guard, reset);
+        __syncthreads();
+    }
     if (d.ctl->active) {
         if (MODE != 1) plan_body(d, *reinterpret_cast<PlanSh*>(serial_smem));
         if (MODE == 2) __syncthreads();
         if (MODE != 0) apply_body(d, *reinterpret_cast<ApplySh*>(serial_smem));
+    }
+    if (MODE != 0) {
+        __syncthreads();
+        if (threadIdx.x == 0) classify_counters_reset(d);  // for the next step's k_classify
     }
     if (mir || (pack && MODE != 0)) __syncthreads();
     if (pack && MODE != 0 && threadIdx.x == 0) {
@@ -178,6 +187,9 @@ struct co_engine {
     int nranks = 1, rank = 0;
     cudaStream_t side = nullptr;
     cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
+    cudaStream_t io = nullptr;                           // split swap I/O (k_swapio)
+    cudaEvent_t io_fork = nullptr, io_join = nullptr;
+    bool io_pending = false;                             // k_swapio not yet joined by the compute stream
     int64_t* red = nullptr;  // two slots of [send 2][recv 2]; step j of a sequence uses slot j & 1
     int join_pending = -1;   // slot whose all-reduce the compute stream has not joined yet
     int last_slot = 0;       // slot of the last all-reduce enqueued (co_global_reserve)
@@ -269,9 +281,22 @@ static void launch_coop(void (*kern)(KArgs...), int grid, int block, cudaStream_
 // joins it only at the end of the NEXT step (the totals never
 // feed a decision), so a step's collective latency hides behind the next
 // step.  Every sequence ends with flush_join (a capture must rejoin its fork).
-static void flush_join(co_engine* E) {
+static void flush_n4(co_engine* E) {
     if (E->comm && E->join_pending >= 0) cudaStreamWaitEvent(E->stream, E->join[E->join_pending], 0);
     E->join_pending = -1;
+}
+// The split swap I/O (k_swapio) of a step overlaps that step's decode; the
+// compute stream joins it before the next step's planner/apply (which may
+// preempt or release the pages it writes), or at the end of the step/sequence.
+static bool flush_io(co_engine* E) {
+    if (!E->io_pending) return false;
+    cudaStreamWaitEvent(E->stream, E->io_join, 0);
+    E->io_pending = false;
+    return true;
+}
+static void flush_join(co_engine* E) {
+    flush_n4(E);
+    flush_io(E);
 }
 
 static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr, int32_t reset = 0,
@@ -280,22 +305,24 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr, i
     cudaStream_t s = E->stream;
     int64_t* pack = E->comm ? E->red + 4 * slot : nullptr;
     if (ev) mark(ev[0], s);
-    k_begin<<<1, 32, 0, s>>>(d, guard, reset);
-    if (ev) mark(ev[1], s);
+    if (ev) mark(ev[1], s);  // (no begin kernel: k_classify evaluates it, k_serial commits it)
     // PDL edges only between back-to-back kernels (an event node in between
     // is a full dependency anyway)
     const bool pdl = E->pdl;
-    launch_pdl(pdl && !ev, k_classify, d.nblk, 256, 0, s, d);
+    launch_pdl(pdl && !ev, k_classify, d.nblk, 256, 0, s, d, guard, reset);
     if (ev) mark(ev[2], s);
     if (ev) mark(ev[3], s);  // (no bucket stage: k_classify collects the N'_w head)
+    const bool io_waited = flush_io(E);  // the previous step's swap I/O, before this apply
     if (ev) {
         launch_pdl(false, k_serial<0>, 1, E->plan_threads, sizeof(PlanSh), s, d, (LogMirror*)nullptr,
-                   (int64_t*)nullptr);
+                   (int64_t*)nullptr, guard, reset);
         mark(ev[4], s);
-        launch_pdl(false, k_serial<1>, 1, E->plan_threads, sizeof(PlanSh), s, d, (LogMirror*)nullptr, pack);
+        launch_pdl(false, k_serial<1>, 1, E->plan_threads, sizeof(PlanSh), s, d, (LogMirror*)nullptr, pack,
+                   guard, reset);
         mark(ev[5], s);
     } else {
-        launch_pdl(pdl, k_serial<2>, 1, E->plan_threads, sizeof(PlanSh), s, d, mir, pack);
+        launch_pdl(pdl && !io_waited, k_serial<2>, 1, E->plan_threads, sizeof(PlanSh), s, d, mir, pack, guard,
+                   reset);
     }
     if (ev) mark(ev[6], s);  // (the validate_every check runs inside k_apply)
     if (E->comm) {
@@ -309,6 +336,13 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr, i
     }
     if (d.dp.on) {
         launch_coop(k_data, E->sms, 512, s, d, d.dp, d.dctl, 0);
+        if (d.dp.split_io) {
+            cudaEventRecord(E->io_fork, s);
+            cudaStreamWaitEvent(E->io, E->io_fork, 0);
+            k_swapio<<<d.dp.io_ctas, IO_T, 0, E->io>>>(d, d.dp, d.dctl);
+            cudaEventRecord(E->io_join, E->io);
+            E->io_pending = true;
+        }
         if (ev) mark(ev[7], s);
         if (d.dp.decode_on) {
             if (E->tc_decode) {
@@ -327,10 +361,11 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr, i
         mark(ev[8], s);
     }
     if (E->comm) {
-        flush_join(E);  // the previous step's collective (deferred) ...
+        flush_n4(E);  // the previous step's collective (deferred) ...
         E->join_pending = slot;
-        if (!defer) flush_join(E);  // ... and this one's unless deferred to the next step
+        if (!defer) flush_n4(E);  // ... and this one's unless deferred to the next step
     }
+    if (!defer) flush_io(E);  // (after the decode it overlapped)
     return CO_OK;
 }
 
@@ -441,6 +476,9 @@ int co_destroy(co_engine* E) {
     if (E->result_host) cudaFreeHost(E->result_host);
     if (E->comm) nccl().commDestroy(E->comm);
     if (E->side) cudaStreamDestroy(E->side);
+    if (E->io) { cudaStreamSynchronize(E->io); cudaStreamDestroy(E->io); }
+    if (E->io_fork) cudaEventDestroy(E->io_fork);
+    if (E->io_join) cudaEventDestroy(E->io_join);
     if (E->fork) cudaEventDestroy(E->fork);
     for (cudaEvent_t j : E->join)
         if (j) cudaEventDestroy(j);
@@ -653,6 +691,22 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
         x.group_moves = cfg->allow_stacking ? 1 : 0;
         x.stage_tokens = cfg->allow_stacking ? std::max<int64_t>(max_s, cfg->capacity_tokens) + 1 : max_s + 1;
         AL(x.stage, x.stage_tokens * x.rows * x.D);
+        // split swap I/O (default on; CACHEOPT_SPLIT_IO=0 runs the host-link
+        // copies inside k_data, before the decode, as round 1 did)
+        x.split_io = 1;
+        if (const char* sv = std::getenv("CACHEOPT_SPLIT_IO")) x.split_io = std::atoi(sv) != 0;
+        x.io_ctas = 32;
+        if (const char* cv = std::getenv("CACHEOPT_IO_CTAS")) x.io_ctas = std::max(1, std::atoi(cv));
+        x.gstage_tokens = x.split_io ? cfg->capacity_tokens + 1 : 0;
+        if (x.split_io) {
+            AL(x.gstage, x.gstage_tokens * x.rows * x.D);
+            if (cudaStreamCreateWithFlags(&E->io, cudaStreamNonBlocking) != cudaSuccess ||
+                cudaEventCreateWithFlags(&E->io_fork, cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&E->io_join, cudaEventDisableTiming) != cudaSuccess) {
+                co_destroy(E);
+                return fail(CO_ECUDA, "swap I/O stream");
+            }
+        }
         x.op_cap = 8 * n + 4096;
         x.snap_cap = 16 * (int64_t)n_pages + 8 * n + 65536;
         AL(x.ops, x.op_cap); AL(x.snap, x.snap_cap); AL(x.hstack, x.h_pages);
@@ -756,6 +810,7 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     std::memset(&c0, 0, sizeof(c0));
     c0.now = first; c0.horizon = horizon; c0.first_arrival = first; c0.t_i = cfg->t_i_init_us;
     c0.rsv_cur = cfg->reserved_blocks;
+    c0.kmin = ~0ull;  // classify key range, reset after every step by k_serial
     c0.free_top = n_pages;
     c0.chunk_top = (int32_t)n_chunks;
     *E->h_ctl = c0;
@@ -1334,6 +1389,18 @@ int co_data_stats(co_engine* E, int64_t* st) {
     return CO_OK;
 }
 
+int co_swap_io_stats(co_engine* E, int64_t* out) {
+    if (!E || !out) return fail(CO_EINVAL, "null argument");
+    if (!E->d.dp.on) return fail(CO_EINVAL, "data plane is off (kv_layers = 0)");
+    CK(cudaStreamSynchronize(E->stream));
+    DataCtl dc;
+    CK(cudaMemcpyAsync(&dc, E->d.dctl, sizeof(dc), cudaMemcpyDeviceToHost, E->stream));
+    CK(cudaStreamSynchronize(E->stream));
+    out[0] = dc.io_bytes_out; out[1] = dc.io_bytes_in; out[2] = dc.io_ns; out[3] = dc.io_launches;
+    out[4] = E->d.dp.split_io; out[5] = E->d.dp.io_ctas;
+    return CO_OK;
+}
+
 int co_kv_verify(co_engine* E, int64_t* bad, int64_t* checked) {
     if (!E || !bad || !checked) return fail(CO_EINVAL, "null argument");
     { int rw_ = begin_work(E); if (rw_) return rw_; }
@@ -1434,7 +1501,7 @@ int co_swap_bench(co_engine* E, int64_t ntok, int32_t iters, double* out_ms, dou
     std::vector<int32_t> snap(2 * np);
     for (int64_t k = 0; k < np; k++) { snap[k] = (int32_t)k; snap[np + k] = (int32_t)k; }
     CK(cudaMemcpyAsync(x.snap, snap.data(), snap.size() * 4, cudaMemcpyHostToDevice, E->stream));
-    DOp ops[2];
+    DOp ops[2] = {};
     for (int q = 0; q < 2; q++) {
         ops[q].kind = q == 0 ? D_GATHER : D_SCATTER; ops[q].req = 0; ops[q].ntok = (int32_t)ntok; ops[q].t0 = 0;
         ops[q].src_end = ops[q].dst_end = -1;
@@ -1533,8 +1600,8 @@ int co_phase_profile(co_engine* E, int32_t enable, int64_t* out /* 64 */) {
 int co_kernels_per_step(co_engine* E, int32_t* n) {
     if (!E || !n) return fail(CO_EINVAL, "null argument");
     // begin, classify(+admit, N'_w head), serial (plan + apply + check
-    // [+ mirror]); the data plane adds k_data (+ decode + combine)
-    *n = 3 + (E->d.dp.on ? 1 + (E->d.dp.decode_on ? 2 : 0) : 0);
+    // [+ mirror]); the data plane adds k_data (+ k_swapio, + decode + combine)
+    *n = 2 + (E->d.dp.on ? 1 + (E->d.dp.split_io ? 1 : 0) + (E->d.dp.decode_on ? 2 : 0) : 0);
     return CO_OK;
 }
 

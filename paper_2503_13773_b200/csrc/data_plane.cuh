@@ -112,6 +112,14 @@ __device__ void log_swap_out(const Dev& d, const DataCfg& x, int i) {
     }
     x.hsaved[i] = hp;
     op.dst_where = W_HOST; op.dst_snap = o; op.dst_end = -1;
+    op.io = 0; op.hp = 0; op.stage_off = -1;
+    if (x.split_io) {  // k_data stages the pages in HBM; k_swapio sends them over the link
+        if (c.stage_fill + ntok > x.gstage_tokens) { d.ctl->error = 6; return; }
+        op.io = 1;
+        op.stage_off = c.stage_fill;
+        c.stage_fill += ntok;
+        c.n_io += 1;
+    }
     log_op(d, x, op);
 }
 // readmission: swap-in of the restored prefix or its recompute
@@ -124,12 +132,23 @@ __device__ void log_readmit(const Dev& d, const DataCfg& x, int i, bool swap) {
         DOp op;
         op.req = i; op.ntok = ntok; op.t0 = 0;
         op.dst_where = W_TABLE; op.dst_snap = 0; op.dst_end = -1;
+        op.io = 0; op.hp = 0; op.stage_off = -1;
         if (swap && hp > 0) {
             op.kind = D_SCATTER;
             int64_t o = snap_alloc(d, x, hp);
             if (o < 0) return;
             for (int32_t k = 0; k < hp; k++) x.snap[o + k] = x.hdir[(int64_t)i * x.hdir_w + k];
             op.src_where = W_HOST; op.src_snap = o; op.src_end = -1;
+            if (x.split_io) {
+                // k_swapio reads the host pages after this step's apply, so
+                // they return to the swap pool only once it has (below)
+                op.io = 1;
+                op.hp = hp;
+                c.n_io += 1;
+                log_op(d, x, op);
+                x.hsaved[i] = 0;
+                return;
+            }
         } else {
             op.kind = D_FILL;
             op.src_where = W_DEV; op.src_snap = 0; op.src_end = -1;
@@ -145,6 +164,7 @@ __device__ void log_move(const Dev& d, const DataCfg& x, int g, int32_t ntok, in
     if (!x.on || ntok <= 0) return;
     DOp op;
     op.kind = D_MOVE; op.req = g; op.ntok = ntok; op.t0 = 0;
+    op.io = 0; op.hp = 0; op.stage_off = -1;
     op.src_where = W_DEV; op.src_snap = src_snap; op.src_end = src_end;
     op.dst_where = W_DEV; op.dst_end = -1;
     op.dst_snap = snap_table(d, x, g, (ntok + d.bs - 1) / d.bs);
@@ -155,6 +175,7 @@ __device__ void log_fill(const Dev& d, const DataCfg& x, int i, int32_t t0, int3
     if (!x.on || n <= 0) return;
     DOp op;
     op.kind = D_FILL; op.req = i; op.ntok = n; op.t0 = t0;
+    op.io = 0; op.hp = 0; op.stage_off = -1;
     op.src_where = W_DEV; op.src_snap = 0; op.src_end = -1;
     if (d.host[i] >= 0) {
         op.dst_where = W_DEV;
@@ -205,6 +226,11 @@ __device__ __forceinline__ int64_t loc_elem(const Dev& d, const DataCfg& x, int3
     return (int64_t)page * x.page_elems + ((int64_t)row * bs + slot) * x.D;
 }
 
+// tokens an op moves inside k_data (a split SCATTER is k_swapio's entirely)
+__device__ __forceinline__ int64_t kdata_tokens(const DOp& op) {
+    return (op.kind == D_SCATTER && op.io) ? 0 : op.ntok;
+}
+
 __global__ void __launch_bounds__(512, 1) k_data(Dev d, DataCfg x, DataCtl* dc, int force = 0) {
     const Ctl& c = *d.ctl;
     if (!(c.active || force) || !x.on) return;
@@ -225,14 +251,14 @@ __global__ void __launch_bounds__(512, 1) k_data(Dev d, DataCfg x, DataCtl* dc, 
         }
         // ops [a, b): independent, same kind; flat work over their units
         int64_t total = 0;
-        for (int32_t o = a; o < b; o++) total += (int64_t)x.ops[o].ntok * units_per_tok;
+        for (int32_t o = a; o < b; o++) total += kdata_tokens(x.ops[o]) * units_per_tok;
         const int passes = kind == D_MOVE ? 2 : 1;
         for (int pass = 0; pass < passes; pass++) {
             int32_t o = a;
             int64_t obase = 0;
             for (int64_t u = gtid; u < total; u += gsz) {
-                while (u >= obase + (int64_t)x.ops[o].ntok * units_per_tok) {
-                    obase += (int64_t)x.ops[o].ntok * units_per_tok;
+                while (u >= obase + kdata_tokens(x.ops[o]) * units_per_tok) {
+                    obase += kdata_tokens(x.ops[o]) * units_per_tok;
                     o++;
                 }
                 const DOp& op = x.ops[o];
@@ -264,6 +290,8 @@ __global__ void __launch_bounds__(512, 1) k_data(Dev d, DataCfg x, DataCtl* dc, 
                 }
                 if (op.kind == D_MOVE && pass == 0) {
                     dst = x.stage + (so * x.rows + r) * x.D + ch * 8;
+                } else if (op.kind == D_GATHER && op.io) {  // split I/O: stage in HBM
+                    dst = x.gstage + ((op.stage_off + j) * x.rows + r) * x.D + ch * 8;
                 } else {
                     uint16_t* base = op.dst_where == W_HOST ? x.hkv : x.kv;
                     dst = base + loc_elem(d, x, op.dst_where, op.dst_snap, op.dst_end, op.req, tok, r) + ch * 8;
@@ -287,8 +315,85 @@ __global__ void __launch_bounds__(512, 1) k_data(Dev d, DataCfg x, DataCtl* dc, 
                 default: dc->bytes_fill += bytes;
             }
         }
-        dc->n_ops = 0;
-        dc->n_snap = 0;
+        if (dc->n_io == 0) {  // else k_swapio still reads the log and the snapshots
+            dc->n_ops = 0;
+            dc->n_snap = 0;
+        }
+    }
+}
+
+// The host-link half of the split swap I/O, on a side stream while the
+// decode runs: staged swap-outs to the pinned host pool, swap-ins from it
+// into the restored request's pages.  Every such op touches its own pages
+// (fresh host pages, the staging slot, or pages of a request that is not a
+// decode member before its ready time), so they are independent: one flat
+// grid-stride pass, no barrier, an ordinary launch of `io_ctas` small CTAs
+// that fit beside the decode's one-CTA-per-SM residency.  The last CTA out
+// returns the swap-ins' host pages to the pool and clears the log.
+constexpr int IO_T = 256;
+__global__ void __launch_bounds__(IO_T) k_swapio(Dev d, DataCfg x, DataCtl* dc) {
+    const int32_t nops = dc->n_ops;
+    if (dc->n_io == 0) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        dc->io_t0 = (int64_t)t;
+    }
+    const int64_t upt = (int64_t)x.rows * (x.D / 8);
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gsz = (int64_t)gridDim.x * blockDim.x;
+    int64_t obase = 0;
+    for (int32_t o = 0; o < nops; o++) {
+        const DOp& op = x.ops[o];
+        if (!op.io) continue;
+        const int64_t units = (int64_t)op.ntok * upt;
+        // this thread's first unit of the op (units are numbered across io ops)
+        int64_t u0 = gtid - obase % gsz;
+        if (u0 < 0) u0 += gsz;
+        for (int64_t w = u0; w < units; w += gsz) {
+            const int32_t j = (int32_t)(w / upt);
+            const int32_t r = (int32_t)((w % upt) / (x.D / 8));
+            const int32_t ch = (int32_t)(w % (x.D / 8));
+            const uint16_t* src;
+            uint16_t* dst;
+            if (op.kind == D_GATHER) {
+                src = x.gstage + ((op.stage_off + j) * x.rows + r) * x.D + ch * 8;
+                dst = x.hkv + loc_elem(d, x, W_HOST, op.dst_snap, -1, op.req, j, r) + ch * 8;
+            } else {
+                src = x.hkv + loc_elem(d, x, W_HOST, op.src_snap, -1, op.req, j, r) + ch * 8;
+                dst = x.kv + loc_elem(d, x, W_TABLE, 0, -1, op.req, j, r) + ch * 8;
+            }
+            *reinterpret_cast<uint4*>(dst) = __ldcv(reinterpret_cast<const uint4*>(src));
+        }
+        obase += units;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&dc->io_done, 1) == (int)gridDim.x - 1) {
+            __threadfence();
+            DataCtl& c = *dc;
+            const int64_t tb = (int64_t)x.rows * x.D * 2;
+            for (int32_t o = 0; o < nops; o++) {
+                const DOp& op = x.ops[o];
+                if (!op.io) continue;
+                if (op.kind == D_GATHER) {
+                    c.io_bytes_out += (int64_t)op.ntok * tb;
+                } else {
+                    c.io_bytes_in += (int64_t)op.ntok * tb;
+                    for (int32_t k = op.hp - 1; k >= 0; k--) x.hstack[c.htop++] = x.snap[op.src_snap + k];
+                }
+            }
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            c.io_ns += (int64_t)t - c.io_t0;
+            c.io_launches += 1;
+            c.n_io = 0;
+            c.io_done = 0;
+            c.stage_fill = 0;
+            c.n_ops = 0;
+            c.n_snap = 0;
+        }
     }
 }
 

@@ -11,6 +11,11 @@ struct DOp {
     int32_t kind, req, ntok, t0;
     int32_t src_where, dst_where, src_end, dst_end;
     int64_t src_snap, dst_snap;
+    // split swap I/O (DataCfg::split_io): io = 1 marks a GATHER / SCATTER whose
+    // host-link half runs in k_swapio (side stream, overlapping the decode);
+    // a GATHER's pages are first staged at gstage[stage_off ..) by k_data
+    int64_t stage_off;
+    int32_t io, hp;  // hp: host pages a deferred SCATTER returns to the swap pool
 };
 
 struct DataCfg {
@@ -42,6 +47,11 @@ struct DataCfg {
     // new pages can be the pages that still hold a later guest's KV, so a run
     // of MOVEs is staged as one group (all reads, then all writes)
     int32_t group_moves;
+    // swap-out staging (HBM, token-major, `gstage_tokens` = the pool's tokens:
+    // every victim's KV of one step was resident at once) for the split I/O
+    uint16_t* gstage;
+    int64_t gstage_tokens;
+    int32_t split_io, io_ctas;
 };
 
 struct DataCtl {
@@ -50,6 +60,10 @@ struct DataCtl {
     int64_t bytes_out, bytes_in, bytes_fill, bytes_move;
     int64_t dec_steps, dec_members, dec_tokens;
     int64_t last_bytes_out, last_bytes_in;
+    // split swap I/O: ops pending for k_swapio, staged tokens, and its
+    // device-timed totals (%globaltimer, first CTA in -> last CTA out)
+    int32_t n_io, io_done;
+    int64_t stage_fill, io_t0, io_ns, io_bytes_out, io_bytes_in, io_launches;
 };
 
 }  // namespace co

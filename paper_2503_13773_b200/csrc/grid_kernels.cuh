@@ -1,6 +1,7 @@
 // Grid-wide (data-parallel) phases of one engine step:
-//   k_begin     engine.py:606-614 guards, clock jump and the arrival window
-//   k_admit     engine.py:344-353 + estimation.py:85-128 (row a1)
+//   begin_*     engine.py:606-614 guards, clock jump and the arrival window
+//               (evaluated by every k_classify CTA, committed by k_serial)
+//   admit_one   engine.py:344-353 + estimation.py:85-128 (row a1), in k_classify
 //   k_classify  engine.py:284-334 snapshot + scheduler.py:129-163 (rows a2/a3):
 //               one 64-bit composite sort key per request so ONE radix sort
 //               yields N_w (by rt,id), N'_w (by queue key) and the running
@@ -11,42 +12,93 @@
 
 namespace co {
 
-// reset = 1: the host consumed the whole append log from the step mirror
-// (co_engine::drain fast path), so it restarts empty
-__global__ void k_begin(Dev d, int32_t guard, int32_t reset) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    Ctl& c = *d.ctl;
-    if (reset) { c.ev_count = 0; c.mem_count = 0; c.sample_count = 0; c.paused = 0; }
-    c.active = 0;
-    if (d.result) d.result[0] = -1;
-    if (c.done) { c.last_result = 0; return; }
-    if (c.paused || c.error) return;
+// engine.py:606-614 step guards, the clock jump and the arrival window, as a
+// PURE function of the control block at the step's start: every k_classify
+// CTA evaluates it to know the step's clock and admission window, and
+// k_serial's thread 0 evaluates it again and commits it (begin_commit)
+// before planning -- so no kernel of its own runs ahead of classify, and no
+// CTA ever reads a half-updated control block.  reset = 1: the host consumed
+// the whole append log from the step mirror, so it restarts empty.
+struct BeginR {
+    int32_t active, paused, done, err3, adm_lo, adm_hi;
+    int64_t now, ev0;  // ev0: where this step's arrive records start
+};
+__device__ __forceinline__ int32_t arrivals_upto(const Dev& d, int32_t lo, int64_t now) {
+    // first index >= lo with arr > now: gallop from lo (the window is usually
+    // short), then binary search
+    int32_t hi = d.n;
+    if (lo >= hi || d.arr[lo] > now) return lo;
+    int32_t step = 1, prev = lo;
+    while (true) {
+        const int32_t probe = lo + step;
+        if (probe >= hi) break;
+        if (d.arr[probe] > now) { hi = probe; break; }
+        prev = probe;
+        step <<= 1;
+    }
+    lo = prev + 1;
+    while (lo < hi) {
+        const int32_t mid = lo + (hi - lo) / 2;
+        if (d.arr[mid] <= now) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+__device__ __forceinline__ BeginR begin_eval(const Dev& d, const Ctl& c, int32_t guard, int32_t reset) {
+    BeginR r{};
+    r.active = 0;
+    const int64_t ev_count = reset ? 0 : c.ev_count, mem_count = reset ? 0 : c.mem_count,
+                  sample_count = reset ? 0 : c.sample_count;
+    const int32_t paused = reset ? 0 : c.paused;
+    r.ev0 = ev_count;
+    r.now = c.now;
+    if (c.done) { r.done = 1; return r; }
+    if (paused || c.error) { r.paused = paused; return r; }
     // append-buffer headroom for the worst case of this step: pause (the host
     // drains and relaunches) before touching any state
     {
         int64_t now = c.now;
         if (c.n_live == 0 && c.next_pending < d.n && d.arr[c.next_pending] > now) now = d.arr[c.next_pending];
-        int32_t lo = c.next_pending, hi = d.n;
-        while (lo < hi) {
-            int32_t mid = lo + (hi - lo) / 2;
-            if (d.arr[mid] <= now) lo = mid + 1; else hi = mid;
-        }
-        int64_t live_after = (int64_t)c.n_live + (lo - c.next_pending);
-        bool full = c.sample_count + 1 > d.sample_cap;
+        const int32_t lo = arrivals_upto(d, c.next_pending, now);
+        const int64_t live_after = (int64_t)c.n_live + (lo - c.next_pending);
+        bool full = sample_count + 1 > d.sample_cap;
         if (d.record_events)
-            full = full || c.ev_count + (lo - c.next_pending) + 4 * live_after + 8 > d.ev_cap ||
-                   c.mem_count + live_after + 8 > d.mem_cap;
-        if (full) { c.paused = 1; return; }
+            full = full || ev_count + (lo - c.next_pending) + 4 * live_after + 8 > d.ev_cap ||
+                   mem_count + live_after + 8 > d.mem_cap;
+        if (full) { r.paused = 1; return r; }
     }
+    if (guard) {
+        // engine.py:644-659 no-progress guard, evaluated before each step()
+        const int64_t m[5] = {c.now, c.gen_total, c.n_live, (int64_t)(d.n - c.next_pending), c.fp_sum};
+        bool same = c.has_mark;
+        for (int k = 0; k < 5; k++) same = same && m[k] == c.mark[k];
+        if (same && c.streak + 1 > 1000000) { r.err3 = 1; r.done = 1; return r; }
+    }
+    if (c.n_live == 0 && c.next_pending >= d.n) { r.done = 1; return r; }
+    if (c.now > c.horizon) { r.done = 1; return r; }
+    int64_t now = c.now;
+    if (c.n_live == 0 && d.arr[c.next_pending] > now) now = d.arr[c.next_pending];
+    r.now = now;
+    r.adm_lo = c.next_pending;
+    r.adm_hi = arrivals_upto(d, c.next_pending, now);
+    r.active = 1;
+    return r;
+}
+// k_serial thread 0: apply the step's begin to the control block (what the
+// round-1 k_begin kernel wrote), given the classify CTAs' counts untouched
+__device__ __forceinline__ void begin_commit(const Dev& d, int32_t guard, int32_t reset) {
+    Ctl& c = *d.ctl;
+    const BeginR r = begin_eval(d, c, guard, reset);
+    if (reset) { c.ev_count = 0; c.mem_count = 0; c.sample_count = 0; c.paused = 0; }
+    c.active = 0;
+    if (d.result) d.result[0] = -1;
+    if (c.done) { c.last_result = 0; return; }
+    if (c.paused || c.error) return;
+    if (r.paused) { c.paused = 1; return; }
     c.last_result = 0;
     c.sid += 1;
     if (d.dp.on) { d.dctl->n_dec = 0; d.dctl->dec_items = 0; }
-    c.cnt_nw = c.cnt_nwp = c.cnt_run = c.cnt_blown = c.cnt_cand = 0;
-    c.kmin = ~0ull;
-    c.kmax = 0;
     if (guard) {
-        // engine.py:644-659 no-progress guard, evaluated before each step()
-        int64_t m[5] = {c.now, c.gen_total, c.n_live, (int64_t)(d.n - c.next_pending), c.fp_sum};
+        const int64_t m[5] = {c.now, c.gen_total, c.n_live, (int64_t)(d.n - c.next_pending), c.fp_sum};
         bool same = c.has_mark;
         for (int k = 0; k < 5; k++) same = same && m[k] == c.mark[k];
         if (same) {
@@ -59,22 +111,24 @@ __global__ void k_begin(Dev d, int32_t guard, int32_t reset) {
         c.has_mark = 1;
     }
     c.steps += 1;
-    if (c.n_live == 0 && c.next_pending >= d.n) { c.done = 1; return; }
-    if (c.now > c.horizon) { c.done = 1; return; }
-    if (c.n_live == 0 && d.arr[c.next_pending] > c.now) c.now = d.arr[c.next_pending];
-    int32_t lo = c.next_pending, hi = d.n;
-    while (lo < hi) {
-        int32_t mid = lo + (hi - lo) / 2;
-        if (d.arr[mid] <= c.now) lo = mid + 1; else hi = mid;
-    }
-    int32_t adm = lo - c.next_pending;
-    c.adm_lo = c.next_pending;
-    c.adm_hi = lo;
-    c.next_pending = lo;
+    if (r.done) { c.done = 1; return; }
+    c.now = r.now;
+    const int32_t adm = r.adm_hi - r.adm_lo;
+    c.adm_lo = r.adm_lo;
+    c.adm_hi = r.adm_hi;
+    c.next_pending = r.adm_hi;
     c.n_live += adm;
     c.decisions += c.n_live;  // one decision per live request per step
-    if (d.record_events) c.ev_count += adm;  // arrive records written by k_admit
+    if (d.record_events) c.ev_count += adm;  // arrive records written by k_classify
     c.active = 1;
+}
+// the classify counters for the NEXT step (k_serial's tail, after the
+// planner consumed this step's)
+__device__ __forceinline__ void classify_counters_reset(const Dev& d) {
+    Ctl& c = *d.ctl;
+    c.cnt_nw = c.cnt_nwp = c.cnt_run = c.cnt_blown = c.cnt_cand = 0;
+    c.kmin = ~0ull;
+    c.kmax = 0;
 }
 
 // estimation.py:92-99 + 122-128 with the host-drawn noise, and the arrive
@@ -107,18 +161,21 @@ __device__ __forceinline__ void admit_one(const Dev& d, int32_t i, int32_t lo, i
 // The planner's 64-byte views are written for the running, critical, blown
 // and candidate requests only: a waiting request outside the head costs one
 // state byte and one key read per step.
-__global__ void __launch_bounds__(256) k_classify(Dev d) {
+__global__ void __launch_bounds__(256) k_classify(Dev d, int32_t guard, int32_t reset) {
     pdl_enter();
     __shared__ int32_t sc[32];
-    __shared__ int32_t tot_s[2];
     __shared__ uint64_t kr[2][8];
+    __shared__ int32_t tot_s[2];
+    __shared__ BeginR br;
     const Ctl& c = *d.ctl;
-    if (!c.active) return;
-    const int64_t now = c.now, ti = c.t_i, eps = d.eps;
+    if (threadIdx.x == 0) br = begin_eval(d, c, guard, reset);  // the step's begin, read-only
+    __syncthreads();
+    if (!br.active) return;
+    const int64_t now = br.now, ti = c.t_i, eps = d.eps;
     const uint64_t thr = c.thr;
-    const int32_t hi_live = c.next_pending;
-    const int32_t alo = c.adm_lo, ahi = c.adm_hi;
-    const int64_t ev0 = c.ev_count - (ahi - alo);
+    const int32_t hi_live = br.adm_hi;
+    const int32_t alo = br.adm_lo, ahi = br.adm_hi;
+    const int64_t ev0 = br.ev0;
     const int32_t lo = blockIdx.x * d.chunk, hi = min(d.n, lo + d.chunk);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int32_t run_base = 0, blown_base = 0, ncrit = 0, nf0 = 0;

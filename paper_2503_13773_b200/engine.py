@@ -576,6 +576,15 @@ class Engine:
                 "decode_member_steps", "decode_ctx_tokens")
         return dict(zip(keys, (int(v) for v in st)))
 
+    def swap_io_stats(self) -> Dict[str, float]:
+        """The split swap I/O's device-timed totals (k_swapio beside the decode):
+        bytes each way over the host link, device seconds, launches."""
+        st = np.zeros(6, dtype=np.int64)
+        N.check(self._lib.co_swap_io_stats(self._h, _ptr(st, C.c_int64)), "co_swap_io_stats")
+        out, inn, ns, launches, split, ctas = (int(v) for v in st)
+        return {"bytes_out": out, "bytes_in": inn, "device_s": ns * 1e-9, "launches": launches,
+                "gbs": (out + inn) / (ns * 1e-9) / 1e9 if ns else 0.0, "split": bool(split), "ctas": ctas}
+
     # -- N4 global reserve telemetry ---------------------------------------------
 
     def attach_nccl(self, uid: bytes, nranks: int, rank: int) -> None:

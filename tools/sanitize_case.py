@@ -15,9 +15,13 @@ from tests.cases import build_product, case_params  # noqa: E402
 
 mode = sys.argv[1] if len(sys.argv) > 1 else "sched"
 seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
-reqs, cfg = build_product(case_params(seed))
+max_steps = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # 0: to the end
+params = case_params(seed)
+if mode == "stack":  # several guests per host; their re-homing goes through the grouped MOVE staging
+    params["allow_stacking"] = True
+reqs, cfg = build_product(params)
 kv = None
-if mode == "data":
+if mode in ("data", "stack"):
     pages = cfg.capacity_tokens // cfg.sched.small_block_b
     kv = P.KVLayout(layers=2, kv_heads=2, q_heads=16, host_swap_pages=16 * pages + 64, decode=True, decode_split=64)
 eng = P.Engine(reqs, cfg, kv=kv)
@@ -29,14 +33,22 @@ for _ in range(60):  # per-step API (the mirrored step graph)
     steps += 1
     if not more:
         break
-eng.run_steps(0)  # multi-step graphs to the end
-orc.run()
+if max_steps:
+    eng.run_steps(max_steps)  # a multi-step graph
+    for _ in range(max_steps):
+        orc.step()
+else:
+    eng.run_steps(0)  # multi-step graphs to the end
+    orc.run()
 assert eng.events == orc.events, "device events differ from the oracle"
 if kv is not None:
     bad, checked = eng.kv_verify()
     assert bad == 0, f"{bad} KV elements wrong"
-rep = eng.run()
-print(f"{mode} seed {seed}: {len(orc.events)} events identical; completed {rep.completed}")
+if not max_steps:
+    rep = eng.run()
+    print(f"{mode} seed {seed}: {len(orc.events)} events identical; completed {rep.completed}")
+else:
+    print(f"{mode} seed {seed}: {len(orc.events)} events identical after {steps + max_steps} steps")
 eng.close()
 if mode == "sched":
     from paper_2503_13773_b200 import devrng
