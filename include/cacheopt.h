@@ -248,6 +248,20 @@ int co_read_block_tables(co_engine* eng, int32_t* lens, int32_t* pages, int64_t 
 int co_data_stats(co_engine* eng, int64_t* stats);
 /* counts KV elements of every holder's tokens [0, used) that differ from the
  * synthetic content (0 = the data path never lost or misplaced a byte) */
+/* plan_batch(PlannerInputs, cfg) (scheduler.py:939-950) on a snapshot: the
+ * engine must have been created over the snapshot's requests (sorted order)
+ * without data plane or communicator.  cols [n][20] per request (sorted order):
+ * state, generated, used, kv_need, prefill_done, preemption_count, predicted,
+ * estimated, first_token_us (-1 = none), last_token_us, max_tbt_us, ready_at_us,
+ * holds, granted, host (index or -1), embed_offset, reserved_drawn, first guest,
+ * next guest, record creation seq; scal[8] = {now, t_i_max, reserved_current,
+ * footprint_sum, granted_sum, used_sum, record seq, live count}.  hdr[8] =
+ * {members, actions, preempt, claims, deferred, overflow, batch_tokens, active};
+ * lists = members (idx[], tokens[]), actions (kind[], idx[], tokens[], blocks[],
+ * host[], start[]), preempt (idx[], strategy[]), claims (waiter[], provider[]),
+ * deferred (idx[]) -- each array of its count, concatenated. */
+int co_plan_snapshot(co_engine* eng, const int64_t* cols, const int64_t* scal, int64_t* hdr, int32_t* lists,
+                     int64_t cap);
 /* Split swap I/O totals (k_swapio, the host-link half of swap-out/in, run on
  * a side stream beside the decode): out[6] = {bytes to host, bytes from host,
  * device ns from its first CTA in to its last CTA out, summed over launches,

@@ -84,7 +84,7 @@ class CoEvent(C.Structure):
 EXPORTS = (
     "co_create", "co_destroy", "co_step", "co_run", "co_preempt", "co_get_scalars", "co_read_field",
     "co_drain_events", "co_pending_events", "co_pending_log", "co_drain_log", "co_pool_create", "co_pool_destroy", "co_pool_op", "co_pool_find_host",
-    "co_pool_state", "co_pool_check", "co_pool_read_tables", "co_sched_op", "co_swap_io_stats", "co_drain_samples", "co_read_token_times",
+    "co_pool_state", "co_pool_check", "co_pool_read_tables", "co_sched_op", "co_swap_io_stats", "co_plan_snapshot", "co_drain_samples", "co_read_token_times",
     "co_check_invariants", "co_last_device_ms", "co_kernels_per_step", "co_time_steps", "co_last_error",
     "co_version", "co_read_block_tables", "co_data_stats", "co_kv_verify", "co_read_decode", "co_host_link_gbs",
     "co_set_decode", "co_swap_bench", "co_nccl_unique_id", "co_attach_nccl", "co_global_reserve",
@@ -156,6 +156,7 @@ def load() -> C.CDLL:
         "co_pool_check": (C.c_int, [V]),
         "co_sched_op": (C.c_int, [C.c_int32, C.c_int32, I64P, I64P, I64P, C.c_int32]),
         "co_swap_io_stats": (C.c_int, [V, I64P]),
+        "co_plan_snapshot": (C.c_int, [V, I64P, I64P, I64P, I32P, C.c_int64]),
         "co_pool_read_tables": (C.c_int, [V, I32P, I32P, C.c_int64, I32P, I32P]),
         "co_drain_log": (C.c_int, [V, C.POINTER(CoEvent), C.c_int64, I32P, C.c_int64, I64P, C.c_int64, I64P]),
         "co_drain_samples": (C.c_int, [V, I64P, C.c_int64, I64P]),

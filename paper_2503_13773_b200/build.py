@@ -23,7 +23,35 @@ def sources():
     return sorted((PKG / "csrc").glob("*.cu*")) + [PKG.parent / "include" / "cacheopt.h"]
 
 
+
+HOSTLOG_SRC = PKG / "csrc" / "hostlog.c"
+
+
+def hostlog_path() -> Path:
+    import sysconfig
+    return PKG / ("_hostlog" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_hostlog(force: bool = False) -> Path:
+    """The CPython extension that turns drained device events into the
+    reference's dicts (csrc/hostlog.c), built in-tree with the system C
+    compiler against this interpreter's headers."""
+    import sysconfig
+    out = hostlog_path()
+    if out.exists() and not force and out.stat().st_mtime >= HOSTLOG_SRC.stat().st_mtime:
+        return out
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if not cc:
+        raise RuntimeError("no C compiler for csrc/hostlog.c")
+    tmp = out.with_suffix(".tmp")
+    subprocess.run([cc, "-O2", "-shared", "-fPIC", "-I", sysconfig.get_paths()["include"], "-o", str(tmp),
+                    str(HOSTLOG_SRC)], check=True)
+    tmp.replace(out)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
+    build_hostlog(force)
     if OUT.exists() and not force:
         newest = max(p.stat().st_mtime for p in sources())
         if OUT.stat().st_mtime >= newest:

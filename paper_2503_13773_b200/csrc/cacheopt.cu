@@ -1389,6 +1389,85 @@ int co_data_stats(co_engine* E, int64_t* st) {
     return CO_OK;
 }
 
+// ---- snapshot planning: plan_batch(PlannerInputs, cfg) (scheduler.py:939-950)
+// The caller's views and pool records are written into the engine's SoA (the
+// request space of a co_create over the views' ids) and ONE planner pass runs
+// -- k_classify, then k_serial in plan-only mode -- with the plan read back.
+constexpr int SNAP_COLS = 20;
+__global__ void k_load_snapshot(Dev d, const int64_t* __restrict__ col, int32_t n) {
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int64_t* r = col + (int64_t)i * SNAP_COLS;
+        d.state[i] = (int8_t)r[0];
+        d.gen[i] = (int32_t)r[1]; d.used[i] = (int32_t)r[2]; d.kv_need[i] = (int32_t)r[3];
+        d.prefill[i] = (int32_t)r[4]; d.pcount[i] = (int32_t)r[5]; d.pred[i] = (int32_t)r[6];
+        d.est[i] = (int32_t)r[7];
+        d.first_tok[i] = r[8]; d.last_tok[i] = r[9]; d.max_tbt[i] = r[10]; d.ready_at[i] = r[11];
+        d.holds[i] = (uint8_t)r[12]; d.granted[i] = (int32_t)r[13]; d.host[i] = (int32_t)r[14];
+        d.off[i] = (int32_t)r[15]; d.rsv[i] = (int32_t)r[16]; d.guest[i] = (int32_t)r[17];
+        d.gnext[i] = (int32_t)r[18]; d.rec_seq[i] = r[19];
+        const int8_t s = d.state[i];
+        if (s == ST_WAITING || s == ST_PREEMPTED) d.key0[i] = wait_key(d, i);
+    }
+}
+__global__ void k_load_snapshot_ctl(Dev d, int64_t now, int64_t ti, int32_t rsv, int64_t fp, int64_t gsum,
+                                    int64_t usum, int64_t seq, int32_t n_live) {
+    Ctl& c = *d.ctl;
+    c.now = now; c.t_i = ti; c.rsv_cur = rsv; c.fp_sum = fp; c.granted_sum = gsum; c.used_sum = usum;
+    c.seq = seq; c.n_live = n_live; c.next_pending = d.n; c.horizon = INT64_MAX / 4;
+    c.done = 0; c.paused = 0; c.error = 0; c.has_mark = 0; c.streak = 0; c.thr = 0;
+    c.cnt_nw = c.cnt_nwp = c.cnt_run = c.cnt_blown = c.cnt_cand = 0;
+    c.kmin = ~0ull; c.kmax = 0;
+    c.ev_count = c.mem_count = c.sample_count = 0;
+}
+
+int co_plan_snapshot(co_engine* E, const int64_t* cols, const int64_t* scal, int64_t* hdr, int32_t* lists,
+                     int64_t cap) {
+    if (!E || !cols || !scal || !hdr || !lists) return fail(CO_EINVAL, "null argument");
+    if (E->comm || E->d.dp.on) return fail(CO_EINVAL, "snapshot planning needs a plain engine (no data plane / NCCL)");
+    { int rw_ = begin_work(E); if (rw_) return rw_; }
+    const int32_t n = (int32_t)E->n;
+    int64_t* dcol = nullptr;
+    CK(cudaMalloc(&dcol, std::max<int64_t>(1, (int64_t)n * SNAP_COLS) * sizeof(int64_t)));
+    int r = CO_OK;
+    cudaError_t e = n ? cudaMemcpyAsync(dcol, cols, (size_t)n * SNAP_COLS * sizeof(int64_t), cudaMemcpyHostToDevice,
+                                        E->stream)
+                      : cudaSuccess;
+    if (e == cudaSuccess) {
+        k_load_snapshot<<<std::max(1, std::min(E->sms * 4, (n + 255) / 256)), 256, 0, E->stream>>>(E->d, dcol, n);
+        k_load_snapshot_ctl<<<1, 1, 0, E->stream>>>(E->d, scal[0], scal[1], (int32_t)scal[2], scal[3], scal[4],
+                                                    scal[5], scal[6], (int32_t)scal[7]);
+        k_classify<<<E->d.nblk, 256, 0, E->stream>>>(E->d, 0, 1);
+        k_serial<0><<<1, E->plan_threads, sizeof(PlanSh), E->stream>>>(E->d, (LogMirror*)nullptr, (int64_t*)nullptr,
+                                                                          0, 1);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(E->stream);
+    cudaFree(dcol);
+    if (e != cudaSuccess) return fail(CO_ECUDA, std::string("snapshot plan: ") + cudaGetErrorString(e));
+    if ((r = sync_ctl(E))) return r;
+    if ((r = check_device_error(E))) return r;
+    PlanHdr P;
+    CK(cudaMemcpy(&P, E->d.plan, sizeof(P), cudaMemcpyDeviceToHost));
+    hdr[0] = P.n_mem; hdr[1] = P.n_act; hdr[2] = P.n_pre; hdr[3] = P.n_cl; hdr[4] = P.n_def;
+    hdr[5] = P.overflow; hdr[6] = P.batch_tokens; hdr[7] = E->h_ctl->active;
+    const int64_t need = 2LL * P.n_mem + 6LL * P.n_act + 2LL * P.n_pre + 2LL * P.n_cl + P.n_def;
+    if (need > cap) return fail(CO_EINVAL, "plan buffer too small");
+    const Dev& d = E->d;
+    int32_t* w = lists;
+    auto get = [&](const int32_t* src, int32_t cnt) -> cudaError_t {
+        cudaError_t x = cnt ? cudaMemcpy(w, src, cnt * sizeof(int32_t), cudaMemcpyDeviceToHost) : cudaSuccess;
+        w += cnt;
+        return x;
+    };
+    for (auto x : {get(d.mem_idx, P.n_mem), get(d.mem_tok, P.n_mem), get(d.act_kind, P.n_act), get(d.act_idx, P.n_act),
+                   get(d.act_tok, P.n_act), get(d.act_nb, P.n_act), get(d.act_host, P.n_act),
+                   get(d.act_start, P.n_act), get(d.pre_idx, P.n_pre), get(d.pre_strat, P.n_pre),
+                   get(d.cl_w, P.n_cl), get(d.cl_p, P.n_cl), get(d.def_idx, P.n_def)})
+        if (x != cudaSuccess) return fail(CO_ECUDA, "plan readback");
+    touch(E);
+    return CO_OK;
+}
+
 int co_swap_io_stats(co_engine* E, int64_t* out) {
     if (!E || !out) return fail(CO_EINVAL, "null argument");
     if (!E->d.dp.on) return fail(CO_EINVAL, "data plane is off (kv_layers = 0)");

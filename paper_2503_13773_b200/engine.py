@@ -18,6 +18,7 @@ from typing import Dict, Iterator, List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _native as N
+from .build import hostlog_path
 from .config import DEVICE_POLICIES, EngineConfig
 from .core import (STATE_FROM_CODE, STRATEGY_FROM_CODE, US_PER_S, Direction, LengthEstimate,
                    Lifecycle, Request, RequestRuntime, Strategy)
@@ -26,6 +27,30 @@ from .hostprep import (bin_of, charge_luts, iteration_us, run_confidence, run_pa
                        sweet_spot)
 
 STRATEGY_CODE = {Strategy.SWAP: 0, Strategy.RECOMPUTE: 1}
+
+
+_hostlog = None
+
+
+def _load_hostlog():
+    global _hostlog
+    if _hostlog is not None:
+        return _hostlog
+    import importlib.machinery
+    import importlib.util
+    path = hostlog_path()
+    if not path.exists():
+        raise N.NativeError(f"{path.name} not built: run __graft_entry__.build()")
+    loader = importlib.machinery.ExtensionFileLoader("paper_2503_13773_b200._hostlog", str(path))
+    spec = importlib.util.spec_from_file_location("paper_2503_13773_b200._hostlog", str(path), loader=loader)
+    mod = importlib.util.module_from_spec(spec)
+    loader.exec_module(mod)
+    _hostlog = mod
+    return mod
+
+
+_STRATEGY_NAMES = tuple(STRATEGY_FROM_CODE[k].value for k in range(2))
+_CAUSE_NAMES = tuple(N.CAUSES)
 
 CAUSE_CODE = {"plan": 0, "squeeze": 1, "collision": 2}
 
@@ -661,30 +686,9 @@ class Engine:
 
     def _convert(self, n: int, mem: np.ndarray) -> List[dict]:
         """Device event records -> the reference's event dicts (engine.py:
-        353, 376-383, 407, 512-518, 533)."""
-        rid = self._rid
-        evs = self._evbuf
-        out = []
-        app = out.append
-        for k in range(n):
-            e = evs[k]
-            kind = e.kind
-            if kind == N.EV_ITER:
-                lo = 2 * e.c
-                it = iter(mem[lo:lo + 2 * e.idx].tolist())
-                app({"ev": "iter", "t": e.t, "end": e.a, "tokens": e.b, "members": [[rid[x], y] for x, y in zip(it, it)]})
-            elif kind == N.EV_ARRIVE:
-                app({"ev": "arrive", "t": e.t, "req": rid[e.idx]})
-            elif kind == N.EV_ADMIT:
-                app({"ev": "admit", "t": e.t, "req": rid[e.idx]})
-            elif kind == N.EV_PREEMPT:
-                app({"ev": "preempt", "t": e.t, "req": rid[e.idx],
-                     "strategy": STRATEGY_FROM_CODE[e.b].value, "kv": e.a, "cause": N.CAUSES[e.c]})
-            elif kind == N.EV_READMIT:
-                app({"ev": "readmit", "t": e.t, "req": rid[e.idx], "ready_at": e.a})
-            else:
-                app({"ev": "complete", "t": e.t, "req": rid[e.idx]})
-        return out
+        353, 376-383, 407, 512-518, 533), built by the _hostlog extension."""
+        return (_hostlog or _load_hostlog()).convert(C.addressof(self._evbuf), n, mem.ctypes.data, self._rid,
+                                                     _STRATEGY_NAMES, _CAUSE_NAMES)
 
     @property
     def events(self) -> List[dict]:

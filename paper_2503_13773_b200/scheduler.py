@@ -254,3 +254,142 @@ def order_victims(candidates: Iterable[VictimInfo], cfg: BucketConfig) -> List[V
         rows[k, 1:4] = (v.slo_tbt_us, v.remaining_tokens, v.occupancy_tokens)
     out = _run(SOP_ORDER_VICTIMS, rows, [cfg.token_step, len(edges)] + edges)
     return [vs[int(x)] for x in out[:len(vs)]]
+
+
+# -- the planner operator on a snapshot (scheduler.py:295-335, 939-950) -----------
+
+@dataclass
+class PlanAction:
+    kind: str
+    req_id: int
+    tokens: int = 0
+    blocks: int = 0
+    quote: Optional[object] = None  # kvc.EmbedQuote for "embed"
+
+
+@dataclass(frozen=True)
+class PlanMember:
+    req_id: int
+    tokens: int
+
+
+@dataclass
+class BatchPlan:
+    members: List[PlanMember]
+    batch_tokens: int = 0
+    preempt: List[Tuple[int, object]] = None
+    actions: List[PlanAction] = None
+    claims: List[Tuple[int, int]] = None
+    deferred: List[int] = None
+    overflow: bool = False
+
+
+@dataclass
+class PlannerInputs:
+    waiting: List[ReqView]
+    running: List[ReqView]
+    pool: object          # kvc.BlockPool (device) or the reference's BlockPool: queried read-only
+    t_i_max_us: int
+    iter_cost: object     # config.IterationCost
+    swap_model: object    # config.SwapModel
+    recompute_model: object
+
+
+_ACT = ("allocate", "grow", "reserve", "embed")
+_NOW = 1 << 40  # snapshot clock: every signed slack maps to positive device times
+
+
+def plan_batch(inp: PlannerInputs, cfg, device: Optional[int] = None) -> BatchPlan:
+    """scheduler.py:939-950 on the device: the snapshot's views and pool
+    records are loaded into an engine's request pool and ONE pass of the
+    device planner (k_classify + k_serial's plan_body, every policy of
+    POLICIES) produces the plan.  The engine gives its planner the live set
+    in arrival order (engine.py:321-323); the views are taken in that order."""
+    from .config import EngineConfig, TruthCosts
+    from .core import Request, Strategy
+    from .engine import Engine
+    from .kvc import EmbedQuote
+    pool = inp.pool
+    if pool.block_size != cfg.small_block_b:
+        raise ValueError("the pool's block size must be the scheduler's small_block_b (engine.py:236)")
+    views = sorted(list(inp.waiting) + list(inp.running), key=lambda v: (v.arrival_us, v.req_id))
+    n = len(views)
+    ids = [v.req_id for v in views]
+    if len(set(ids)) != n:
+        raise ValueError("duplicate request ids in the snapshot")
+    idx = {r: k for k, r in enumerate(ids)}
+    owners = list(pool.owners())
+    for o in owners:
+        if o not in idx:
+            raise ValueError(f"pool record {o} has no view in the snapshot")
+    reqs = []
+    cols = np.zeros((n, 20), dtype=np.int64)
+    code = {Lifecycle.WAITING: 1, Lifecycle.RUNNING: 2, Lifecycle.PREEMPTED: 3}
+    for k, v in enumerate(views):
+        if v.state not in code:
+            raise ValueError(f"view {v.req_id}: state {v.state} is not live")
+        if v.remaining_ttft_us is not None:       # no first token: rt = slo_ttft - (now - arrival)
+            slo_ttft, first, last = v.remaining_ttft_us + _NOW - v.arrival_us, -1, -1
+        else:
+            slo_ttft, first = v.slo_ttft_us, 0
+            last = v.remaining_tbt_us - v.slo_tbt_us + _NOW  # rt = slo_tbt - (now - last_token)
+        out_len = max(1, v.used + 2 - max(1, v.kv_need), v.generated + 1, v.predicted_total, v.estimated_total)
+        reqs.append(Request(id=v.req_id, arrival_us=v.arrival_us, prompt_len=max(1, v.kv_need),
+                            true_output_len=out_len, slo_ttft_us=slo_ttft, slo_tbt_us=v.slo_tbt_us))
+        cols[k, :12] = (code[v.state], v.generated, v.used, v.kv_need, v.prefill_done, v.preemption_count,
+                        v.predicted_total, v.estimated_total, first, last,
+                        v.slo_tbt_us + 1 if v.tbt_blown else 0, _NOW if v.ready else _NOW + 1)
+    cols[:, 14] = -1
+    cols[:, 17] = -1
+    cols[:, 18] = -1
+    fp = lambda t: -(-t // pool.block_size) * pool.block_size  # noqa: E731
+    fp_sum = g_sum = u_sum = 0
+    for seq, o in enumerate(owners, start=1):  # owners() is the records' creation order
+        k = idx[o]
+        g = pool.granted_of(o)
+        h = pool.host_of(o)
+        cols[k, 12:17] = (1, g, -1 if h is None else idx[h], pool.offset_of(o), pool.reserved_drawn_of(o))
+        cols[k, 19] = seq
+        gl = [idx[x] for x in pool.guests_of(o)]
+        if gl:
+            cols[k, 17] = gl[0]
+            for a, b in zip(gl, gl[1:]):
+                cols[a, 18] = b
+        g_sum += g
+        u_sum += pool.used_of(o)
+        if h is None:
+            fp_sum += fp(g)
+        if pool.used_of(o) != views[k].used:
+            raise ValueError(f"request {o}: pool used {pool.used_of(o)} != view used {views[k].used}")
+    ecfg = EngineConfig(capacity_tokens=pool.capacity, reserved_blocks=pool.reserved_target,
+                        allow_stacking=bool(getattr(pool, "allow_stacking", False)), sched=cfg,
+                        iter_cost=inp.iter_cost, truth=TruthCosts(inp.swap_model, inp.recompute_model),
+                        record_events=False)
+    eng = Engine(reqs, ecfg, device=_DEVICE if device is None else device)
+    try:
+        if eng._rid != ids:
+            raise AssertionError("engine order differs from the snapshot order")
+        scal = np.array([_NOW, inp.t_i_max_us, pool.reserved_blocks_current, fp_sum, g_sum, u_sum, len(owners), n],
+                        dtype=np.int64)
+        hdr = np.zeros(8, dtype=np.int64)
+        cap = 12 * n + 64
+        lists = np.zeros(cap, dtype=np.int32)
+        p64 = lambda a: a.ctypes.data_as(C.POINTER(C.c_int64))  # noqa: E731
+        N.check(eng._lib.co_plan_snapshot(eng._h, p64(np.ascontiguousarray(cols)), p64(scal), p64(hdr),
+                                          lists.ctypes.data_as(C.POINTER(C.c_int32)), cap), "co_plan_snapshot")
+    finally:
+        eng.close()
+    nm, na, npre, ncl, nd = (int(x) for x in hdr[:5])
+    it = iter(np.split(lists, np.cumsum([nm, nm, na, na, na, na, na, na, npre, npre, ncl, ncl, nd]))[:13])
+    mi, mt, ak, ai, at, anb, ah, ast, pi, ps, cw, cp, di = (a.tolist() for a in it)
+    plan = BatchPlan(members=[PlanMember(ids[i], t) for i, t in zip(mi, mt)], batch_tokens=int(hdr[6]),
+                     preempt=[(ids[i], Strategy.SWAP if s == 0 else Strategy.RECOMPUTE) for i, s in zip(pi, ps)],
+                     actions=[], claims=[(ids[w], ids[p]) for w, p in zip(cw, cp)], deferred=[ids[i] for i in di],
+                     overflow=bool(hdr[5]))
+    for kind, i, tok, nb, h, start in zip(ak, ai, at, anb, ah, ast):
+        quote = None
+        if _ACT[kind] == "embed":
+            out = tok - views[i].kv_need  # need = kv_need + out (scheduler.py:438-441)
+            quote = EmbedQuote(host=ids[h], start_offset=start, feasible_slack=start - views[h].used - out)
+        plan.actions.append(PlanAction(_ACT[kind], ids[i], tokens=tok, blocks=nb, quote=quote))
+    return plan
