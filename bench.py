@@ -40,6 +40,9 @@ STAGE_KERNEL = {"plan": "k_serial", "apply": "k_serial", "plan+apply": "k_serial
                 "begin+admit": "k_begin", "decode": "k_decode_tc05", "data": "k_data"}
 
 
+E2E_REPS = 3
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -584,8 +587,14 @@ def device_arm(args, rank, world, dist):
         e.close()
         return el, dec, d2h, nev
 
-    e2e_s, e2e_dec, d2h, e2e_nev = e2e_run(True)
-    e2e_s_nd, e2e_dec_nd, _, _ = e2e_run(False)
+    # the window is only K steps of ~70 us of host wall clock each: three
+    # fresh repetitions per variant, the median one reported
+    def median_run(drain):
+        runs = sorted((e2e_run(drain) for _ in range(E2E_REPS)), key=lambda r: r[0] / max(r[1], 1))
+        return runs[len(runs) // 2]
+
+    e2e_s, e2e_dec, d2h, e2e_nev = median_run(True)
+    e2e_s_nd, e2e_dec_nd, _, _ = median_run(False)
     if dist:
         t = torch.tensor([dev_ms, e2e_s * 1e3, e2e_s_nd * 1e3], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -667,8 +676,9 @@ def device_arm(args, rank, world, dist):
                 "how": "Engine.step_result() per step through the public API (control block + the iteration's "
                        "members read back every step) AND the step's event log materialised as host dicts "
                        "(Engine.events) every step, on the same window as the device timing (steps "
-                       f"{WINDOW_START}..{WINDOW_START + args.steps - 1}) of a fresh instance; trace uploaded once "
-                       "at construction (no per-step inputs: no arrivals in the window)",
+                       f"{WINDOW_START}..{WINDOW_START + args.steps - 1}) of a fresh instance, median of "
+                       f"{E2E_REPS} repetitions; trace uploaded once at construction (no per-step inputs: no "
+                       "arrivals in the window)",
                 "without_event_drain": e2e_dec_nd / (e2e_ms_nd * 1e-3)},
         "gpu_launches": args.steps * kernels_per_step,
         "gpu_launches_note": f"{kernels_per_step} own kernels per step (k_begin, k_classify with admission, "

@@ -158,7 +158,7 @@ def load() -> C.CDLL:
         "co_swap_io_stats": (C.c_int, [V, I64P]),
         "co_plan_snapshot": (C.c_int, [V, I64P, I64P, I64P, I32P, C.c_int64]),
         "co_pool_read_tables": (C.c_int, [V, I32P, I32P, C.c_int64, I32P, I32P]),
-        "co_drain_log": (C.c_int, [V, C.POINTER(CoEvent), C.c_int64, I32P, C.c_int64, I64P, C.c_int64, I64P]),
+        "co_drain_log": (C.c_int, [V, V, C.c_int64, V, C.c_int64, V, C.c_int64, V]),
         "co_drain_samples": (C.c_int, [V, I64P, C.c_int64, I64P]),
         "co_read_token_times": (C.c_int, [V, I64P, I64P]),
         "co_check_invariants": (C.c_int, [V]),

@@ -420,8 +420,7 @@ class Engine:
         self._evbuf = self._membuf = self._sbuf = None
         self._drain_args = None
         self._rid_np = np.array(self._rid, dtype=np.int64)
-        self._pend = np.zeros(3, dtype=np.int64)
-        self._pend_p = _ptr(self._pend, C.c_int64)
+        self._cnt = (C.c_int64 * 3)()
 
     # -- lifecycle -----------------------------------------------------------
 
@@ -660,35 +659,36 @@ class Engine:
         """Move the device append log (events, iteration members, utilization
         samples) into the host lists in one library call.  After a step() the
         library serves it from the step graph's pinned mirror, so this is
-        host-only work."""
-        cnt = self._pend
+        host-only work (ctypes buffers: no numpy per call)."""
+        cnt = self._cnt
         while True:
             if self._evbuf is None:
                 ne, nm, ns = (max(1024, int(x)) for x in cnt)
+                nm = max(nm, 16384)
                 self._evbuf = (N.CoEvent * ne)()
-                self._membuf = np.empty(2 * max(nm, 16384), dtype=np.int32)
-                self._sbuf = np.empty(2 * ns, dtype=np.int64)
-                self._drain_args = (self._h, self._evbuf, len(self._evbuf), _ptr(self._membuf, C.c_int32),
-                                    len(self._membuf) // 2, _ptr(self._sbuf, C.c_int64), len(self._sbuf) // 2,
-                                    self._pend_p)
+                self._membuf = (C.c_int32 * (2 * nm))()
+                self._sbuf = (C.c_int64 * (2 * ns))()
+                self._drain_args = (self._h, self._evbuf, ne, self._membuf, nm, self._sbuf, ns, self._cnt)
+                self._mem_addr = C.addressof(self._membuf)
+                self._ev_addr = C.addressof(self._evbuf)
             rc = self._lib.co_drain_log(*self._drain_args)
             if rc != N.CO_EAGAIN:
                 break
             self._evbuf = None  # grow to the sizes returned in cnt and retry
         N.check(rc, "co_drain_log")
-        ne, ns = int(cnt[0]), int(cnt[2])
+        ne, ns = cnt[0], cnt[2]
         if ne:
-            self._events.extend(self._convert(ne, self._membuf))
+            self._events.extend(self._convert(ne, None))
         if ns:
-            it = iter(self._sbuf[:2 * ns].tolist())
+            it = iter(self._sbuf[:2 * ns])
             self._samples.extend(zip(it, it))
         self._sc = None
 
     def _convert(self, n: int, mem: np.ndarray) -> List[dict]:
         """Device event records -> the reference's event dicts (engine.py:
         353, 376-383, 407, 512-518, 533), built by the _hostlog extension."""
-        return (_hostlog or _load_hostlog()).convert(C.addressof(self._evbuf), n, mem.ctypes.data, self._rid,
-                                                     _STRATEGY_NAMES, _CAUSE_NAMES)
+        return (_hostlog or _load_hostlog()).convert(self._ev_addr, n, self._mem_addr, self._rid, _STRATEGY_NAMES,
+                                                     _CAUSE_NAMES)
 
     @property
     def events(self) -> List[dict]:
