@@ -12,6 +12,7 @@
 // done or paused (an append buffer needs draining), so no host round trip is
 // needed inside a launch.
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 #include <dlfcn.h>
 
 #include <algorithm>
@@ -72,6 +73,15 @@ static NcclApi& nccl() {
     }();
     return api;
 }
+
+// NVTX ranges around the C-ABI entry points (header-only nvtx3: a no-op
+// unless a profiler is attached), so an nsys/ncu timeline shows which host
+// call issued which kernels
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+#define CO_RANGE(name) NvtxRange nvtx_range_(name)
 
 static int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -495,6 +505,7 @@ int co_destroy(co_engine* E) {
 }
 
 int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int device, co_engine** out) {
+    CO_RANGE("co_create");
     if (!cfg || !tr || !lu || !out) return fail(CO_EINVAL, "null argument");
     *out = nullptr;
     if (cfg->block_size < 1 || cfg->buffer_b < 0 || cfg->token_budget < 1 || cfg->preallocate_m < 0 ||
@@ -947,6 +958,7 @@ int co_prepare_step(co_engine* E) {
 
 int co_step_result(co_engine* E, int32_t* result, int32_t* members, int64_t max_members, int64_t* n_members,
                    int64_t* iter_end_us) {
+    CO_RANGE("co_step_result");
     if (!E || !result || !n_members) return fail(CO_EINVAL, "null argument");
     int r;
     if ((r = ensure_result_buffer(E))) return r;
@@ -973,6 +985,7 @@ int co_step_result(co_engine* E, int32_t* result, int32_t* members, int64_t max_
 }
 
 int co_step(co_engine* E, int32_t* result) {
+    CO_RANGE("co_step");
     if (!E || !result) return fail(CO_EINVAL, "null argument");
     int r = ensure_step_graph(E);
     if (r) return r;
@@ -992,6 +1005,7 @@ int co_step(co_engine* E, int32_t* result) {
 }
 
 int co_run(co_engine* E, int64_t max_steps, int32_t K, int64_t* steps_done) {
+    CO_RANGE("co_run");
     if (!E) return fail(CO_EINVAL, "null argument");
     { int rw_ = begin_work(E); if (rw_) return rw_; }
     if (E->comm && max_steps <= 0)
@@ -1054,6 +1068,7 @@ int co_run(co_engine* E, int64_t max_steps, int32_t K, int64_t* steps_done) {
 }
 
 int co_preempt(co_engine* E, int64_t idx, int32_t strategy, int64_t now_us, int32_t cause) {
+    CO_RANGE("co_preempt");
     if (!E || idx < 0 || idx >= E->n) return fail(CO_EINVAL, "bad request index");
     { int rw_ = begin_work(E); if (rw_) return rw_; }
     k_preempt_one<<<1, 1, 0, E->stream>>>(E->d, (int32_t)idx, strategy, now_us, cause);
@@ -1133,6 +1148,7 @@ int co_pending_events(co_engine* E, int64_t* ne, int64_t* nm) {
 
 int co_drain_log(co_engine* E, co_event* events, int64_t max_events, int32_t* members, int64_t max_members,
                  int64_t* samples, int64_t max_samples, int64_t* counts) {
+    CO_RANGE("co_drain_log");
     if (!E || !counts) return fail(CO_EINVAL, "null argument");
     int r = drain_device(E);
     if (r) return r;
@@ -1198,6 +1214,7 @@ int co_read_token_times(co_engine* E, int64_t* offsets, int64_t* times) {
 }
 
 int co_metrics(co_engine* E, co_metrics_raw* out) {
+    CO_RANGE("co_metrics");
     if (!E || !out) return fail(CO_EINVAL, "null argument");
     { int rw_ = begin_work(E); if (rw_) return rw_; }
     const int64_t n = E->n, ntok = std::max<int64_t>(E->tok_total, 1);
@@ -1293,6 +1310,7 @@ int co_last_device_ms(co_engine* E, double* ms) {
 }
 
 int co_time_steps(co_engine* E, int32_t k, int64_t flush_bytes, double* step_ms, double* stage_ms) {
+    CO_RANGE("co_time_steps");
     if (!E || k < 1) return fail(CO_EINVAL, "bad arguments");
     { int rw_ = begin_work(E); if (rw_) return rw_; }
     const int NE = CO_NSTAGES + 1;
@@ -1351,6 +1369,7 @@ int co_time_steps(co_engine* E, int32_t k, int64_t flush_bytes, double* step_ms,
 
 int co_read_block_tables(co_engine* E, int32_t* lens, int32_t* pages, int64_t max_pages, int32_t* free_pages,
                          int32_t* n_free) {
+    CO_RANGE("co_read_block_tables");
     if (!E || !lens || !n_free) return fail(CO_EINVAL, "null argument");
     int r = sync_ctl(E);
     if (r) return r;
@@ -1422,6 +1441,7 @@ __global__ void k_load_snapshot_ctl(Dev d, int64_t now, int64_t ti, int32_t rsv,
 
 int co_plan_snapshot(co_engine* E, const int64_t* cols, const int64_t* scal, int64_t* hdr, int32_t* lists,
                      int64_t cap) {
+    CO_RANGE("co_plan_snapshot");
     if (!E || !cols || !scal || !hdr || !lists) return fail(CO_EINVAL, "null argument");
     if (E->comm || E->d.dp.on) return fail(CO_EINVAL, "snapshot planning needs a plain engine (no data plane / NCCL)");
     { int rw_ = begin_work(E); if (rw_) return rw_; }
@@ -1481,6 +1501,7 @@ int co_swap_io_stats(co_engine* E, int64_t* out) {
 }
 
 int co_kv_verify(co_engine* E, int64_t* bad, int64_t* checked) {
+    CO_RANGE("co_kv_verify");
     if (!E || !bad || !checked) return fail(CO_EINVAL, "null argument");
     { int rw_ = begin_work(E); if (rw_) return rw_; }
     if (!E->d.dp.on) return fail(CO_EINVAL, "data plane is off (kv_layers = 0)");
@@ -1570,6 +1591,7 @@ int co_set_decode(co_engine* E, int32_t on) {
 // kernel the engine runs, on the first pages of the pool.  Clobbers KV
 // contents: use a dedicated instance.
 int co_swap_bench(co_engine* E, int64_t ntok, int32_t iters, double* out_ms, double* in_ms) {
+    CO_RANGE("co_swap_bench");
     if (!E || !out_ms || !in_ms || iters < 1) return fail(CO_EINVAL, "bad arguments");
     { int rw_ = begin_work(E); if (rw_) return rw_; }
     DataCfg& x = E->d.dp;
@@ -1822,6 +1844,7 @@ int co_gen_std(int32_t kind, uint64_t seed, uint64_t stream, int64_t n, int devi
 
 int co_gen_trace(const co_trace_spec* sp, uint64_t seed, int device, int64_t* arrival_us, int32_t* prompt_len,
                  int32_t* output_len) {
+    CO_RANGE("co_gen_trace");
     if (!sp || sp->n < 0 || sp->n > (1ll << 30)) return fail(CO_EINVAL, "bad trace spec");
     const int64_t n = sp->n;
     if (n && (!arrival_us || !prompt_len || !output_len)) return fail(CO_EINVAL, "null output");
@@ -1854,6 +1877,7 @@ int co_gen_trace(const co_trace_spec* sp, uint64_t seed, int device, int64_t* ar
 
 int co_gen_slos(int64_t n, const int32_t* prompt_len, const co_slo_spec* sp, uint64_t seed, int device,
                 int64_t* slo_ttft_us, int64_t* slo_tbt_us) {
+    CO_RANGE("co_gen_slos");
     if (!sp || n < 0 || (n && (!prompt_len || !slo_ttft_us || !slo_tbt_us))) return fail(CO_EINVAL, "bad arguments");
     if (sp->base_ttft_us <= 0 || sp->base_tbt_us <= 0) return fail(CO_EINVAL, "baselines must be > 0");
     if (!(0 < sp->scale_lo && sp->scale_lo <= sp->scale_hi) || sp->chunk_budget < 1)
@@ -1878,6 +1902,7 @@ int co_gen_slos(int64_t n, const int32_t* prompt_len, const co_slo_spec* sp, uin
 
 int co_gen_predictor(int64_t n, const co_predictor_spec* sp, uint64_t seed, int device, int32_t* err,
                      uint8_t* flip) {
+    CO_RANGE("co_gen_predictor");
     if (!sp || n < 0 || (n && (!err || !flip))) return fail(CO_EINVAL, "bad arguments");
     if (sp->error_dist < CO_ERR_ZERO || sp->error_dist > CO_ERR_NORMAL || !(sp->error_scale >= 0) ||
         !(sp->direction_accuracy >= 0.0 && sp->direction_accuracy <= 1.0))

@@ -168,6 +168,13 @@ __global__ void __launch_bounds__(256) k_classify(Dev d, int32_t guard, int32_t 
     __shared__ int32_t tot_s[2];
     __shared__ BeginR br;
     const Ctl& c = *d.ctl;
+    // this thread's first slot: its state and waiting key are loaded before
+    // the begin's control-block round trip, so the two overlap (admitted
+    // slots are rewritten below and take admit_one's values instead)
+    const int32_t i0 = blockIdx.x * d.chunk + (int32_t)threadIdx.x;
+    int8_t s_pre = ST_PENDING;
+    uint64_t k_pre = 0;
+    if (i0 < d.n) { s_pre = d.state[i0]; k_pre = d.key0[i0]; }
     if (threadIdx.x == 0) br = begin_eval(d, c, guard, reset);  // the step's begin, read-only
     __syncthreads();
     if (!br.active) return;
@@ -184,12 +191,22 @@ __global__ void __launch_bounds__(256) k_classify(Dev d, int32_t guard, int32_t 
         const int32_t i = c0 + (int32_t)threadIdx.x;
         int32_t is_run = 0, is_blown = 0, is_cand = 0;
         if (i < hi) {
-            if (i >= alo && i < ahi) admit_one(d, i, alo, ev0);
+            int8_t s;
+            uint64_t k;
+            if (i >= alo && i < ahi) {
+                admit_one(d, i, alo, ev0);
+                s = ST_WAITING;
+                k = d.key0[i];
+            } else if (c0 == lo) {
+                s = s_pre;
+                k = k_pre;
+            } else {
+                s = d.state[i];
+                k = d.key0[i];
+            }
             if (i < hi_live) {
-                const int8_t s = d.state[i];
                 bool view = false;
                 if (s == ST_WAITING || s == ST_PREEMPTED) {
-                    const uint64_t k = d.key0[i];
                     const int32_t wc = wait_class(d, s, k, now, ti, eps);
                     if (wc == WC_CRIT) {
                         d.crit_idx[atomicAdd(&d.ctl->cnt_nw, 1)] = i;
