@@ -299,6 +299,16 @@ __device__ __forceinline__ PV make_pv(const Dev& d, int32_t i, int64_t now) {
     v.gain = (d.holds[i] && d.host[i] < 0) ? gain_of(d, i) : 0;
     return v;
 }
+// L1 prefetch of the fields make_pv reads (k_classify issues it for a slot
+// it already knows needs a view, ahead of the step's begin round trip)
+__device__ __forceinline__ void pv_prefetch(const Dev& d, int32_t i) {
+#define CO_PF(ptr) asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr))
+    CO_PF(d.granted + i); CO_PF(d.used + i); CO_PF(d.holds + i); CO_PF(d.host + i); CO_PF(d.guest + i);
+    CO_PF(d.kv_need + i); CO_PF(d.prefill + i); CO_PF(d.est + i); CO_PF(d.gen + i); CO_PF(d.pred + i);
+    CO_PF(d.pcount + i); CO_PF(d.idrank + i); CO_PF(d.ready_at + i); CO_PF(d.first_tok + i);
+    CO_PF(d.last_tok + i); CO_PF(d.slo_tbt + i); CO_PF(d.rsv + i);
+#undef CO_PF
+}
 // the step's snapshot view, written by k_classify for every live request
 __device__ __forceinline__ PV view_of(const Dev& d, int32_t i) {
     const uint4* src = reinterpret_cast<const uint4*>(d.views + i);

@@ -176,6 +176,7 @@ __global__ void __launch_bounds__(256) k_classify(Dev d, int32_t guard, int32_t 
     uint64_t k_pre = 0;
     if (i0 < d.n) { s_pre = d.state[i0]; k_pre = d.key0[i0]; }
     if (threadIdx.x == 0) br = begin_eval(d, c, guard, reset);  // the step's begin, read-only
+    else if (i0 < d.n && s_pre == ST_RUNNING) pv_prefetch(d, i0);  // a running slot always gets a view
     __syncthreads();
     if (!br.active) return;
     const int64_t now = br.now, ti = c.t_i, eps = d.eps;
