@@ -174,9 +174,14 @@ __global__ void __launch_bounds__(256) k_classify(Dev d, int32_t guard, int32_t 
     const int32_t i0 = blockIdx.x * d.chunk + (int32_t)threadIdx.x;
     int8_t s_pre = ST_PENDING;
     uint64_t k_pre = 0;
+    const uint64_t thr_pre = c.thr;  // (not changed by the begin)
     if (i0 < d.n) { s_pre = d.state[i0]; k_pre = d.key0[i0]; }
-    if (threadIdx.x == 0) br = begin_eval(d, c, guard, reset);  // the step's begin, read-only
-    else if (i0 < d.n && s_pre == ST_RUNNING) pv_prefetch(d, i0);  // a running slot always gets a view
+    if (threadIdx.x == 0) {
+        br = begin_eval(d, c, guard, reset);  // the step's begin, read-only
+    } else if (i0 < d.n && (s_pre == ST_RUNNING ||
+                            ((s_pre == ST_WAITING || s_pre == ST_PREEMPTED) && k_pre < thr_pre))) {
+        pv_prefetch(d, i0);  // running slots and the N'_w head always get a view
+    }
     __syncthreads();
     if (!br.active) return;
     const int64_t now = br.now, ti = c.t_i, eps = d.eps;
