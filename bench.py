@@ -41,6 +41,27 @@ STAGE_KERNEL = {"plan": "k_serial", "apply": "k_serial", "plan+apply": "k_serial
 
 
 E2E_REPS = 3
+_RESULT_FD = None  # the real stdout while native libraries' banners are routed to stderr
+
+
+def emit(line: dict) -> None:
+    """The ONE JSON line on stdout (NCCL and driver banners go to stderr)."""
+    data = (json.dumps(line) + "\n").encode()
+    if _RESULT_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_RESULT_FD, data)
+
+
+def route_native_stdout_to_stderr() -> None:
+    """fd 1 -> fd 2 for everything native code prints (NCCL prints its version
+    banner on stdout at communicator init); the result goes to the saved fd."""
+    global _RESULT_FD
+    if _RESULT_FD is None:
+        sys.stdout.flush()
+        _RESULT_FD = os.dup(1)
+        os.dup2(2, 1)
 
 
 def load_peaks():
@@ -273,7 +294,7 @@ def reference_arm(args, rank, world):
                          "host_cpu": cpu},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    emit(line)
 
 
 def workload_config(world):
@@ -687,7 +708,7 @@ def device_arm(args, rank, world, dist):
         "collective": coll,
         **extra,
     }
-    print(json.dumps(line))
+    emit(line)
 
 
 def main():
@@ -702,6 +723,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     dist = None
+    route_native_stdout_to_stderr()
     if args.impl == "reference":
         reference_arm(args, rank, world)
         return
