@@ -489,11 +489,9 @@ class Engine:
         if rc:
             N.check(rc, "co_step_result")
         k = n.value
-        out = np.empty((k, 2), dtype=np.int64)
+        out = self._resbuf[:2 * k].reshape(k, 2).astype(np.int64)
         if k:
-            m = self._resbuf[:2 * k]
-            out[:, 0] = self._rid_np[m[0::2]]
-            out[:, 1] = m[1::2]
+            out[:, 0] = self._rid_np[out[:, 0]]
         return bool(r.value), out, int(end.value)
 
     def run_steps(self, max_steps: int = 0, steps_per_launch: Optional[int] = None) -> int:
