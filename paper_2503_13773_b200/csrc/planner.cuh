@@ -44,6 +44,7 @@ struct PlanSh {
     // every keyed item with key < lo_key (then the blown tail)
     uint64_t lo_key;
     int32_t cand_done, xcnt, xbest;
+    int32_t any_flags;  // over the running views: 1 returned, 2 proactive candidate, 4 top-up candidate
     int32_t xh[XNB];
 };
 
@@ -607,6 +608,7 @@ __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
         S.rsvb = c.rsv_cur;
         S.n_mem = S.n_act = S.n_pre = S.n_cl = S.n_def = S.n_gm = S.n_pend = S.n_mready = S.n_part = 0;
         S.batch_now = 0; S.gm_tokens = 0; S.overflow = 0; S.sated = 0;
+        S.any_flags = 0;
     }
     __syncthreads();
 
@@ -678,9 +680,25 @@ __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
     };
 
     const bool rcached = n_run <= RV_CAP;
-    if (rcached)
-        for (int32_t k = tid; k < n_run; k += (int)blockDim.x) S.rv[k] = view_of(d, RUN[k]);
+    // which later phases can have members at all (supersets of their
+    // predicates, from the staged views): the empty ones are skipped whole
+    const int64_t mpre = d.prealloc_m;
+    int fl = 0;
+    if (rcached) {
+        for (int32_t k = tid; k < n_run; k += (int)blockDim.x) {
+            const PV v = view_of(d, RUN[k]);
+            S.rv[k] = v;
+            const bool ret = (v.flags & PV_RETURNED) != 0;
+            fl |= (ret ? 1 : 0) | ((!ret && v.eff < v.target && v.er <= mpre) ? 2 : 0) |
+                  ((!ret && !(v.flags & PV_GUEST) && (v.flags & PV_READY) && v.pre >= v.kvn &&
+                    (int64_t)v.eff - v.used <= mpre) ? 4 : 0);
+        }
+        fl = (int)__reduce_or_sync(0xffffffffu, (unsigned)fl);
+        if ((tid & 31) == 0 && fl) atomicOr(&S.any_flags, fl);
+    }
     __syncthreads();
+    fl = rcached ? S.any_flags : 7;
+    const bool any_ret = (fl & 1) != 0;
     auto RV = [&](int32_t k) -> PV { return rcached ? S.rv[k] : view_of(d, RUN[k]); };
 
     if (d.policy != CO_POLICY_CACHEOPT) {
@@ -690,22 +708,25 @@ __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
 
     // ---- returned running (scheduler.py:142-150, 161-162) ------------------
     auto crit_rt = [&](int64_t r) { return r >= -eps && r - ti < eps; };
-    const int32_t n_nr = blk_compact_at(RUN, n_run, d.l_nr, [&](int32_t k, int32_t i) {
-        const PV v = RV(k);
-        return (v.flags & PV_READY) && (v.flags & PV_RETURNED) && crit_rt(v.rt);
-    }, S.b);
-    const int32_t n_nrp = blk_compact_at(RUN, n_run, d.l_nrp, [&](int32_t k, int32_t i) {
-        const PV v = RV(k);
-        return (v.flags & PV_READY) && (v.flags & PV_RETURNED) && !crit_rt(v.rt);
-    }, S.b);
-    blk_sort(d.l_nr, n_nr, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
-        k0 = (uint64_t)(rt_of(d, i, now) + (1ll << 62)); k1 = (uint64_t)d.idrank[i]; k2 = 0;
-    }, d, S.b);
-    blk_sort(d.l_nrp, n_nrp, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
-        int64_t r = rt_of(d, i, now);
-        k0 = r < 0 ? 1 : 0; k1 = r < 0 ? (uint64_t)d.arr[i] : (uint64_t)r; k2 = (uint64_t)d.idrank[i];
-    }, d, S.b);
-    for (int32_t k = tid; k < n_nr; k += (int)blockDim.x) d.st_nr[d.l_nr[k]] = sid;
+    int32_t n_nr = 0, n_nrp = 0;
+    if (any_ret) {
+        n_nr = blk_compact_at(RUN, n_run, d.l_nr, [&](int32_t k, int32_t i) {
+            const PV v = RV(k);
+            return (v.flags & PV_READY) && (v.flags & PV_RETURNED) && crit_rt(v.rt);
+        }, S.b);
+        n_nrp = blk_compact_at(RUN, n_run, d.l_nrp, [&](int32_t k, int32_t i) {
+            const PV v = RV(k);
+            return (v.flags & PV_READY) && (v.flags & PV_RETURNED) && !crit_rt(v.rt);
+        }, S.b);
+        blk_sort(d.l_nr, n_nr, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
+            k0 = (uint64_t)(rt_of(d, i, now) + (1ll << 62)); k1 = (uint64_t)d.idrank[i]; k2 = 0;
+        }, d, S.b);
+        blk_sort(d.l_nrp, n_nrp, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
+            int64_t r = rt_of(d, i, now);
+            k0 = r < 0 ? 1 : 0; k1 = r < 0 ? (uint64_t)d.arr[i] : (uint64_t)r; k2 = (uint64_t)d.idrank[i];
+        }, d, S.b);
+        for (int32_t k = tid; k < n_nr; k += (int)blockDim.x) d.st_nr[d.l_nr[k]] = sid;
+    }
 
     prof_mark(d, 1);
     // ---- embedding hosts (scheduler.py:425-430) sorted by (a_j - u_j, id) --
@@ -751,16 +772,18 @@ __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
     prof_mark(d, 3);
     // ---- exact-consumption demand and reserve (scheduler.py:459-472) ------
     int64_t dem = 0;
-    for (int32_t k = tid; k < n_pend0; k += (int)blockDim.x) {
-        const PV v = view_of(d, d.l_pend[k]);
-        int64_t need = (int64_t)v.kvn + B - v.eff;
-        dem += pv_cost(v, need > 0 ? need : 0, bs);
+    if (n_pend0 + n_nr > 0) {  // (block-uniform; nothing to sum in a step without critical requests)
+        for (int32_t k = tid; k < n_pend0; k += (int)blockDim.x) {
+            const PV v = view_of(d, d.l_pend[k]);
+            int64_t need = (int64_t)v.kvn + B - v.eff;
+            dem += pv_cost(v, need > 0 ? need : 0, bs);
+        }
+        for (int32_t k = tid; k < n_nr; k += (int)blockDim.x) {
+            const PV v = view_of(d, d.l_nr[k]);
+            if (!(v.flags & PV_GUEST)) dem += pv_cost(v, B, bs);
+        }
+        dem = blk_sum(dem, S.b);
     }
-    for (int32_t k = tid; k < n_nr; k += (int)blockDim.x) {
-        const PV v = view_of(d, d.l_nr[k]);
-        if (!(v.flags & PV_GUEST)) dem += pv_cost(v, B, bs);
-    }
-    dem = blk_sum(dem, S.b);
     if (tid == 0) {
         int64_t sf = dem - S.free;
         if (sf < 0) sf = 0;
@@ -1001,27 +1024,28 @@ __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
     __syncthreads();
     prof_mark(d, 9);
     // proactive_include (scheduler.py:269-279) over the post-eviction running set
-    const int64_t mpre = d.prealloc_m;
-    const int32_t n_pro = blk_compact_at(RUN, n_run, d.l_pro, [&](int32_t k, int32_t i) {
-        const PV v = RV(k);
-        return d.st_removed[i] != sid && !(v.flags & PV_RETURNED) && v.eff < v.target && v.er <= mpre;
-    }, S.b);
-    blk_sort(d.l_pro, n_pro, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
-        const PV v = view_of(d, i);
-        k0 = (uint64_t)v.er; k1 = (uint64_t)v.idrank; k2 = 0;
-    }, d, S.b);
-    if (tid == 0) {
-        for (int32_t k = 0; k < n_pro; k++) {
-            int32_t i = d.l_pro[k];
-            if (guest_of(d, i) || d.st_parts[i] == sid) continue;
-            d.l_part[S.n_part] = i; d.l_part_need[S.n_part] = target_of(d, i) - eff_of(d, i); S.n_part++;
-            d.st_parts[i] = sid;
+    if (fl & 2) {
+        const int32_t n_pro = blk_compact_at(RUN, n_run, d.l_pro, [&](int32_t k, int32_t i) {
+            const PV v = RV(k);
+            return d.st_removed[i] != sid && !(v.flags & PV_RETURNED) && v.eff < v.target && v.er <= mpre;
+        }, S.b);
+        blk_sort(d.l_pro, n_pro, [&](int32_t i, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
+            const PV v = view_of(d, i);
+            k0 = (uint64_t)v.er; k1 = (uint64_t)v.idrank; k2 = 0;
+        }, d, S.b);
+        if (tid == 0) {
+            for (int32_t k = 0; k < n_pro; k++) {
+                int32_t i = d.l_pro[k];
+                if (guest_of(d, i) || d.st_parts[i] == sid) continue;
+                d.l_part[S.n_part] = i; d.l_part_need[S.n_part] = target_of(d, i) - eff_of(d, i); S.n_part++;
+                d.st_parts[i] = sid;
+            }
         }
+        __syncthreads();
     }
-    __syncthreads();
     prof_mark(d, 10);
     // pre-exhaust top-up, running order (scheduler.py:625-638)
-    {
+    if (fl & 4) {
         const int32_t base = S.n_part;
         const int32_t n_top = blk_compact_at(RUN, n_run, d.l_part + base, [&](int32_t k, int32_t i) {
             const PV v = RV(k);
