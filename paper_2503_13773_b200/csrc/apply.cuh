@@ -374,15 +374,18 @@ __device__ __forceinline__ void apply_body(const Dev& d, ApplySh& S) {
 
     prof_mark(d, 36);
     // ---- collisions (engine.py:573-591), hosts in record-creation order ----
-    const int32_t n_coll = blk_compact(RUN, n_run, d.l_coll, [&](int32_t h) {
-        if (d.state[h] != ST_RUNNING || !d.holds[h] || d.host[h] >= 0) return false;
-        for (int32_t g = d.guest[h]; g >= 0; g = d.gnext[g])
-            if (d.used[h] >= d.off[g]) return true;
-        return false;
-    }, S.b);
-    blk_sort(d.l_coll, n_coll, [&](int32_t h, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
-        k0 = (uint64_t)d.rec_seq[h]; k1 = 0; k2 = 0;
-    }, d, S.b);
+    int32_t n_coll = 0;
+    if (c.n_guests > 0) {  // (no guest record: nothing can collide)
+        n_coll = blk_compact(RUN, n_run, d.l_coll, [&](int32_t h) {
+            if (d.state[h] != ST_RUNNING || !d.holds[h] || d.host[h] >= 0) return false;
+            for (int32_t g = d.guest[h]; g >= 0; g = d.gnext[g])
+                if (d.used[h] >= d.off[g]) return true;
+            return false;
+        }, S.b);
+        blk_sort(d.l_coll, n_coll, [&](int32_t h, uint64_t& k0, uint64_t& k1, uint64_t& k2) {
+            k0 = (uint64_t)d.rec_seq[h]; k1 = 0; k2 = 0;
+        }, d, S.b);
+    }
     if (tid == 0) {
         for (int32_t k = 0; k < n_coll; k++) {
             int32_t h = d.l_coll[k];

@@ -55,6 +55,7 @@ struct Ctl {
     int32_t chunk_top;                                // N1: free table chunks
     int32_t err_info[4];
     uint64_t mir_seq;                                 // step mirrors written (mapped completion flag)
+    int32_t n_guests;                                 // live guest records (apply skips collisions at 0)
 };
 
 // The plan of one step (scheduler.py:295-323 BatchPlan) as device lists.

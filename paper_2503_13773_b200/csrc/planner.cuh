@@ -45,6 +45,7 @@ struct PlanSh {
     uint64_t lo_key;
     int32_t cand_done, xcnt, xbest;
     int32_t any_flags;  // over the running views: 1 returned, 2 proactive candidate, 4 top-up candidate
+    int32_t ndec0;      // running views past prefill and not guests (the decode runway before victims)
     int32_t xh[XNB];
 };
 
@@ -609,6 +610,7 @@ __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
         S.n_mem = S.n_act = S.n_pre = S.n_cl = S.n_def = S.n_gm = S.n_pend = S.n_mready = S.n_part = 0;
         S.batch_now = 0; S.gm_tokens = 0; S.overflow = 0; S.sated = 0;
         S.any_flags = 0;
+        S.ndec0 = 0;
     }
     __syncthreads();
 
@@ -685,6 +687,7 @@ __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
     const int64_t mpre = d.prealloc_m;
     int fl = 0;
     if (rcached) {
+        unsigned nd = 0;
         for (int32_t k = tid; k < n_run; k += (int)blockDim.x) {
             const PV v = view_of(d, RUN[k]);
             S.rv[k] = v;
@@ -692,9 +695,12 @@ __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
             fl |= (ret ? 1 : 0) | ((!ret && v.eff < v.target && v.er <= mpre) ? 2 : 0) |
                   ((!ret && !(v.flags & PV_GUEST) && (v.flags & PV_READY) && v.pre >= v.kvn &&
                     (int64_t)v.eff - v.used <= mpre) ? 4 : 0);
+            nd += (!(v.flags & PV_GUEST) && v.pre >= v.kvn) ? 1u : 0u;
         }
         fl = (int)__reduce_or_sync(0xffffffffu, (unsigned)fl);
+        nd = __reduce_add_sync(0xffffffffu, nd);
         if ((tid & 31) == 0 && fl) atomicOr(&S.any_flags, fl);
+        if ((tid & 31) == 0 && nd) atomicAdd(&S.ndec0, (int32_t)nd);
     }
     __syncthreads();
     fl = rcached ? S.any_flags : 7;
@@ -1073,12 +1079,16 @@ __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
     prof_mark(d, 12);
     // ---- amortized round (scheduler.py:662-682) ---------------------------
     int64_t ndec = 0;
-    for (int32_t k = tid; k < n_run; k += (int)blockDim.x) {
-        int32_t i = RUN[k];
-        const PV v = RV(k);
-        if (d.st_removed[i] != sid && !(v.flags & PV_GUEST) && v.pre >= v.kvn) ndec++;
+    if (rcached && S.n_pre == 0) {  // no victims: the count taken while staging the views
+        ndec = S.ndec0;
+    } else {
+        for (int32_t k = tid; k < n_run; k += (int)blockDim.x) {
+            int32_t i = RUN[k];
+            const PV v = RV(k);
+            if (d.st_removed[i] != sid && !(v.flags & PV_GUEST) && v.pre >= v.kvn) ndec++;
+        }
+        ndec = blk_sum(ndec, S.b);
     }
-    ndec = blk_sum(ndec, S.b);
     prof_mark(d, 16);
     auto part_running = [&](int32_t p) { return (part_pv(d, S, p, now).flags & PV_RUNNING) != 0; };
     const int32_t n_fl = blk_compact(nullptr, n_part, d.l_grp, [&](int32_t p) { return part_running(p); }, S.b);
@@ -1094,9 +1104,11 @@ __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
     amortize(d, S, d.l_grp, n_fl, S.f_supply, now, &ftot);
     prof_mark(d, 18);
     int64_t spent = 0;  // sum of the in-flight grants (amortize compacts grp in place)
-    for (int32_t p = tid; p < n_part; p += (int)blockDim.x)
-        if (part_running(p)) spent += part_grant(d, S, p);
-    spent = blk_sum(spent, S.b);
+    if (n_fl > 0) {
+        for (int32_t p = tid; p < n_part; p += (int)blockDim.x)
+            if (part_running(p)) spent += part_grant(d, S, p);
+        spent = blk_sum(spent, S.b);
+    }
     if (tid == 0) {
         int64_t a = S.free - spent - S.runway;
         if (a < 0) a = 0;

@@ -81,6 +81,7 @@ __device__ __forceinline__ void guest_unlink(const Dev& d, int h, int i) {
         if (g != i) continue;
         if (prev < 0) d.guest[h] = d.gnext[g]; else d.gnext[prev] = d.gnext[g];
         d.gnext[g] = -1;
+        d.ctl->n_guests -= 1;
         return;
     }
 }
@@ -96,6 +97,7 @@ __device__ bool pool_embed(const Dev& d, int i, int64_t n, int h, int64_t start)
         if (!(start + n <= d.off[g] || (int64_t)d.off[g] + d.granted[g] <= start)) return false;
     new_record(d, i, (int32_t)n, h, (int32_t)start);
     if (tail < 0) d.guest[h] = i; else d.gnext[tail] = i;  // guests.append
+    d.ctl->n_guests += 1;
     d.ctl->granted_sum += n;
     return true;
 }
@@ -198,6 +200,7 @@ __device__ void pool_release(const Dev& d, int i) {
         d.host[g] = -1;
         d.off[g] = 0;
         d.gnext[g] = -1;
+        c.n_guests -= 1;
         const int64_t gfp = fp_tokens(d.granted[g], d.bs);
         c.fp_sum += gfp;
         pop_pages(d, g, gfp / d.bs);
