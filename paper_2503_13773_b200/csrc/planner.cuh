@@ -760,19 +760,21 @@ __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
 
     prof_mark(d, 2);
     // ---- critical waiting: embed first (scheduler.py:451-457) -------------
-    if (tid == 0) {
-        for (int32_t k = 0; k < n_nw; k++) {
-            int32_t i = NW[k];
-            if (try_embed(d, S, view_of(d, i), n_tri, sid)) {
-                int32_t ch = d.kv_need[i] - d.prefill[i];
-                d.l_gm_idx[S.n_gm] = i; d.l_gm_tok[S.n_gm] = ch; S.n_gm++;
-                S.gm_tokens += ch;
-            } else {
-                d.l_pend[S.n_pend++] = i;
+    if (n_nw > 0) {
+        if (tid == 0) {
+            for (int32_t k = 0; k < n_nw; k++) {
+                int32_t i = NW[k];
+                if (try_embed(d, S, view_of(d, i), n_tri, sid)) {
+                    int32_t ch = d.kv_need[i] - d.prefill[i];
+                    d.l_gm_idx[S.n_gm] = i; d.l_gm_tok[S.n_gm] = ch; S.n_gm++;
+                    S.gm_tokens += ch;
+                } else {
+                    d.l_pend[S.n_pend++] = i;
+                }
             }
         }
+        __syncthreads();
     }
-    __syncthreads();
     const int32_t n_pend0 = S.n_pend;
 
     prof_mark(d, 3);
@@ -860,68 +862,70 @@ __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
 
     prof_mark(d, 5);
     // ---- continuation, resumption, critical admission (scheduler.py:515-574)
-    if (tid == 0) {
-        const int32_t nb_B = (B + bs - 1) / bs;
-        for (int32_t k = 0; k < n_nr; k++) {
-            int32_t i = d.l_nr[k];
-            if (d.st_removed[i] == sid) continue;
-            int64_t cst = cost_of(d, i, B);
-            if (guest_of(d, i)) {
-                push_act(d, S, A_GROW, i, B);
-            } else if (cst <= S.free) {
-                push_act(d, S, A_GROW, i, B);
-                S.free -= cst;
-            } else if (S.rsvb >= nb_B) {
-                push_act(d, S, A_RESERVE, i, 0, nb_B);
-                S.rsvb -= nb_B;
-            } else {
-                d.st_stalled[i] = sid;
+    if (n_nr + n_nrp + n_pend0 > 0) {
+        if (tid == 0) {
+            const int32_t nb_B = (B + bs - 1) / bs;
+            for (int32_t k = 0; k < n_nr; k++) {
+                int32_t i = d.l_nr[k];
+                if (d.st_removed[i] == sid) continue;
+                int64_t cst = cost_of(d, i, B);
+                if (guest_of(d, i)) {
+                    push_act(d, S, A_GROW, i, B);
+                } else if (cst <= S.free) {
+                    push_act(d, S, A_GROW, i, B);
+                    S.free -= cst;
+                } else if (S.rsvb >= nb_B) {
+                    push_act(d, S, A_RESERVE, i, 0, nb_B);
+                    S.rsvb -= nb_B;
+                } else {
+                    d.st_stalled[i] = sid;
+                }
             }
-        }
-        for (int32_t k = 0; k < n_nrp; k++) {
-            int32_t i = d.l_nrp[k];
-            if (d.st_removed[i] == sid) continue;
-            if (guest_of(d, i)) {
-                push_act(d, S, A_GROW, i, B);
-                d.st_resumed[i] = sid;
-                continue;
+            for (int32_t k = 0; k < n_nrp; k++) {
+                int32_t i = d.l_nrp[k];
+                if (d.st_removed[i] == sid) continue;
+                if (guest_of(d, i)) {
+                    push_act(d, S, A_GROW, i, B);
+                    d.st_resumed[i] = sid;
+                    continue;
+                }
+                int64_t cst = cost_of(d, i, B);
+                if (cst <= S.free) {
+                    push_act(d, S, A_GROW, i, B);
+                    S.free -= cst;
+                    d.st_resumed[i] = sid;
+                }
             }
-            int64_t cst = cost_of(d, i, B);
-            if (cst <= S.free) {
-                push_act(d, S, A_GROW, i, B);
-                S.free -= cst;
-                d.st_resumed[i] = sid;
-            }
-        }
-        for (int32_t k = 0; k < n_pend0; k++) {
-            int32_t i = d.l_pend[k];
-            if (d.st_deferred[i] == sid) continue;
-            int64_t need = nw_need(d, i);
-            int64_t cst = cost_of(d, i, need);
-            if (cst <= S.free) {
-                push_act(d, S, d.holds[i] ? A_GROW : A_ALLOCATE, i, need);
-                S.free -= cst;
-            } else if (!guest_of(d, i)) {
-                int32_t nb = (int32_t)((need + bs - 1) / bs);
-                if (nb <= S.rsvb) {
-                    push_act(d, S, A_RESERVE, i, 0, nb);
-                    S.rsvb -= nb;
+            for (int32_t k = 0; k < n_pend0; k++) {
+                int32_t i = d.l_pend[k];
+                if (d.st_deferred[i] == sid) continue;
+                int64_t need = nw_need(d, i);
+                int64_t cst = cost_of(d, i, need);
+                if (cst <= S.free) {
+                    push_act(d, S, d.holds[i] ? A_GROW : A_ALLOCATE, i, need);
+                    S.free -= cst;
+                } else if (!guest_of(d, i)) {
+                    int32_t nb = (int32_t)((need + bs - 1) / bs);
+                    if (nb <= S.rsvb) {
+                        push_act(d, S, A_RESERVE, i, 0, nb);
+                        S.rsvb -= nb;
+                    } else {
+                        d.def_idx[S.n_def++] = i;
+                        continue;
+                    }
                 } else {
                     d.def_idx[S.n_def++] = i;
                     continue;
                 }
-            } else {
-                d.def_idx[S.n_def++] = i;
-                continue;
-            }
-            int32_t ch = d.kv_need[i] - d.prefill[i];
-            if (ch > 0) {
-                d.l_gm_idx[S.n_gm] = i; d.l_gm_tok[S.n_gm] = ch; S.n_gm++;
-                S.gm_tokens += ch;
+                int32_t ch = d.kv_need[i] - d.prefill[i];
+                if (ch > 0) {
+                    d.l_gm_idx[S.n_gm] = i; d.l_gm_tok[S.n_gm] = ch; S.n_gm++;
+                    S.gm_tokens += ch;
+                }
             }
         }
+        __syncthreads();
     }
-    __syncthreads();
 
     prof_mark(d, 6);
     // ---- decode members in running order (scheduler.py:576-593) -----------
