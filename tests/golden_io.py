@@ -15,7 +15,9 @@ TRACE_COLS = ("id", "arrival_us", "prompt_len", "true_output_len", "slo_ttft_us"
 
 
 def names():
-    return sorted(os.path.basename(p)[:-8] for p in glob.glob(os.path.join(GOLDEN, "*.json.gz")))
+    """Engine-run fixtures (plan_snapshots.json.gz holds planner snapshots instead)."""
+    return sorted(n for n in (os.path.basename(p)[:-8] for p in glob.glob(os.path.join(GOLDEN, "*.json.gz")))
+                  if not n.startswith("plan_"))
 
 
 def load(name):
