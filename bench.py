@@ -596,7 +596,7 @@ def device_arm(args, rank, world, dist):
         d2h = 0
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            _, members, _ = e.step_result()
+            _, members, _ = e.step_result(drain=drain_events)
             d2h += members.size * 4 + 16
             if drain_events:
                 e.events

@@ -216,6 +216,33 @@ int co_preempt(co_engine* eng, int64_t idx, int32_t strategy, int64_t now_us, in
 /* Blocking readbacks into caller-owned host buffers. */
 int co_get_scalars(co_engine* eng, co_scalars* out);
 int co_read_field(co_engine* eng, int32_t field, int64_t* out /* n values */);
+/* co_step_result followed by co_drain_log in one call (the per-step API with
+ * the step's event log taken along; CO_EAGAIN as co_drain_log when the log
+ * buffers are too small -- the step has run, drain again with larger ones). */
+int co_step_result_log(co_engine* eng, int32_t* result, int32_t* members, int64_t max_members,
+                       int64_t* n_members, int64_t* iter_end_us, co_event* events, int64_t max_events,
+                       int32_t* log_members, int64_t max_log_members, int64_t* samples, int64_t max_samples,
+                       int64_t* counts);
+/* The same with every argument in one caller-owned struct (filled once and
+ * reused: a binding then passes a single pointer per step). */
+typedef struct co_step_args {
+    co_engine* eng;
+    int32_t* result;
+    int32_t* members;
+    int64_t max_members;
+    int64_t* n_members;
+    int64_t* iter_end_us;
+    co_event* events;
+    int64_t max_events;
+    int32_t* log_members;
+    int64_t max_log_members;
+    int64_t* samples;
+    int64_t max_samples;
+    int64_t* counts;
+    int32_t drain;  /* 0: co_step_result, 1: co_step_result_log */
+    int32_t _pad;
+} co_step_args;
+int co_step_packed(const co_step_args* args);
 /* Undrained append-log sizes in one call: out[0] events, out[1] iteration
  * members, out[2] utilization samples (the counts co_pending_events and
  * co_get_scalars' n_samples report). */

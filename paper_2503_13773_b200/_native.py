@@ -76,6 +76,14 @@ class CoScalars(C.Structure):
     ]
 
 
+class CoStepArgs(C.Structure):  # include/cacheopt.h co_step_args
+    _fields_ = [("eng", C.c_void_p), ("result", C.c_void_p), ("members", C.c_void_p), ("max_members", C.c_int64),
+                ("n_members", C.c_void_p), ("iter_end_us", C.c_void_p), ("events", C.c_void_p),
+                ("max_events", C.c_int64), ("log_members", C.c_void_p), ("max_log_members", C.c_int64),
+                ("samples", C.c_void_p), ("max_samples", C.c_int64), ("counts", C.c_void_p), ("drain", C.c_int32),
+                ("_pad", C.c_int32)]
+
+
 class CoEvent(C.Structure):
     _fields_ = [("kind", C.c_int32), ("idx", C.c_int32), ("t", C.c_int64), ("a", C.c_int64),
                 ("b", C.c_int64), ("c", C.c_int64)]
@@ -83,7 +91,7 @@ class CoEvent(C.Structure):
 
 EXPORTS = (
     "co_create", "co_destroy", "co_step", "co_run", "co_preempt", "co_get_scalars", "co_read_field",
-    "co_drain_events", "co_pending_events", "co_pending_log", "co_drain_log", "co_pool_create", "co_pool_destroy", "co_pool_op", "co_pool_find_host",
+    "co_drain_events", "co_pending_events", "co_pending_log", "co_drain_log", "co_step_result_log", "co_step_packed", "co_pool_create", "co_pool_destroy", "co_pool_op", "co_pool_find_host",
     "co_pool_state", "co_pool_check", "co_pool_read_tables", "co_sched_op", "co_swap_io_stats", "co_plan_snapshot", "co_drain_samples", "co_read_token_times",
     "co_check_invariants", "co_last_device_ms", "co_kernels_per_step", "co_time_steps", "co_last_error",
     "co_version", "co_read_block_tables", "co_data_stats", "co_kv_verify", "co_read_decode", "co_host_link_gbs",
@@ -159,6 +167,8 @@ def load() -> C.CDLL:
         "co_plan_snapshot": (C.c_int, [V, I64P, I64P, I64P, I32P, C.c_int64]),
         "co_pool_read_tables": (C.c_int, [V, I32P, I32P, C.c_int64, I32P, I32P]),
         "co_drain_log": (C.c_int, [V, V, C.c_int64, V, C.c_int64, V, C.c_int64, V]),
+        "co_step_result_log": (C.c_int, [V, V, V, C.c_int64, V, V, V, C.c_int64, V, C.c_int64, V, C.c_int64, V]),
+        "co_step_packed": (C.c_int, [V]),
         "co_drain_samples": (C.c_int, [V, I64P, C.c_int64, I64P]),
         "co_read_token_times": (C.c_int, [V, I64P, I64P]),
         "co_check_invariants": (C.c_int, [V]),

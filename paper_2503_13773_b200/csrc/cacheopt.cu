@@ -475,6 +475,8 @@ static int read_arr(co_engine* E, const T* src, int64_t* out) {
 extern "C" {
 
 const char* co_last_error(void) { return g_err.c_str(); }
+int co_drain_log(co_engine* E, co_event* events, int64_t max_events, int32_t* members, int64_t max_members,
+                 int64_t* samples, int64_t max_samples, int64_t* counts);
 const char* co_version(void) { return "cacheopt-b200 0.1 (sm_100a)"; }
 
 int co_destroy(co_engine* E) {
@@ -982,6 +984,24 @@ int co_step_result(co_engine* E, int32_t* result, int32_t* members, int64_t max_
         return CO_OK;
     }
     return fail(CO_EDEVICE, "step could not make buffer headroom");
+}
+
+int co_step_result_log(co_engine* E, int32_t* result, int32_t* members, int64_t max_members, int64_t* n_members,
+                       int64_t* iter_end_us, co_event* events, int64_t max_events, int32_t* log_members,
+                       int64_t max_log_members, int64_t* samples, int64_t max_samples, int64_t* counts) {
+    CO_RANGE("co_step_result_log");
+    int r = co_step_result(E, result, members, max_members, n_members, iter_end_us);
+    if (r) return r;
+    return co_drain_log(E, events, max_events, log_members, max_log_members, samples, max_samples, counts);
+}
+
+int co_step_packed(const co_step_args* a) {
+    if (!a) return fail(CO_EINVAL, "null argument");
+    if (!a->drain)
+        return co_step_result(a->eng, a->result, a->members, a->max_members, a->n_members, a->iter_end_us);
+    return co_step_result_log(a->eng, a->result, a->members, a->max_members, a->n_members, a->iter_end_us,
+                              a->events, a->max_events, a->log_members, a->max_log_members, a->samples,
+                              a->max_samples, a->counts);
 }
 
 int co_step(co_engine* E, int32_t* result) {

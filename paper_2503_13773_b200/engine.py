@@ -419,6 +419,8 @@ class Engine:
         self._resbuf = None
         self._evbuf = self._membuf = self._sbuf = None
         self._drain_args = None
+        self._log_clean = False
+        self._step_args = {}
         self._rid_np = np.array(self._rid, dtype=np.int64)
         self._cnt = (C.c_int64 * 3)()
 
@@ -439,6 +441,7 @@ class Engine:
         self._cache.clear()
         self._sc = None
         self._req_stale = True
+        self._log_clean = False
 
     def _scalars(self) -> N.CoScalars:
         if self._sc is None:
@@ -472,22 +475,46 @@ class Engine:
         so the first step()/step_result() after this is not a capture."""
         N.check(self._lib.co_prepare_step(self._h), "co_prepare_step")
 
-    def step_result(self):
+    def step_result(self, drain: bool = True):
         """step() plus this iteration's result in one device round trip:
-        (step()'s bool, int32 array [m, 2] of (req_id, tokens) that ran, end_us)."""
+        (step()'s bool, int32 array [m, 2] of (req_id, tokens) that ran, end_us).
+        With `drain` (default) the step's event log and utilization sample
+        come back in the same library call (co_step_packed -> co_step_result_log)
+        into the host lists, so `events` then has nothing left to fetch."""
+        drain = bool(drain and self.cfg.record_events)
         if self._resbuf is None:
             self._resbuf = np.empty(2 * (3 * self._n + 64), dtype=np.int32)
             self._sr_out = (C.c_int32(), C.c_int64(), C.c_int64())
+        if drain and self._evbuf is None:
+            self._drain()  # sizes the host log buffers once
+        sa = self._step_args.get(drain)
+        if sa is None:
             r, n, end = self._sr_out
-            self._sr_args = (self._h, C.byref(r), _ptr(self._resbuf, C.c_int32), len(self._resbuf) // 2,
-                             C.byref(n), C.byref(end))
+            a = N.CoStepArgs(eng=self._h.value, result=C.addressof(r), members=self._resbuf.ctypes.data,
+                             max_members=len(self._resbuf) // 2, n_members=C.addressof(n),
+                             iter_end_us=C.addressof(end), drain=int(drain))
+            if drain:
+                a.events, a.max_events = self._ev_addr, len(self._evbuf)
+                a.log_members, a.max_log_members = self._mem_addr, len(self._membuf) // 2
+                a.samples, a.max_samples = C.addressof(self._sbuf), len(self._sbuf) // 2
+                a.counts = C.addressof(self._cnt)
+            sa = self._step_args[drain] = (a, C.addressof(a))
         r, n, end = self._sr_out
         self._cache.clear()
         self._sc = None
         self._req_stale = True
-        rc = self._lib.co_step_result(*self._sr_args)
-        if rc:
-            N.check(rc, "co_step_result")
+        self._log_clean = False
+        rc = self._lib.co_step_packed(sa[1])
+        if drain:
+            if rc == N.CO_EAGAIN:  # the step ran; its log needs larger buffers
+                self._drain()
+            elif rc:
+                N.check(rc, "co_step_packed")
+            else:
+                self._take_log()
+            self._log_clean = True
+        elif rc:
+            N.check(rc, "co_step_packed")
         k = n.value
         out = self._resbuf[:2 * k].reshape(k, 2).astype(np.int64)
         if k:
@@ -667,6 +694,7 @@ class Engine:
                 self._membuf = (C.c_int32 * (2 * nm))()
                 self._sbuf = (C.c_int64 * (2 * ns))()
                 self._drain_args = (self._h, self._evbuf, ne, self._membuf, nm, self._sbuf, ns, self._cnt)
+                self._step_args = {}  # (they point at these buffers)
                 self._mem_addr = C.addressof(self._membuf)
                 self._ev_addr = C.addressof(self._evbuf)
             rc = self._lib.co_drain_log(*self._drain_args)
@@ -674,6 +702,10 @@ class Engine:
                 break
             self._evbuf = None  # grow to the sizes returned in cnt and retry
         N.check(rc, "co_drain_log")
+        self._take_log()
+
+    def _take_log(self) -> None:
+        cnt = self._cnt
         ne, ns = cnt[0], cnt[2]
         if ne:
             self._events.extend(self._convert(ne, None))
@@ -690,7 +722,8 @@ class Engine:
 
     @property
     def events(self) -> List[dict]:
-        self._drain()
+        if not self._log_clean:
+            self._drain()
         return self._events
 
     @property
