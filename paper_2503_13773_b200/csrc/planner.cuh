@@ -222,7 +222,7 @@ __device__ __forceinline__ int32_t& part_grant(const Dev& d, PlanSh& S, int32_t 
 // The exact share computation of a warp of demands with a 128-bit weight sum
 // (some weight >= 2^57; never on realistic traces).
 __device__ __forceinline__ int64_t amortize_lane_wide(const Dev& d, const PV& v, bool live, int64_t supply,
-                                                   int64_t tot) {
+                                                   int64_t tot, int32_t m) {
     const uint64_t w = live ? amort_weight(v) : 0;
     uint64_t lo = w, hi = 0;
 #pragma unroll
@@ -241,7 +241,7 @@ __device__ __forceinline__ int64_t amortize_lane_wide(const Dev& d, const PV& v,
     const uint64_t rhi = (uint64_t)(r >> 64), rlo = (uint64_t)r;
     const uint32_t id = live ? (uint32_t)v.idrank : 0xffffffffu;
     int32_t rank = 0;
-    for (int j = 0; j < 32; j++) {
+    for (int j = 0; j < m; j++) {
         const uint64_t jhi = __shfl_sync(0xffffffffu, rhi, j), jlo = __shfl_sync(0xffffffffu, rlo, j);
         const uint32_t jid = __shfl_sync(0xffffffffu, id, j);
         const bool jlive = __shfl_sync(0xffffffffu, live ? 1 : 0, j);
@@ -255,7 +255,7 @@ __device__ __forceinline__ int64_t amortize_lane_wide(const Dev& d, const PV& v,
         const int64_t left_blocks = (supply - warp_sum64(live ? fl : 0)) / bs;
         const uint64_t rem = (uint64_t)(g - fl);
         int32_t rk = 0;
-        for (int j = 0; j < 32; j++) {
+        for (int j = 0; j < m; j++) {
             const uint64_t jr = __shfl_sync(0xffffffffu, rem, j);
             const uint32_t jid = __shfl_sync(0xffffffffu, id, j);
             const bool jlive = __shfl_sync(0xffffffffu, live ? 1 : 0, j);
@@ -290,7 +290,7 @@ __device__ void amortize_warp(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, 
                 const PV v = live ? part_pv(d, S, p, now) : PV{};
                 const uint64_t w = live ? amort_weight(v) : 0;
                 if (__any_sync(0xffffffffu, w >= (1ull << 57))) {
-                    g = amortize_lane_wide(d, v, live, supply, tot);
+                    g = amortize_lane_wide(d, v, live, supply, tot, m);
                 } else {
                     uint64_t W = w;
 #pragma unroll
@@ -315,7 +315,7 @@ __device__ void amortize_warp(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, 
                     // largest remainder first, ties by id (scheduler.py:240-242)
                     int32_t rank = 0;
 #pragma unroll 4
-                    for (int j = 0; j < 32; j++) {
+                    for (int j = 0; j < m; j++) {
                         const uint64_t jr = __shfl_sync(0xffffffffu, r, j);
                         const uint32_t jid = __shfl_sync(0xffffffffu, id, j);
                         const bool jlive = __shfl_sync(0xffffffffu, live ? 1 : 0, j);
@@ -332,7 +332,7 @@ __device__ void amortize_warp(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, 
                         const int32_t rem = gi - fl;
                         int32_t rk = 0;
 #pragma unroll 4
-                        for (int j = 0; j < 32; j++) {
+                        for (int j = 0; j < m; j++) {
                             const int32_t jr = __shfl_sync(0xffffffffu, rem, j);
                             const uint32_t jid = __shfl_sync(0xffffffffu, id, j);
                             const bool jlive = __shfl_sync(0xffffffffu, live ? 1 : 0, j);
