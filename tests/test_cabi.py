@@ -40,8 +40,9 @@ def test_struct_layouts_match_header():
 #include <stddef.h>
 #include "cacheopt.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu %zu\n", sizeof(co_config), sizeof(co_trace), sizeof(co_luts),
-         sizeof(co_scalars), sizeof(co_event), offsetof(co_config, s_star), offsetof(co_scalars, n_live));
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(co_config), sizeof(co_trace), sizeof(co_luts),
+         sizeof(co_scalars), sizeof(co_event), offsetof(co_config, s_star), offsetof(co_scalars, n_live),
+         sizeof(co_step_args), offsetof(co_step_args, counts), offsetof(co_step_args, drain));
   return 0;
 }'''
     with tempfile.TemporaryDirectory() as d:
@@ -51,7 +52,8 @@ int main(void) {
         subprocess.run(["gcc", "-I", os.path.dirname(HEADER), c, "-o", exe], check=True)
         got = [int(x) for x in subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split()]
     want = [C.sizeof(N.CoConfig), C.sizeof(N.CoTrace), C.sizeof(N.CoLuts), C.sizeof(N.CoScalars),
-            C.sizeof(N.CoEvent), N.CoConfig.s_star.offset, N.CoScalars.n_live.offset]
+            C.sizeof(N.CoEvent), N.CoConfig.s_star.offset, N.CoScalars.n_live.offset,
+            C.sizeof(N.CoStepArgs), N.CoStepArgs.counts.offset, N.CoStepArgs.drain.offset]
     assert got == want
 
 
