@@ -684,7 +684,7 @@ def device_arm(args, rank, world, dist):
                      "peak_kind": peak_kind, "algorithmic_bytes_per_launch": algo,
                      "note": "the step's dominant kernel is the single-CTA plan+apply (k_serial: the ordered greedy "
                              "loops of scheduler.py and engine.py): latency-bound on instruction fetch (ncu: "
-                             "stall_no_instruction ~50%, ~75 KB of SASS executed per step), so its HBM fraction "
+                             "stall_no_instruction ~46%, ~54 KB of SASS executed per step), so its HBM fraction "
                              "is ~0 by construction; the decode leg carries the bandwidth roofline"},
         "cpu_baseline": {"value": cpu_val, "unit": UNIT, "cores": cpu_cores, "kind": "port",
                          "ms_per_step": cpu_ms, "host_cpu": host_cpu(),
@@ -702,8 +702,8 @@ def device_arm(args, rank, world, dist):
                        "arrivals in the window)",
                 "without_event_drain": e2e_dec_nd / (e2e_ms_nd * 1e-3)},
         "gpu_launches": args.steps * kernels_per_step,
-        "gpu_launches_note": f"{kernels_per_step} own kernels per step (k_begin, k_classify with admission, "
-                             "k_serial = plan + apply + invariant check); no library kernels",
+        "gpu_launches_note": f"{kernels_per_step} own kernels per step (k_classify: begin + admission + "
+                             "the planner's views; k_serial: plan + apply + invariant check + log mirror); no library kernels",
         "clocks": clocks.summary(),
         "collective": coll,
         **extra,
