@@ -81,7 +81,7 @@ typedef struct co_config {
     int32_t validate_every;         /* engine.py:77 */
     int32_t record_events;          /* engine.py:78 */
     int32_t padding;                /* estimation.py:139-142 for the run's confidence */
-    int32_t _pad0;
+    int32_t invert_amortization;    /* scheduler.py:43, :233: amortization weights 1/(rt*p) */
     int64_t s_star;                 /* scheduler.py:381-393 sweet spot */
     int64_t t_i_init_us;            /* engine.py:268-270 */
     /* N2/N3 KV data plane (no reference counterpart; 0 layers = off).

@@ -126,6 +126,28 @@ def estimate_from_noise(true_len: int, err: int, flip: bool, pad: int) -> Tuple[
     return pred, est
 
 
+def split_largest_remainder_inverted(demands: List[Tuple[int, int, int, int]], supply: int) -> Dict[int, int]:
+    """scheduler.py:211-243 with ``invert=True`` (weights 1/(rt*p), :233),
+    restated with ``Fraction`` exactly as the reference computes it (the
+    shares have no small common denominator)."""
+    from fractions import Fraction
+    if supply < 0:
+        raise ValueError("a_prime must be >= 0")
+    live = [d for d in demands if d[1] > 0]
+    if not live:
+        return {}
+    if sum(d[1] for d in live) <= supply:
+        return {d[0]: d[1] for d in live}
+    w = {d[0]: 1 / Fraction(max(1, d[2]) * max(1, d[3])) for d in live}
+    W = sum(w.values())
+    share = {r: Fraction(supply) * x / W for r, x in w.items()}
+    q = {r: int(x) for r, x in share.items()}
+    left = supply - sum(q.values())
+    for rid in sorted(share, key=lambda r: (-(share[r] - q[r]), r))[:left]:
+        q[rid] += 1
+    return q
+
+
 def split_largest_remainder(demands: List[Tuple[int, int, int, int]], supply: int) -> Dict[int, int]:
     """scheduler.py:211-243 without ``Fraction``: every share has the common
     denominator W = sum(w), so floor(a*w_i/W) and the remainder a*w_i mod W
@@ -165,8 +187,6 @@ class CacheOptOracle:
             raise ValueError("request ids must be unique")
         if cfg.sched.policy not in ("cacheopt", "vllm_block", "sarathi_chunked", "rlp", "s3"):
             raise ValueError(f"unknown policy {cfg.sched.policy!r}")
-        if cfg.sched.invert_amortization:
-            raise ValueError("invert_amortization is not restated")
         self.cfg = cfg
         reqs = sorted(requests, key=lambda r: (r.arrival_us, r.id))  # engine.py:241
         n = self.n = len(reqs)
@@ -1059,7 +1079,7 @@ class CacheOptOracle:
         # amortized round (scheduler.py:640-682)
         def amortize(ps, supply):
             dem = [(self.rid[i], mt, max(1, rt[i]), max(1, int(kvn[i]))) for i, mt in ps]
-            g = split_largest_remainder(dem, supply)
+            g = (split_largest_remainder_inverted if sc.invert_amortization else split_largest_remainder)(dem, supply)
             total = sum(d[1] for d in dem)
             if total > supply and g:
                 fl = {r: (x // bs) * bs for r, x in g.items()}

@@ -29,7 +29,8 @@ OUT = os.path.join(ROOT, "tests", "golden")
 sys.path.insert(0, ROOT)
 
 SEEDS = [0, 1, 2, 5, 9, 13, 21, 34]
-STACK_SEEDS = [8, 13, 57]  # regimes where a host carries up to 3-4 stacked guests (allow_stacking=True)
+STACK_SEEDS = [8, 13, 57]
+INVERT_SEEDS = [7, 9, 12, 18]  # invert_amortization=True (scheduler.py:43, :233): grants differ from the default  # regimes where a host carries up to 3-4 stacked guests (allow_stacking=True)
 BASELINE_CASES = [("vllm_block", 5), ("vllm_block", 13), ("sarathi_chunked", 13), ("sarathi_chunked", 9),
                   ("rlp", 6), ("s3", 2), ("s3", 13)]
 
@@ -136,6 +137,15 @@ def main():
             continue
         p = case_params(s)
         p["allow_stacking"] = True
+        reqs, cfg = ref_build(p)
+        run_and_store(name, p, reqs, cfg)
+    # invert_amortization=True: amortization weights 1/(rt*p) (scheduler.py:233)
+    for s in INVERT_SEEDS:
+        name = f"inv_case{s:02d}"
+        if only and name not in only:
+            continue
+        p = case_params(s)
+        p["sched"] = {**p["sched"], "invert_amortization": True}
         reqs, cfg = ref_build(p)
         run_and_store(name, p, reqs, cfg)
     # the four baseline planners (scheduler.py:760-936) on regimes that preempt

@@ -39,7 +39,7 @@ class CoConfig(C.Structure):
         ("epsilon_us", C.c_int64), ("n_slo_edges", C.c_int32), ("token_step", C.c_int32),
         ("slo_edges_us", C.c_int64 * MAX_SLO_EDGES), ("iter_base_ms", C.c_double),
         ("iter_per_token_ms", C.c_double), ("horizon_factor", C.c_int64), ("validate_every", C.c_int32),
-        ("record_events", C.c_int32), ("padding", C.c_int32), ("_pad0", C.c_int32), ("s_star", C.c_int64),
+        ("record_events", C.c_int32), ("padding", C.c_int32), ("invert_amortization", C.c_int32), ("s_star", C.c_int64),
         ("t_i_init_us", C.c_int64), ("kv_layers", C.c_int32), ("kv_heads", C.c_int32), ("q_heads", C.c_int32),
         ("head_dim", C.c_int32), ("host_swap_pages", C.c_int64), ("decode", C.c_int32), ("decode_split", C.c_int32),
         ("policy", C.c_int32), ("vllm_block_tokens", C.c_int32), ("s3_bucket_tokens", C.c_int32),

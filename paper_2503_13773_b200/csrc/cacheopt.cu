@@ -614,6 +614,7 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     d.rsv_target = cfg->reserved_blocks; d.eps = cfg->epsilon_us; d.capacity = cfg->capacity_tokens;
     d.s_star = cfg->s_star; d.s_max = lu->s_max;
     d.policy = cfg->policy; d.vbt = cfg->vllm_block_tokens; d.s3b = cfg->s3_bucket_tokens; d.rlp_pad = cfg->rlp_padding;
+    d.inv = cfg->invert_amortization ? 1 : 0;
     for (int k = 0; k < CO_MAX_SLO_EDGES; k++) d.edges[k] = k < cfg->n_slo_edges ? cfg->slo_edges_us[k] : 0;
     d.base_ms = cfg->iter_base_ms; d.per_token_ms = cfg->iter_per_token_ms;
     d.ev_cap = std::max<int64_t>(1 << 16, 8 * n + 4096);
@@ -760,6 +761,7 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
     }
     AL(d.l_tri_key, n); AL(d.am_rhi, n3); AL(d.am_rlo, n3); AL(d.rank_to_idx, n);
     AL(d.sk0, n3); AL(d.sk1, n3); AL(d.sk2, n3); AL(d.sk_item, n3);
+    if (d.inv) AL(d.big, 5 * (int64_t)INV_LIMBS);
     AL(d.events, d.ev_cap); AL(d.members, 2 * d.mem_cap); AL(d.samples, 2 * d.sample_cap);
     AL(d.ctl, 1);
 
@@ -851,6 +853,9 @@ static int check_device_error(co_engine* E) {
                      : err == 7 ? "host swap pool exhausted (raise KVLayout.host_swap_pages)"
                      : err == 8 ? "decode work-item buffer full"
                      : err == 9 ? "more decode members than the decode output buffer holds (4096)"
+                     : err == 10 ? "N'_w queue extension found no candidates"
+                     : err == 11 ? "invert_amortization: more live participants in one amortized group than the "
+                                   "exact serial path takes (1024)"
                                 : "device engine error";
     snprintf(buf, sizeof(buf), "%s [code %d, info %d %d]", what, err, E->h_ctl->err_info[0], E->h_ctl->err_info[1]);
     return fail(CO_EDEVICE, buf);

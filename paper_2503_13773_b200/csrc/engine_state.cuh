@@ -70,6 +70,8 @@ struct Dev {
     int32_t record_events, validate_every, pad, idbits, n_edges, token_step, rsv_target;
     int32_t key_bits;            // composite sort key width: class(2) | blown(1) | time | idrank
     int32_t policy, vbt, s3b, rlp_pad;  // planner (CO_POLICY_*) and the baselines' parameters
+    int32_t inv;                 // invert_amortization (scheduler.py:43): exact serial path, planner.cuh
+    uint64_t* big;               // its multi-precision scratch: 5 numbers of INV_LIMBS limbs
     int64_t eps, capacity, s_star, s_max, ev_cap, mem_cap, sample_cap;
     int64_t edges[CO_MAX_SLO_EDGES];
     double base_ms, per_token_ms;

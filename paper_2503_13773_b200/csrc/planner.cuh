@@ -17,6 +17,8 @@ __device__ __forceinline__ int64_t pv_cost(const PV& v, int64_t grant, int bs) {
 }
 
 constexpr int PV_CAP = 1024;
+constexpr int INV_CAP = 1024;            // live demands per group on the inverted-weight path
+constexpr int INV_LIMBS = INV_CAP + 8;   // 64-bit limbs per multi-precision number there
 struct FV {  // fulfilled provider candidate (scheduler.py:685-689, 711-716)
     int64_t gain;
     int32_t er, idrank, i, _pad;
@@ -352,10 +354,214 @@ __device__ void amortize_warp(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, 
     __syncthreads();
 }
 
+// ---------------------------------------------------------------------------
+// invert_amortization=True (scheduler.py:43, :229-243 with weights 1/w_i,
+// w_i = max(1,rt)*max(1,prompt), :233).  The shares a'*(1/w_i)/S, S = sum
+// 1/w_j, have no small common denominator, so this path is exact
+// multi-precision arithmetic on one thread (an ablation mode: no fast path).
+//   S = p/q with q = prod w_j, p = sum_j prod_{k!=j} w_k  (unreduced; exact)
+//   T = a'/S = a'q/p,  F = floor(T) (< 2^128),  phi = T - F = R/p, R = a'q - F p
+//   floor(share_i) = floor(T/w_i) = floor(F/w_i),  rho_i = F mod w_i
+//   frac_i = (rho_i + phi)/w_i, so frac_i - frac_k has the sign of
+//   c*p - D*R with c = rho_i w_k - rho_k w_i and D = w_i - w_k.
+// Most comparisons are settled by a double estimate (error < 2^-50); the rest
+// are exact.  Limbs are little-endian uint64.
+struct Big { uint64_t* l; int n; };
+
+__device__ inline void big_set1(Big& a, uint64_t v) { a.l[0] = v; a.n = v ? 1 : 0; }
+__device__ inline void big_trim(Big& a) { while (a.n > 0 && a.l[a.n - 1] == 0) a.n--; }
+// o = a * m (m < 2^128); o must not alias a
+__device__ inline void big_mul_u128(Big& o, const Big& a, unsigned __int128 m) {
+    const uint64_t m0 = (uint64_t)m, m1 = (uint64_t)(m >> 64);
+    for (int k = 0; k < a.n + 2; k++) o.l[k] = 0;
+    for (int t = 0; t < 2; t++) {
+        const uint64_t mm = t ? m1 : m0;
+        if (!mm) continue;
+        uint64_t carry = 0;
+        for (int k = 0; k < a.n; k++) {
+            unsigned __int128 x = (unsigned __int128)a.l[k] * mm + o.l[k + t] + carry;
+            o.l[k + t] = (uint64_t)x;
+            carry = (uint64_t)(x >> 64);
+        }
+        for (int k = a.n + t; carry; k++) {
+            unsigned __int128 x = (unsigned __int128)o.l[k] + carry;
+            o.l[k] = (uint64_t)x;
+            carry = (uint64_t)(x >> 64);
+        }
+    }
+    o.n = a.n + 2;
+    big_trim(o);
+}
+// a = a * m + b (in place; m < 2^64)
+__device__ inline void big_muladd(Big& a, uint64_t m, const Big& b) {
+    uint64_t carry = 0;
+    const int n = a.n > b.n ? a.n : b.n;
+    for (int k = 0; k < n; k++) {
+        const uint64_t ak = k < a.n ? a.l[k] : 0, bk = k < b.n ? b.l[k] : 0;
+        unsigned __int128 x = (unsigned __int128)ak * m + bk + carry;
+        a.l[k] = (uint64_t)x;
+        carry = (uint64_t)(x >> 64);
+    }
+    a.n = n;
+    if (carry) a.l[a.n++] = carry;
+    big_trim(a);
+}
+__device__ inline int big_cmp(const Big& a, const Big& b) {
+    if (a.n != b.n) return a.n < b.n ? -1 : 1;
+    for (int k = a.n - 1; k >= 0; k--)
+        if (a.l[k] != b.l[k]) return a.l[k] < b.l[k] ? -1 : 1;
+    return 0;
+}
+// a -= b (a >= b)
+__device__ inline void big_sub(Big& a, const Big& b) {
+    uint64_t borrow = 0;
+    for (int k = 0; k < a.n; k++) {
+        const uint64_t bk = k < b.n ? b.l[k] : 0;
+        const uint64_t d1 = a.l[k] - bk, b1 = a.l[k] < bk ? 1 : 0;
+        a.l[k] = d1 - borrow;
+        borrow = b1 | (d1 < borrow ? 1 : 0);
+    }
+    big_trim(a);
+}
+// a / b as a double (b > 0): the top limbs of both
+__device__ inline double big_ratio(const Big& a, const Big& b) {
+    auto top = [](const Big& x, int n) {
+        double v = 0;
+        for (int k = n - 1; k >= 0 && k >= n - 3; k--) v = v * 18446744073709551616.0 + (k < x.n ? (double)x.l[k] : 0.0);
+        return v;
+    };
+    const int n = a.n > b.n ? a.n : b.n;
+    return n ? top(a, n) / top(b, n) : 0.0;
+}
+
+struct InvCtx {
+    Big p, R, X, Y;
+    double phi;
+};
+// sign of frac_i - frac_k (see above); w = weights, rho = F mod w
+__device__ inline int inv_frac_cmp(InvCtx& C, uint64_t wi, uint64_t ri, uint64_t wk, uint64_t rk) {
+    if (wi == wk) return ri == rk ? 0 : (ri > rk ? 1 : -1);
+    const double fi = ((double)ri + C.phi) / (double)wi, fk = ((double)rk + C.phi) / (double)wk;
+    if (fi - fk > 0x1p-40) return 1;
+    if (fk - fi > 0x1p-40) return -1;
+    const unsigned __int128 a = (unsigned __int128)ri * wk, b = (unsigned __int128)rk * wi;
+    const int sc = a == b ? 0 : (a > b ? 1 : -1);
+    const unsigned __int128 cm = a >= b ? a - b : b - a;
+    const int sd = wi > wk ? 1 : -1;
+    const uint64_t dm = wi > wk ? wi - wk : wk - wi;
+    if (sc == 0) return C.R.n == 0 ? 0 : -sd;
+    if (sc != sd) return sc;  // c*p and -D*R share the sign of c
+    big_mul_u128(C.X, C.p, cm);
+    big_mul_u128(C.Y, C.R, dm);
+    const int s = big_cmp(C.X, C.Y);
+    return sc > 0 ? s : -s;
+}
+
+// amortize() with inverted weights: thread 0 computes every grant; the block
+// waits at one barrier.  Errors (code 11) when a group holds more than
+// INV_CAP live demands.
+__device__ __noinline__ void amortize_inverted(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64_t supply, int64_t now,
+                                  int64_t* total_out) {
+    if (threadIdx.x == 0) {
+        int64_t tot = 0, live_tot = 0;
+        int32_t L = 0;
+        int32_t* live = d.sk_item;
+        for (int32_t k = 0; k < m; k++) {
+            const int32_t p = grp[k];
+            const int64_t need = part_need(d, S, p);
+            tot += need;
+            part_grant(d, S, p) = 0;
+            if (need > 0) { live_tot += need; live[L++] = p; }
+        }
+        S.b.red[0] = tot;
+        if (L > 0 && supply > 0 && live_tot <= supply) {
+            for (int32_t k = 0; k < L; k++) part_grant(d, S, live[k]) = part_need(d, S, live[k]);
+        } else if (L > INV_CAP && supply > 0) {
+            if (d.ctl) { d.ctl->error = 11; d.ctl->err_info[0] = L; }
+        } else if (L > 0 && supply > 0) {
+            Big q{d.big, 0}, A{d.big + INV_LIMBS, 0};
+            InvCtx C{{d.big + 2 * INV_LIMBS, 0}, {d.big + INV_LIMBS, 0}, {d.big + 3 * INV_LIMBS, 0},
+                     {d.big + 4 * INV_LIMBS, 0}, 0.0};
+            uint64_t* w = d.am_rhi;   // weights by live position
+            uint64_t* rho = d.am_rlo;
+            big_set1(q, 1);
+            C.p.n = 0;
+            for (int32_t k = 0; k < L; k++) {
+                w[k] = amort_weight(part_pv(d, S, live[k], now));
+                big_muladd(C.p, w[k], q);    // p = p*w + q
+                Big z{C.X.l, 0};
+                big_muladd(q, w[k], z);      // q = q*w
+            }
+            big_mul_u128(A, q, (unsigned __int128)(uint64_t)supply);  // A = a' q
+            // F = floor(A / p) by bits (F <= a' * min w < 2^128)
+            unsigned __int128 F = 0;
+            for (int b = 127; b >= 0; b--) {
+                const unsigned __int128 cand = F | ((unsigned __int128)1 << b);
+                big_mul_u128(C.X, C.p, cand);
+                if (big_cmp(C.X, A) <= 0) F = cand;
+            }
+            big_mul_u128(C.X, C.p, F);
+            big_sub(A, C.X);  // A becomes R = a'q - F p (C.R aliases it)
+            C.R.n = A.n;
+            C.phi = big_ratio(C.R, C.p);
+            int64_t sq = 0;
+            for (int32_t k = 0; k < L; k++) {
+                const uint64_t g = (uint64_t)(F / w[k]);
+                rho[k] = (uint64_t)(F % w[k]);
+                part_grant(d, S, live[k]) = (int32_t)g;
+                sq += (int64_t)g;
+            }
+            // largest remainder first, ties by req_id (scheduler.py:240-242):
+            // partial selection of the `left` best positions to the front
+            const int64_t left = supply - sq;
+            auto id_of = [&](int32_t k) { return part_pv(d, S, live[k], now).idrank; };
+            for (int32_t t = 0; t < left && t < L; t++) {
+                int32_t best = t;
+                for (int32_t k = t + 1; k < L; k++) {
+                    const int c = inv_frac_cmp(C, w[k], rho[k], w[best], rho[best]);
+                    if (c > 0 || (c == 0 && id_of(k) < id_of(best))) best = k;
+                }
+                if (best != t) {
+                    int32_t ti = live[t]; live[t] = live[best]; live[best] = ti;
+                    uint64_t tw = w[t]; w[t] = w[best]; w[best] = tw;
+                    uint64_t tr = rho[t]; rho[t] = rho[best]; rho[best] = tr;
+                }
+                part_grant(d, S, live[t]) += 1;
+            }
+            if (tot > supply) {  // block flooring (scheduler.py:653-659)
+                const int32_t bs = d.bs;
+                int64_t fsum = 0;
+                for (int32_t k = 0; k < L; k++) {
+                    const int32_t g = part_grant(d, S, live[k]);
+                    fsum += (g / bs) * bs;
+                }
+                const int64_t left_blocks = (supply - fsum) / bs;
+                for (int32_t t = 0; t < L; t++) {
+                    int32_t best = t;
+                    if (t < left_blocks) {
+                        for (int32_t k = t + 1; k < L; k++) {
+                            const int32_t gk = part_grant(d, S, live[k]), gb = part_grant(d, S, live[best]);
+                            const int32_t rk = gk - (gk / bs) * bs, rb = gb - (gb / bs) * bs;
+                            if (rk > rb || (rk == rb && id_of(k) < id_of(best))) best = k;
+                        }
+                        int32_t ti = live[t]; live[t] = live[best]; live[best] = ti;
+                    }
+                    int32_t& g = part_grant(d, S, live[t]);
+                    g = (g / bs) * bs + (t < left_blocks ? bs : 0);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    *total_out = S.b.red[0];
+    __syncthreads();
+}
+
 __device__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64_t supply, int64_t now,
                          int64_t* total_out) {
     const int tid = threadIdx.x;
     if (m == 0) { *total_out = 0; return; }  // block-uniform: nothing to split
+    if (d.inv) { amortize_inverted(d, S, grp, m, supply, now, total_out); return; }
     if (m <= 32) { amortize_warp(d, S, grp, m, supply, now, total_out); return; }
     int64_t tot = 0, live_tot = 0, nlive = 0;
     for (int32_t k = tid; k < m; k += (int)blockDim.x) {

@@ -187,13 +187,14 @@ extern "C" int co_sched_op(int32_t op, int32_t n, const int64_t* rows, const int
     for (cudaError_t x : {al(&drows, 8 * m), al(&dprm, 16), al(&dout, nout), al(&d.l_part, m), al(&d.l_grp, 2 * m),
                           al(&d.l_ful, m), al(&d.l_pro, m), al(const_cast<int32_t**>(&d.idrank), m), al(&d.am_rhi, m), al(&d.am_rlo, m), al(&d.sk0, m),
                           al(&d.sk1, m), al(&d.sk2, m), al(&d.sk_item, m), al(&d.l_part_need, m),
-                          al(&d.l_part_grant, m)})
+                          al(&d.l_part_grant, m), al(&d.big, 5 * (int64_t)co::INV_LIMBS)})
         if (x != cudaSuccess) e = x;
     int r = CO_OK;
     if (e != cudaSuccess) {
         r = fail(CO_ECUDA, std::string("sched op buffers: ") + cudaGetErrorString(e));
     } else {
         d.bs = 1;  // allocate_remaining: no block flooring
+        d.inv = op == CO_SOP_ALLOCATE_REMAINING && params[1] ? 1 : 0;  // scheduler.py:212 invert
         if (n) e = cudaMemcpy(drows, rows, 8 * n * sizeof(int64_t), cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemcpy(dprm, params, 16 * sizeof(int64_t), cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemset(dout, 0, nout * sizeof(int64_t));

@@ -324,8 +324,6 @@ class Engine:
         if cfg.sched.policy not in DEVICE_POLICIES:
             raise ValueError(f"policy {cfg.sched.policy!r} has no device implementation "
                              f"(device policies: {DEVICE_POLICIES})")
-        if cfg.sched.invert_amortization:
-            raise ValueError("invert_amortization=True is not supported by the device planner")
         self.cfg = cfg
         # the caller's Request objects, kept current like the reference's
         # in-step transitions (core.py:113-130): refreshed lazily on access
@@ -364,6 +362,7 @@ class Engine:
         c.capacity_tokens = cfg.capacity_tokens
         c.reserved_blocks = cfg.reserved_blocks
         c.allow_stacking = int(cfg.allow_stacking)
+        c.invert_amortization = int(sc.invert_amortization)  # scheduler.py:43, :233
         c.block_size = sc.small_block_b
         c.buffer_b = sc.buffer_b
         c.token_budget = sc.token_budget

@@ -184,8 +184,6 @@ def fill_token_budget(sets: CriticalSets, waiting_ordered: Sequence[ReqView], to
 def allocate_remaining(demands: Sequence[AllocDemand], a_prime: int, invert: bool = False) -> Dict[int, int]:
     if a_prime < 0:
         raise ValueError("a_prime must be >= 0")
-    if invert:
-        raise ValueError("invert=True is not supported on the device (DESIGN.md section 7)")
     ds = list(demands)
     if not ds:
         return {}
@@ -193,7 +191,7 @@ def allocate_remaining(demands: Sequence[AllocDemand], a_prime: int, invert: boo
     rows[:, 0] = _ranks([d.req_id for d in ds])
     for k, d in enumerate(ds):
         rows[k, 1:4] = (d.m_tokens, d.rt_us, d.prompt_len)
-    out = _run(SOP_ALLOCATE_REMAINING, rows, [a_prime])
+    out = _run(SOP_ALLOCATE_REMAINING, rows, [a_prime, int(bool(invert))])
     return {d.req_id: int(out[k]) for k, d in enumerate(ds) if d.m_tokens > 0}
 
 

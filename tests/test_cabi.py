@@ -72,8 +72,6 @@ def test_unsupported_modes_are_rejected_not_emulated():
     reqs = [P.Request(0, 0, 10, 3, 10**9, 10**9)]
     with pytest.raises(ValueError):
         P.Engine(reqs, P.EngineConfig(sched=P.SchedulerConfig(policy="fifo")))  # not a reference policy
-    with pytest.raises(ValueError):  # exact Fraction weights 1/(rt*p) are not restated
-        P.Engine(reqs, P.EngineConfig(sched=P.SchedulerConfig(invert_amortization=True)))
 
 
 def test_loading_the_library_before_torch_keeps_torch_importable():

@@ -135,3 +135,36 @@ def test_stacking_guest_lists_every_step(cuda_ok, seed):
         if not more:
             break
     assert most >= 3
+
+
+# invert_amortization=True (scheduler.py:43, :229-243 with weights 1/(rt*p),
+# :233): the exact multi-precision amortization (planner.cuh
+# amortize_inverted); the oracle's Fraction restatement is pinned to the
+# reference by tests/golden/inv_case* and the live cross-check
+@pytest.mark.parametrize("seed", [0, 5, 6, 7, 9, 11, 12, 15, 16, 18, 20, 25, 29])
+def test_inverted_amortization_full_run(cuda_ok, seed):
+    from paper_2503_13773_b200 import Engine
+    p = case_params(seed)
+    p["sched"] = {**p["sched"], "invert_amortization": True}
+    reqs, cfg = build_product(p)
+    eng = Engine(reqs, cfg)
+    eng.run_steps(0)
+    orc = CacheOptOracle(reqs, cfg)
+    orc.run()
+    _compare(eng, orc, f"inverted amortization seed {seed}")
+    eng.close()
+
+
+@pytest.mark.parametrize("seed", [8, 13])
+def test_inverted_amortization_with_stacking(cuda_ok, seed):
+    from paper_2503_13773_b200 import Engine
+    p = case_params(seed)
+    p["sched"] = {**p["sched"], "invert_amortization": True}
+    p["allow_stacking"] = True
+    reqs, cfg = build_product(p)
+    eng = Engine(reqs, cfg)
+    eng.run_steps(0)
+    orc = CacheOptOracle(reqs, cfg)
+    orc.run()
+    _compare(eng, orc, f"inverted amortization + stacking seed {seed}")
+    eng.close()

@@ -56,3 +56,21 @@ def test_config_slo_baselines_match_reference_calibration():
     reqs = generate(PRESETS["sharegpt"].sized(1000, 4.0), 0)
     cfg = EngineConfig(capacity_tokens=53_696, reserved_blocks=8, sched=SchedulerConfig(small_block_b=8), seed=0)
     assert calibrate_slo_baselines(copy.deepcopy(reqs), cfg) == CONFIG1_SLO
+
+
+@pytest.mark.parametrize("seed", [0, 6, 11, 16])
+def test_oracle_matches_live_reference_inverted_amortization(seed):
+    # invert_amortization=True: weights 1/(rt*p) (scheduler.py:233)
+    sys.path.insert(0, REFERENCE_SRC)
+    from kvcsim.engine import Engine
+    from oracle.cacheopt_oracle import CacheOptOracle
+    from oracle.make_golden import ref_build
+    from tests.cases import case_params
+    p = case_params(seed)
+    p["sched"] = {**p["sched"], "invert_amortization": True}
+    reqs, cfg = ref_build(p)
+    eng = Engine(copy.deepcopy(reqs), cfg)
+    eng.run()
+    orc = CacheOptOracle(reqs, cfg)
+    orc.run()
+    assert orc.events == eng.events

@@ -135,6 +135,49 @@ def test_allocate_remaining_sums_exactly_and_matches_rational_oracle(cuda_ok, n_
         assert grants == _rational(demands, a_prime)
 
 
+def _rational_inverted(demands, a_prime):
+    # scheduler.py:229-243 with invert=True (weights 1/(rt*p), :233)
+    live = [d for d in demands if d.m_tokens > 0]
+    if sum(d.m_tokens for d in live) <= a_prime:
+        return {d.req_id: d.m_tokens for d in live}
+    w = {d.req_id: 1 / Fraction(max(1, d.rt_us) * max(1, d.prompt_len)) for d in live}
+    wsum = sum(w.values())
+    shares = {i: Fraction(a_prime) * x / wsum for i, x in w.items()}
+    floors = {i: int(s) for i, s in shares.items()}
+    for i in sorted(shares, key=lambda i: (-(shares[i] - floors[i]), i))[:a_prime - sum(floors.values())]:
+        floors[i] += 1
+    return floors
+
+
+@pytest.mark.parametrize("n_max", [9, 40, 300])
+def test_allocate_remaining_inverted_matches_rational_oracle(cuda_ok, n_max):
+    # exact multi-precision path (planner.cuh amortize_inverted)
+    rng = np.random.default_rng(5)
+    for t in range(40 if n_max < 100 else 6):
+        n = int(rng.integers(1, n_max))
+        hi = [10, 1000, 10_000_000][t % 3]  # small weight ranges force duplicate weights and exact ties
+        demands = [AllocDemand(int(i), int(rng.integers(0, 500)), int(rng.integers(-5, hi)),
+                               int(rng.integers(1, 3000 if hi > 10 else 4))) for i in rng.permutation(n)]
+        a_prime = int(rng.integers(0, max(1, sum(d.m_tokens for d in demands))))
+        grants = allocate_remaining(demands, a_prime=a_prime, invert=True)
+        assert grants == _rational_inverted(demands, a_prime)
+
+
+def test_allocate_remaining_inverted_exact_ties_and_wide_weights(cuda_ok):
+    # equal weights with m | a': integer shares, no remainder; equal weights
+    # otherwise: ties broken by id; weights near 2^62 (rt*p wide)
+    same = [AllocDemand(i, 100, 50, 4) for i in (5, 2, 9, 7)]
+    assert allocate_remaining(same, a_prime=80, invert=True) == {5: 20, 2: 20, 9: 20, 7: 20}
+    assert allocate_remaining(same, a_prime=82, invert=True) == _rational_inverted(same, 82) == \
+        {5: 21, 2: 21, 9: 20, 7: 20}
+    # w = 1 and w = 2: shares 2/3 a' and 1/3 a'
+    pair = [AllocDemand(1, 1000, 1, 1), AllocDemand(2, 1000, 2, 1), AllocDemand(3, 1000, 2, 1)]
+    for a in (0, 1, 2, 3, 4, 5, 99, 100, 101):
+        assert allocate_remaining(pair, a_prime=a, invert=True) == _rational_inverted(pair, a), a
+    wide = [AllocDemand(i, 10**6, (1 << 40) + 977 * i, (1 << 22) - i) for i in range(12)]
+    assert allocate_remaining(wide, a_prime=777_777, invert=True) == _rational_inverted(wide, 777_777)
+
+
 def test_allocate_remaining_rt_scaling_invariance(cuda_ok):
     # test_scheduler.py:204-219
     rng = np.random.default_rng(4)
