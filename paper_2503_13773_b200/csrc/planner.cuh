@@ -557,11 +557,14 @@ __device__ __noinline__ void amortize_inverted(const Dev& d, PlanSh& S, int32_t*
     __syncthreads();
 }
 
+// INV: invert_amortization (a separate k_serial instantiation, so the
+// default planner's code carries no trace of the inverted path)
+template <bool INV>
 __device__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64_t supply, int64_t now,
                          int64_t* total_out) {
     const int tid = threadIdx.x;
     if (m == 0) { *total_out = 0; return; }  // block-uniform: nothing to split
-    if (d.inv) { amortize_inverted(d, S, grp, m, supply, now, total_out); return; }
+    if (INV) { amortize_inverted(d, S, grp, m, supply, now, total_out); return; }
     if (m <= 32) { amortize_warp(d, S, grp, m, supply, now, total_out); return; }
     int64_t tot = 0, live_tot = 0, nlive = 0;
     for (int32_t k = tid; k < m; k += (int)blockDim.x) {
@@ -799,6 +802,7 @@ __device__ void plan_baseline(const Dev& d, PlanSh& S, const int32_t* RUN, int32
 
 // the planner body (run by k_serial, csrc/cacheopt.cu); all threads call it
 // when the step is active
+template <bool INV>
 __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
     const Ctl& c = *d.ctl;
     const int tid = threadIdx.x;
@@ -1311,7 +1315,7 @@ __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
     __syncthreads();
     prof_mark(d, 17);
     int64_t ftot;
-    amortize(d, S, d.l_grp, n_fl, S.f_supply, now, &ftot);
+    amortize<INV>(d, S, d.l_grp, n_fl, S.f_supply, now, &ftot);
     prof_mark(d, 18);
     int64_t spent = 0;  // sum of the in-flight grants (amortize compacts grp in place)
     if (n_fl > 0) {
@@ -1328,7 +1332,7 @@ __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
     __syncthreads();
     prof_mark(d, 19);
     int64_t atot;
-    amortize(d, S, d.l_grp + n_part, n_ad, S.a_supply, now, &atot);
+    amortize<INV>(d, S, d.l_grp + n_part, n_ad, S.a_supply, now, &atot);
     prof_mark(d, 20);
     if (tid == 0) {
         S.a_total = atot;

@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(NT, 1) k_sched_op(Dev d, int32_t op, int32_t n
             }
             __syncthreads();
             int64_t tot = 0;
-            amortize(d, S, d.l_grp, n, prm[0], 0, &tot);
+            if (d.inv) amortize<true>(d, S, d.l_grp, n, prm[0], 0, &tot);
+            else amortize<false>(d, S, d.l_grp, n, prm[0], 0, &tot);
             __syncthreads();
             for (int32_t p = tid; p < n; p += (int)blockDim.x) out[p] = R(p, 1) > 0 ? (int64_t)S.pgrant[p] : -1;
             return;
