@@ -854,7 +854,8 @@ static int check_device_error(co_engine* E) {
                      : err == 8 ? "decode work-item buffer full"
                      : err == 9 ? "more decode members than the decode output buffer holds (4096)"
                      : err == 10 ? "N'_w queue extension found no candidates"
-                     : err == 11 ? "invert_amortization: more live participants in one amortized group than the "
+                     : err == 11 ? "more than 32 stacked guests on one released host"
+                     : err == 12 ? "invert_amortization: more live participants in one amortized group than the "
                                    "exact serial path takes (1024)"
                                 : "device engine error";
     snprintf(buf, sizeof(buf), "%s [code %d, info %d %d]", what, err, E->h_ctl->err_info[0], E->h_ctl->err_info[1]);

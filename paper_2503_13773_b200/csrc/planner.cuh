@@ -458,7 +458,7 @@ __device__ inline int inv_frac_cmp(InvCtx& C, uint64_t wi, uint64_t ri, uint64_t
 }
 
 // amortize() with inverted weights: thread 0 computes every grant; the block
-// waits at one barrier.  Errors (code 11) when a group holds more than
+// waits at one barrier.  Errors (code 12) when a group holds more than
 // INV_CAP live demands.
 __device__ __noinline__ void amortize_inverted(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64_t supply, int64_t now,
                                   int64_t* total_out) {
@@ -477,7 +477,7 @@ __device__ __noinline__ void amortize_inverted(const Dev& d, PlanSh& S, int32_t*
         if (L > 0 && supply > 0 && live_tot <= supply) {
             for (int32_t k = 0; k < L; k++) part_grant(d, S, live[k]) = part_need(d, S, live[k]);
         } else if (L > INV_CAP && supply > 0) {
-            if (d.ctl) { d.ctl->error = 11; d.ctl->err_info[0] = L; }
+            if (d.ctl) { d.ctl->error = 12; d.ctl->err_info[0] = L; }
         } else if (L > 0 && supply > 0) {
             Big q{d.big, 0}, A{d.big + INV_LIMBS, 0};
             InvCtx C{{d.big + 2 * INV_LIMBS, 0}, {d.big + INV_LIMBS, 0}, {d.big + 3 * INV_LIMBS, 0},
