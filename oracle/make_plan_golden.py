@@ -63,12 +63,16 @@ def main():
     from tests.cases import case_params
     rnd = random.Random(0)
     snaps = []
-    runs = [(s, None, False) for s in (0, 1, 2, 5, 13, 21)] + [(8, None, True), (27, None, True)] + \
-        [(5, "vllm_block", False), (13, "sarathi_chunked", False), (6, "rlp", False), (2, "s3", False)]
-    for seed, pol, stack in runs:
+    runs = [(s, None, False, False) for s in (0, 1, 2, 5, 13, 21)] + [(8, None, True, False), (27, None, True, False)] + \
+        [(5, "vllm_block", False, False), (13, "sarathi_chunked", False, False), (6, "rlp", False, False),
+         (2, "s3", False, False)] + \
+        [(s, None, False, True) for s in (7, 9, 12)]  # invert_amortization=True (scheduler.py:233)
+    for seed, pol, stack, inv in runs:
         p = case_params(seed)
         if pol:
             p["sched"] = {**p["sched"], "policy": pol}
+        if inv:
+            p["sched"] = {**p["sched"], "invert_amortization": True}
         p["allow_stacking"] = stack
         reqs, cfg = ref_build(p)
         got = []
@@ -79,7 +83,7 @@ def main():
             n = len(inp.waiting) + len(inp.running)
             if n <= 400 and (interesting(plan) or rnd.random() < 0.01):
                 got.append({
-                    "run": f"seed{seed}-{pol or 'cacheopt'}{'-stack' if stack else ''}",
+                    "run": f"seed{seed}-{pol or 'cacheopt'}{'-stack' if stack else ''}{'-inv' if inv else ''}",
                     "waiting": [view_doc(v) for v in inp.waiting], "running": [view_doc(v) for v in inp.running],
                     "pool": pool_doc(inp.pool), "t_i_max_us": inp.t_i_max_us,
                     "iter_cost": asdict(inp.iter_cost), "swap_model": asdict(inp.swap_model),
@@ -105,7 +109,7 @@ def main():
             take += rnd.sample(pool_f, min(2, len(pool_f), 8 - len(take)))
         rest = [d for d in got if d not in take]
         take += rnd.sample(rest, min(len(rest), 8 - len(take)))
-        print(f"seed {seed} {pol} stack={stack}: {len(got)} candidate snapshots, kept {len(take)}")
+        print(f"seed {seed} {pol} stack={stack} inv={inv}: {len(got)} candidate snapshots, kept {len(take)}")
         snaps.extend(take)
     with open(OUT, "wb") as raw, gzip.GzipFile(fileobj=raw, mode="wb", mtime=0) as fh:
         fh.write(json.dumps(snaps).encode())

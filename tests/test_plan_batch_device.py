@@ -1,8 +1,9 @@
 """plan_batch(PlannerInputs, cfg) (scheduler.py:939-950) on the device against
 BatchPlans the UNMODIFIED reference returned on the same snapshots
-(tests/golden/plan_snapshots.json.gz, oracle/make_plan_golden.py): 96
-snapshots from 12 runs -- cacheopt with preemptions, embeddings, reserve
-draws, claims and deferrals, stacking, and the four baseline policies."""
+(tests/golden/plan_snapshots.json.gz, oracle/make_plan_golden.py): 120
+snapshots from 15 runs -- cacheopt with preemptions, embeddings, reserve
+draws, claims and deferrals, stacking, invert_amortization, and the four
+baseline policies."""
 import gzip
 import json
 import os
@@ -60,10 +61,11 @@ def test_fixture_covers_the_plan_kinds():
     assert any(s["plan"]["preempt"] for s in snaps) and any(s["plan"]["claims"] for s in snaps)
     assert any(s["plan"]["deferred"] for s in snaps)
     assert {s["sched"]["policy"] for s in snaps} == {"cacheopt", "vllm_block", "sarathi_chunked", "rlp", "s3"}
+    assert sum(1 for s in snaps if s["sched"]["invert_amortization"]) >= 24
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("k", list(range(96)))
+@pytest.mark.parametrize("k", list(range(120)))
 def test_device_plan_batch_equals_reference_plan(cuda_ok, k):
     from paper_2503_13773_b200.scheduler import PlannerInputs, ReqView, plan_batch
     s = _snaps()[k]
