@@ -50,6 +50,7 @@ def main():
             if not ok:
                 bad += 1
                 print(f"MISMATCH seed {seed} {name}", flush=True)
+        print(f"seed {seed}: {tot} runs, {bad} mismatches so far, {time.time() - t0:.0f} s", flush=True)
     print(f"{tot} runs ({ns} seeds x 4 variants), {events} events, {bad} mismatches, {time.time() - t0:.0f} s")
 
 
