@@ -470,7 +470,8 @@ int co_pool_read_tables(co_pool* pool, int32_t* lens, int32_t* pages, int64_t ma
  *                      row indices of n_w, n_r, n_w', n_r' in the reference's order
  *   FILL_BUDGET        rows (chunk); params (token_budget, consumed); out (k, overflow)
  *   ALLOCATE_REMAINING rows (rank, m_tokens, rt_us, prompt_len), n <= 1024;
- *                      params (a_prime); out[k] = grant, -1 for m_tokens <= 0
+ *                      params (a_prime, invert: scheduler.py:212/:233 weights 1/(rt*p));
+ *                      out[k] = grant, -1 for m_tokens <= 0
  *   PAIR_RELEASE       rows (rank, est_remaining_iters, release_gain);
  *                      params (residual_tokens, runway_iters); out[0] = row or -1
  *   ORDER_VICTIMS      rows (rank, slo_tbt_us, remaining_tokens, occupancy);
