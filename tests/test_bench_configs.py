@@ -116,7 +116,7 @@ def test_config5_full_run_with_70b_data_plane(cuda_ok):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", [n for n in G.names() if n.startswith(("case", "base_", "inv_", "config1", "config3"))])
+@pytest.mark.parametrize("name", [n for n in G.names() if n.startswith(("case", "base_", "inv_", "stack_", "config1", "config3"))])
 def test_device_metrics_equal_reference_report(cuda_ok, name):
     """Row (f).1 pinned to the reference: Engine.run()'s device-aggregated
     MetricsReport equals the unmodified reference's eng.run().to_dict()."""
