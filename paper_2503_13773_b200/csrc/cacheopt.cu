@@ -147,7 +147,7 @@ __device__ __forceinline__ void mirror_body(const Dev& d, LogMirror* m) {
 // `pack` (a communicator is attached): N4's send slot for this step, filled
 // with the instance's [free_tokens, reserved_blocks_current] (kvc.py:92-98,
 // :79) after apply, every step whether or not it ran.
-template <int MODE, bool INV = false>
+template <int MODE, int PLAN = PLAN_CACHEOPT>
 __global__ void __launch_bounds__(NT, 1) k_serial(Dev d, LogMirror* mir, int64_t* pack, int32_t guard,
                                                   int32_t reset) {
     pdl_enter();
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(NT, 1) k_serial(Dev d, LogMirror* mir, int64_t
         __syncthreads();
     }
     if (d.ctl->active) {
-        if (MODE != 1) plan_body<INV>(d, *reinterpret_cast<PlanSh*>(serial_smem));
+        if (MODE != 1) plan_body<PLAN>(d, *reinterpret_cast<PlanSh*>(serial_smem));
         if (MODE == 2) __syncthreads();
         if (MODE != 0) apply_body(d, *reinterpret_cast<ApplySh*>(serial_smem));
     }
@@ -171,6 +171,18 @@ __global__ void __launch_bounds__(NT, 1) k_serial(Dev d, LogMirror* mir, int64_t
         pack[1] = d.ctl->rsv_cur;
     }
     if (mir) mirror_body(d, mir);
+}
+
+// the k_serial instantiation for a planning MODE (0 = plan only, 2 = plan +
+// apply) and the engine's planner configuration
+using SerialKernel = void (*)(Dev, LogMirror*, int64_t*, int32_t, int32_t);
+static SerialKernel serial_kernel(int mode, const Dev& d) {
+    const int plan = d.policy != CO_POLICY_CACHEOPT ? PLAN_BASELINES : d.inv ? PLAN_INVERTED : PLAN_CACHEOPT;
+    if (mode == 0)
+        return plan == PLAN_BASELINES ? k_serial<0, PLAN_BASELINES>
+             : plan == PLAN_INVERTED  ? k_serial<0, PLAN_INVERTED> : k_serial<0, PLAN_CACHEOPT>;
+    return plan == PLAN_BASELINES ? k_serial<2, PLAN_BASELINES>
+         : plan == PLAN_INVERTED  ? k_serial<2, PLAN_INVERTED> : k_serial<2, PLAN_CACHEOPT>;
 }
 
 struct co_engine {
@@ -324,15 +336,15 @@ static int launch_step(co_engine* E, int32_t guard, cudaEvent_t* ev = nullptr, i
     if (ev) mark(ev[3], s);  // (no bucket stage: k_classify collects the N'_w head)
     const bool io_waited = flush_io(E);  // the previous step's swap I/O, before this apply
     if (ev) {
-        launch_pdl(false, d.inv ? k_serial<0, true> : k_serial<0>, 1, E->plan_threads, sizeof(PlanSh), s, d,
-                   (LogMirror*)nullptr, (int64_t*)nullptr, guard, reset);
+        launch_pdl(false, serial_kernel(0, d), 1, E->plan_threads, sizeof(PlanSh), s, d, (LogMirror*)nullptr,
+                   (int64_t*)nullptr, guard, reset);
         mark(ev[4], s);
         launch_pdl(false, k_serial<1>, 1, E->plan_threads, sizeof(PlanSh), s, d, (LogMirror*)nullptr, pack,
                    guard, reset);
         mark(ev[5], s);
     } else {
-        launch_pdl(pdl && !io_waited, d.inv ? k_serial<2, true> : k_serial<2>, 1, E->plan_threads,
-                   sizeof(PlanSh), s, d, mir, pack, guard, reset);
+        launch_pdl(pdl && !io_waited, serial_kernel(2, d), 1, E->plan_threads, sizeof(PlanSh), s, d, mir, pack,
+                   guard, reset);
     }
     if (ev) mark(ev[6], s);  // (the validate_every check runs inside k_apply)
     if (E->comm) {
@@ -833,7 +845,7 @@ int co_create(const co_config* cfg, const co_trace* tr, const co_luts* lu, int d
         co_destroy(E);
         return fail(CO_ECUDA, "ctl upload");
     }
-    for (auto k : {k_serial<0>, k_serial<1>, k_serial<2>, k_serial<0, true>, k_serial<2, true>})
+    for (auto k : {serial_kernel(0, d), k_serial<1>, serial_kernel(2, d)})
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PlanSh));
     cudaError_t e = cudaStreamSynchronize(E->stream);
     if (e != cudaSuccess) { co_destroy(E); return fail(CO_ECUDA, cudaGetErrorString(e)); }
@@ -1483,8 +1495,8 @@ int co_plan_snapshot(co_engine* E, const int64_t* cols, const int64_t* scal, int
         k_load_snapshot_ctl<<<1, 1, 0, E->stream>>>(E->d, scal[0], scal[1], (int32_t)scal[2], scal[3], scal[4],
                                                     scal[5], scal[6], (int32_t)scal[7]);
         k_classify<<<E->d.nblk, 256, 0, E->stream>>>(E->d, 0, 1);
-        (E->d.inv ? k_serial<0, true> : k_serial<0>)<<<1, E->plan_threads, sizeof(PlanSh), E->stream>>>(
-            E->d, (LogMirror*)nullptr, (int64_t*)nullptr, 0, 1);
+        serial_kernel(0, E->d)<<<1, E->plan_threads, sizeof(PlanSh), E->stream>>>(E->d, (LogMirror*)nullptr,
+                                                                               (int64_t*)nullptr, 0, 1);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(E->stream);

@@ -802,7 +802,12 @@ __device__ void plan_baseline(const Dev& d, PlanSh& S, const int32_t* RUN, int32
 
 // the planner body (run by k_serial, csrc/cacheopt.cu); all threads call it
 // when the step is active
-template <bool INV>
+// PLAN: which planner this k_serial instantiation carries -- PLAN_CACHEOPT,
+// PLAN_INVERTED (cacheopt with invert_amortization) or PLAN_BASELINES (the
+// four baseline policies); the host launches the one matching the config
+// (csrc/cacheopt.cu serial_kernel), so each carries only its own code.
+enum : int { PLAN_CACHEOPT = 0, PLAN_INVERTED = 1, PLAN_BASELINES = 2 };
+template <int PLAN>
 __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
     const Ctl& c = *d.ctl;
     const int tid = threadIdx.x;
@@ -917,7 +922,7 @@ __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
     const bool any_ret = (fl & 1) != 0;
     auto RV = [&](int32_t k) -> PV { return rcached ? S.rv[k] : view_of(d, RUN[k]); };
 
-    if (d.policy != CO_POLICY_CACHEOPT) {
+    if (PLAN == PLAN_BASELINES) {
         plan_baseline(d, S, RUN, n_run, n_f0, n_blown, rcached, sid, ensure);
         return;
     }
@@ -1315,7 +1320,7 @@ __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
     __syncthreads();
     prof_mark(d, 17);
     int64_t ftot;
-    amortize<INV>(d, S, d.l_grp, n_fl, S.f_supply, now, &ftot);
+    amortize<PLAN == PLAN_INVERTED>(d, S, d.l_grp, n_fl, S.f_supply, now, &ftot);
     prof_mark(d, 18);
     int64_t spent = 0;  // sum of the in-flight grants (amortize compacts grp in place)
     if (n_fl > 0) {
@@ -1332,7 +1337,7 @@ __device__ __forceinline__ void plan_body(const Dev& d, PlanSh& S) {
     __syncthreads();
     prof_mark(d, 19);
     int64_t atot;
-    amortize<INV>(d, S, d.l_grp + n_part, n_ad, S.a_supply, now, &atot);
+    amortize<PLAN == PLAN_INVERTED>(d, S, d.l_grp + n_part, n_ad, S.a_supply, now, &atot);
     prof_mark(d, 20);
     if (tid == 0) {
         S.a_total = atot;

@@ -38,5 +38,6 @@ else:
     eng.run_steps(bench.WINDOW_START)
     step = (C.c_double * 3)()
     eng._dirty()
-    N.check(eng._lib.co_time_steps(eng._h, 3, bench.L2_FLUSH_BYTES, step, None), "co_time_steps")
+    flush = int(os.environ.get("FLUSH", bench.L2_FLUSH_BYTES))  # FLUSH=0: warm-L2 steps
+    N.check(eng._lib.co_time_steps(eng._h, 3, flush, step, None), "co_time_steps")
     print("steps us", [round(x * 1e3, 1) for x in step])
