@@ -13,7 +13,7 @@
 namespace co {
 
 // kvc.py:336-375 check_invariants over every record (validate_every)
-__device__ void check_pool(const Dev& d, BlkShared& sb) {
+__device__ __forceinline__ void check_pool(const Dev& d, BlkShared& sb) {
     Ctl& c = *d.ctl;
     int64_t fp = 0, bad = 0;
     for (int32_t i = threadIdx.x; i < d.n; i += (int)blockDim.x) {

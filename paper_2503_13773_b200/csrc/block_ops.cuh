@@ -33,7 +33,7 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
 }
 
 // all threads must call; every thread receives the block total
-__device__ int64_t blk_sum(int64_t v, BlkShared& s) {
+__device__ __forceinline__ int64_t blk_sum(int64_t v, BlkShared& s) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     v = warp_sum64(v);
     if (lane == 0) s.red[w] = v;
@@ -50,7 +50,7 @@ __device__ int64_t blk_sum(int64_t v, BlkShared& s) {
 }
 
 // three sums in one reduction (same barrier count as one)
-__device__ void blk_sum3(int64_t& a, int64_t& b, int64_t& c, BlkShared& s) {
+__device__ __forceinline__ void blk_sum3(int64_t& a, int64_t& b, int64_t& c, BlkShared& s) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
     a = warp_sum64(a); b = warp_sum64(b); c = warp_sum64(c);
     if (lane == 0) { s.red[w] = a; s.ured[w] = (uint64_t)b; s.t0[w] = (uint64_t)c; }
@@ -66,7 +66,7 @@ __device__ void blk_sum3(int64_t& a, int64_t& b, int64_t& c, BlkShared& s) {
     __syncthreads();
 }
 
-__device__ uint64_t blk_min(uint64_t v, BlkShared& s) {
+__device__ __forceinline__ uint64_t blk_min(uint64_t v, BlkShared& s) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     v = warp_min_u64(v);
     if (lane == 0) s.ured[w] = v;
@@ -83,7 +83,7 @@ __device__ uint64_t blk_min(uint64_t v, BlkShared& s) {
 }
 
 // exclusive prefix of a 0/1 (or small int) value across the block
-__device__ int32_t blk_excl_scan(int32_t v, int32_t* total, BlkShared& s) {
+__device__ __forceinline__ int32_t blk_excl_scan(int32_t v, int32_t* total, BlkShared& s) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int32_t x = v;
 #pragma unroll
@@ -113,7 +113,7 @@ __device__ int32_t blk_excl_scan(int32_t v, int32_t* total, BlkShared& s) {
 
 // In-place exclusive prefix sum of a[0..n) in shared memory (any n); returns
 // the total to every thread.
-__device__ int32_t blk_scan_smem(int32_t* a, int32_t n, BlkShared& s) {
+__device__ __forceinline__ int32_t blk_scan_smem(int32_t* a, int32_t n, BlkShared& s) {
     const int32_t bd = (int32_t)blockDim.x, per = (n + bd - 1) / bd;
     const int32_t lo = threadIdx.x * per, hi = min(n, lo + per);
     int32_t t = 0;
@@ -151,7 +151,7 @@ __device__ __forceinline__ int32_t blk_compact_warp(int32_t m, int32_t* dst, Ite
 }
 
 template <class Pred>
-__device__ int32_t blk_compact(const int32_t* src, int32_t m, int32_t* dst, Pred pred, BlkShared& s) {
+__device__ __forceinline__ int32_t blk_compact(const int32_t* src, int32_t m, int32_t* dst, Pred pred, BlkShared& s) {
     if (m <= 32)
         return blk_compact_warp(m, dst, [&](int32_t k) { return src ? src[k] : k; },
                                 [&](int32_t, int32_t item) { return pred(item); }, s);
@@ -176,7 +176,7 @@ __device__ int32_t blk_compact(const int32_t* src, int32_t m, int32_t* dst, Pred
 // Order-preserving compaction over positions k of src[0..m) with a predicate
 // that sees (k, src[k]); writes src[k].
 template <class Pred>
-__device__ int32_t blk_compact_at(const int32_t* src, int32_t m, int32_t* dst, Pred pred, BlkShared& s) {
+__device__ __forceinline__ int32_t blk_compact_at(const int32_t* src, int32_t m, int32_t* dst, Pred pred, BlkShared& s) {
     if (m <= 32) return blk_compact_warp(m, dst, [&](int32_t k) { return src[k]; }, pred, s);
     int32_t base = 0;
     for (int32_t c = 0; c < m; c += (int)blockDim.x) {
@@ -198,7 +198,7 @@ __device__ int32_t blk_compact_at(const int32_t* src, int32_t m, int32_t* dst, P
 // Sort items[0..m) by the unique 192-bit key kf(item, k0, k1, k2),
 // lexicographic ascending, in place (rank sort, O(m^2 / NT)).
 template <class KeyFn>
-__device__ void blk_sort(int32_t* items, int32_t m, KeyFn kf, const Dev& d, BlkShared& s) {
+__device__ __forceinline__ void blk_sort(int32_t* items, int32_t m, KeyFn kf, const Dev& d, BlkShared& s) {
     if (m <= 1) return;
     if (m <= 32) {
         // warp 0 alone: each lane ranks its key against the others by shuffles
@@ -288,7 +288,7 @@ __device__ void blk_sort(int32_t* items, int32_t m, KeyFn kf, const Dev& d, BlkS
 
 // blk_sort for a unique 64-bit key; the small case compares one word
 template <class KeyFn>
-__device__ void blk_sort_u64(int32_t* items, int32_t m, KeyFn kf, const Dev& d, BlkShared& s) {
+__device__ __forceinline__ void blk_sort_u64(int32_t* items, int32_t m, KeyFn kf, const Dev& d, BlkShared& s) {
     if (m <= 1) return;
     if (m <= 32) {
         if (threadIdx.x < 32) {

@@ -63,7 +63,7 @@ __device__ __forceinline__ void log_op(const Dev& d, const DataCfg& x, const DOp
     x.ops[c.n_ops++] = op;
 }
 // snapshot of a standalone request's first npages pages
-__device__ int64_t snap_table(const Dev& d, const DataCfg& x, int i, int32_t npages) {
+__device__ __forceinline__ int64_t snap_table(const Dev& d, const DataCfg& x, int i, int32_t npages) {
     int64_t o = snap_alloc(d, x, npages);
     if (o < 0) return 0;
     for (int32_t k = 0; k < npages; k++) x.snap[o + k] = page_of(d, i, k);
@@ -71,7 +71,7 @@ __device__ int64_t snap_table(const Dev& d, const DataCfg& x, int i, int32_t npa
 }
 // snapshot of the host pages holding a guest view [end-ntok, end);
 // returns the offset, *end_rel = end relative to the first snapshotted page
-__device__ int64_t snap_view(const Dev& d, const DataCfg& x, int h, int32_t end, int32_t ntok, int32_t* end_rel) {
+__device__ __forceinline__ int64_t snap_view(const Dev& d, const DataCfg& x, int h, int32_t end, int32_t ntok, int32_t* end_rel) {
     const int bs = d.bs;
     int32_t p0 = (end - ntok) / bs, p1 = (end - 1) / bs;
     int64_t o = snap_alloc(d, x, p1 - p0 + 1);
@@ -81,7 +81,7 @@ __device__ int64_t snap_view(const Dev& d, const DataCfg& x, int h, int32_t end,
     return o;
 }
 // where a request's tokens [0, ntok) live right now
-__device__ void snap_location(const Dev& d, const DataCfg& x, int i, int32_t ntok, int32_t* where, int64_t* snap,
+__device__ __forceinline__ void snap_location(const Dev& d, const DataCfg& x, int i, int32_t ntok, int32_t* where, int64_t* snap,
                               int32_t* end) {
     const int32_t h = d.host[i];
     *where = W_DEV;
@@ -94,7 +94,7 @@ __device__ void snap_location(const Dev& d, const DataCfg& x, int i, int32_t nto
 }
 
 // swap-out at preemption (before the pool release)
-__device__ void log_swap_out(const Dev& d, const DataCfg& x, int i) {
+__device__ __forceinline__ void log_swap_out(const Dev& d, const DataCfg& x, int i) {
     const int32_t ntok = d.used[i];
     if (!x.on || ntok <= 0 || !d.holds[i]) return;
     DataCtl& c = dctl(d);
@@ -123,7 +123,7 @@ __device__ void log_swap_out(const Dev& d, const DataCfg& x, int i) {
     log_op(d, x, op);
 }
 // readmission: swap-in of the restored prefix or its recompute
-__device__ void log_readmit(const Dev& d, const DataCfg& x, int i, bool swap) {
+__device__ __forceinline__ void log_readmit(const Dev& d, const DataCfg& x, int i, bool swap) {
     if (!x.on) return;
     DataCtl& c = dctl(d);
     const int32_t ntok = d.used[i];
@@ -160,7 +160,7 @@ __device__ void log_readmit(const Dev& d, const DataCfg& x, int i, bool swap) {
 }
 // guest g leaves the view (end) in host h's pages for its own table:
 // call with the view snapshot taken BEFORE the pages moved
-__device__ void log_move(const Dev& d, const DataCfg& x, int g, int32_t ntok, int64_t src_snap, int32_t src_end) {
+__device__ __forceinline__ void log_move(const Dev& d, const DataCfg& x, int g, int32_t ntok, int64_t src_snap, int32_t src_end) {
     if (!x.on || ntok <= 0) return;
     DOp op;
     op.kind = D_MOVE; op.req = g; op.ntok = ntok; op.t0 = 0;
@@ -171,7 +171,7 @@ __device__ void log_move(const Dev& d, const DataCfg& x, int g, int32_t ntok, in
     log_op(d, x, op);
 }
 // KV written by this iteration for tokens [t0, t0+n) of request i
-__device__ void log_fill(const Dev& d, const DataCfg& x, int i, int32_t t0, int32_t n) {
+__device__ __forceinline__ void log_fill(const Dev& d, const DataCfg& x, int i, int32_t t0, int32_t n) {
     if (!x.on || n <= 0) return;
     DOp op;
     op.kind = D_FILL; op.req = i; op.ntok = n; op.t0 = t0;

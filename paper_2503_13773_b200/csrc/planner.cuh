@@ -56,7 +56,7 @@ struct PlanSh {
 // `want` (at most XCHUNK) items come in.  A block-wide pass over the live
 // slots re-derives membership with k_classify's own wait_class; used when
 // the step needs more of the queue than k_classify's candidate head.
-__device__ int32_t nwp_extend(const Dev& d, PlanSh& S, int32_t want, int64_t now, int64_t ti, int64_t eps) {
+__device__ __forceinline__ int32_t nwp_extend(const Dev& d, PlanSh& S, int32_t want, int64_t now, int64_t ti, int64_t eps) {
     const Ctl& c = *d.ctl;
     const int tid = threadIdx.x, bd = (int)blockDim.x;
     const uint64_t lo = S.lo_key;
@@ -149,7 +149,7 @@ __device__ __forceinline__ void push_mem(const Dev& d, PlanSh& S, int32_t i, int
 // places the new one below its lowest guest (end = min offset <= a_j), so it
 // additionally needs (end - u_j) >= b + need + out; every entry before the
 // lower bound is infeasible either way, so the scan stays exact.
-__device__ bool try_embed(const Dev& d, PlanSh& S, const PV& v, int32_t n_tri, int32_t sid) {
+__device__ __forceinline__ bool try_embed(const Dev& d, PlanSh& S, const PV& v, int32_t n_tri, int32_t sid) {
     const int32_t i = v.i;
     if (v.eff > 0 || v.pcount > 0) return false;
     int32_t out = v.er > v.pg ? v.er : v.pg;
@@ -274,7 +274,7 @@ __device__ __forceinline__ int64_t amortize_lane_wide(const Dev& d, const PV& v,
 // fits 62 bits, so q = floor(supply w / W) (< supply < 2^31) comes from a
 // double estimate corrected by exact 64-bit wrap-around remainders (the true
 // remainder lies in (-2W, 2W)): no 128-bit arithmetic, no 64-bit division.
-__device__ void amortize_warp(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64_t supply, int64_t now,
+__device__ __forceinline__ void amortize_warp(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64_t supply, int64_t now,
                               int64_t* total_out) {
     const int lane = threadIdx.x & 31;
     if (threadIdx.x < 32) {
@@ -560,7 +560,7 @@ __device__ __noinline__ void amortize_inverted(const Dev& d, PlanSh& S, int32_t*
 // INV: invert_amortization (a separate k_serial instantiation, so the
 // default planner's code carries no trace of the inverted path)
 template <bool INV>
-__device__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64_t supply, int64_t now,
+__device__ __forceinline__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64_t supply, int64_t now,
                          int64_t* total_out) {
     const int tid = threadIdx.x;
     if (m == 0) { *total_out = 0; return; }  // block-uniform: nothing to split
@@ -673,7 +673,7 @@ __device__ void amortize(const Dev& d, PlanSh& S, int32_t* grp, int32_t m, int64
 // queue (classify keyed it FCFS, preempted first, or by rlp's bucket), so
 // thread 0 runs them; the queue is materialized in 256-item groups.
 template <class Ensure>
-__device__ void plan_baseline(const Dev& d, PlanSh& S, const int32_t* RUN, int32_t n_run, int32_t n_f0,
+__device__ __forceinline__ void plan_baseline(const Dev& d, PlanSh& S, const int32_t* RUN, int32_t n_run, int32_t n_f0,
                               int32_t n_blown, bool rcached, int32_t sid, Ensure& ensure) {
     const int tid = threadIdx.x, bs = d.bs, pol = d.policy;
     const bool vllm = pol == CO_POLICY_VLLM_BLOCK || pol == CO_POLICY_SARATHI_CHUNKED;

@@ -63,7 +63,7 @@ __device__ __forceinline__ void drop_record(const Dev& d, int i) {
 }
 
 // kvc.py:156-167
-__device__ bool pool_allocate(const Dev& d, int i, int64_t n) {
+__device__ __forceinline__ bool pool_allocate(const Dev& d, int i, int64_t n) {
     if (n < 1 || d.holds[i]) return false;
     int64_t fp = fp_tokens(n, d.bs);
     if (fp > free_tokens(d)) return false;
@@ -87,7 +87,7 @@ __device__ __forceinline__ void guest_unlink(const Dev& d, int h, int i) {
 }
 
 // kvc.py:202-227
-__device__ bool pool_embed(const Dev& d, int i, int64_t n, int h, int64_t start) {
+__device__ __forceinline__ bool pool_embed(const Dev& d, int i, int64_t n, int h, int64_t start) {
     if (n < 1 || d.holds[i] || !d.holds[h]) return false;
     if (d.host[h] >= 0 || i == h) return false;
     if (d.guest[h] >= 0 && !d.stacking) return false;
@@ -103,7 +103,7 @@ __device__ bool pool_embed(const Dev& d, int i, int64_t n, int h, int64_t start)
 }
 
 // kvc.py:229-249
-__device__ bool pool_draw_reserved(const Dev& d, int i, int32_t nb) {
+__device__ __forceinline__ bool pool_draw_reserved(const Dev& d, int i, int32_t nb) {
     Ctl& c = *d.ctl;
     if (nb < 1 || nb > c.rsv_cur) return false;
     if (!d.holds[i]) new_record(d, i, 0, -1, 0);
@@ -122,7 +122,7 @@ __device__ bool pool_draw_reserved(const Dev& d, int i, int32_t nb) {
 }
 
 // kvc.py:251-281
-__device__ bool pool_grow(const Dev& d, int i, int64_t n) {
+__device__ __forceinline__ bool pool_grow(const Dev& d, int i, int64_t n) {
     if (n < 1 || !d.holds[i]) return false;
     Ctl& c = *d.ctl;
     int64_t g = d.granted[i];
@@ -152,7 +152,7 @@ __device__ bool pool_grow(const Dev& d, int i, int64_t n) {
 }
 
 // kvc.py:283-297
-__device__ bool pool_promote(const Dev& d, int i) {
+__device__ __forceinline__ bool pool_promote(const Dev& d, int i) {
     int64_t fp = fp_tokens(d.granted[i], d.bs);
     if (fp > free_tokens(d)) return false;
     int32_t h = d.host[i];
@@ -170,7 +170,7 @@ __device__ bool pool_promote(const Dev& d, int i) {
 }
 
 // kvc.py:299-324
-__device__ void pool_release(const Dev& d, int i) {
+__device__ __forceinline__ void pool_release(const Dev& d, int i) {
     Ctl& c = *d.ctl;
     int32_t h = d.host[i];
     if (h >= 0) {
@@ -243,7 +243,7 @@ __device__ __forceinline__ void emit_event(const Dev& d, int32_t kind, int32_t i
 __device__ __forceinline__ bool live_state(int8_t s) { return s >= ST_WAITING && s <= ST_PREEMPTED; }
 
 // engine.py:360-384
-__device__ void do_preempt(const Dev& d, int i, int32_t strat, int64_t now, int32_t cause) {
+__device__ __forceinline__ void do_preempt(const Dev& d, int i, int32_t strat, int64_t now, int32_t cause) {
     if (d.state[i] != ST_RUNNING) return;
     d.state[i] = ST_PREEMPTED;
     d.key0[i] = wait_key(d, i);  // its waiting-queue key (D = last token + TBT SLO)
@@ -265,7 +265,7 @@ __device__ void do_preempt(const Dev& d, int i, int32_t strat, int64_t now, int3
 }
 
 // engine.py:386-402
-__device__ void do_readmit(const Dev& d, int i) {
+__device__ __forceinline__ void do_readmit(const Dev& d, int i) {
     const int64_t now = d.ctl->now;
     d.state[i] = ST_RUNNING;
     int64_t restored = d.prefill[i] > 1 ? d.prefill[i] : 1;
@@ -290,7 +290,7 @@ __device__ __forceinline__ bool claim_valid(const Dev& d, int p) {
 }
 
 // engine.py:419-433
-__device__ void fulfill_claim(const Dev& d, int w) {
+__device__ __forceinline__ void fulfill_claim(const Dev& d, int w) {
     if (d.state[w] != ST_RUNNING || !d.holds[w]) return;
     int64_t target = target_of(d, w);
     int64_t residual = target - d.granted[w];
@@ -298,7 +298,7 @@ __device__ void fulfill_claim(const Dev& d, int w) {
 }
 
 // engine.py:404-417
-__device__ void do_complete(const Dev& d, int i, int64_t now) {
+__device__ __forceinline__ void do_complete(const Dev& d, int i, int64_t now) {
     d.state[i] = ST_COMPLETED;
     d.completion[i] = now;
     if (d.holds[i]) pool_release(d, i);
