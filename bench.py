@@ -40,7 +40,7 @@ STAGE_KERNEL = {"plan": "k_serial", "apply": "k_serial", "plan+apply": "k_serial
                 "begin+admit": "k_begin", "decode": "k_decode_tc05", "data": "k_data"}
 
 
-E2E_REPS = 3
+E2E_REPS = 5
 _RESULT_FD = None  # the real stdout while native libraries' banners are routed to stderr
 
 
@@ -608,7 +608,7 @@ def device_arm(args, rank, world, dist):
         e.close()
         return el, dec, d2h, nev
 
-    # the window is only K steps of ~70 us of host wall clock each: three
+    # the window is only K steps of ~70 us of host wall clock each: E2E_REPS
     # fresh repetitions per variant, the median one reported
     def median_run(drain):
         runs = sorted((e2e_run(drain) for _ in range(E2E_REPS)), key=lambda r: r[0] / max(r[1], 1))
