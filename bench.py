@@ -17,6 +17,7 @@ collective); time = max over ranks, value = sum of decisions / that time.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -231,6 +232,7 @@ def run_cpu_baseline(reqs, cfg, k: int, warmup: int, budget_s: float = 10.0, max
     reps = 0
     while reps < max_reps and (reps == 0 or t_sum < budget_s):
         o = copy.deepcopy(snap)
+        gc.collect()  # as the device arm's e2e: no collection of earlier garbage inside the window
         for _ in range(k):
             live0, pend0 = o.n_live, o.next_pending
             t0 = time.perf_counter()
@@ -588,6 +590,7 @@ def device_arm(args, rank, world, dist):
         e.prepare_step()  # instantiate the single-step graph outside the timed loop
         e.step_result()   # (one untimed step builds the host-side result buffers)
         e.events
+        gc.collect()  # the harness's own garbage (traces, earlier instances) collected before, not inside, the window
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
