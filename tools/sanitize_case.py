@@ -4,7 +4,7 @@ plane (k_data swaps/moves/fills, cooperative launch), the tcgen05 decode +
 split-KV combine, device metrics and the trace generator -- with parity vs
 the oracle checked at the end so a sanitizer-clean run is also a correct one.
 
-  python tools/sanitize_case.py sched|data"""
+  python tools/sanitize_case.py sched|data|stack|invert [seed] [max_steps]"""
 import os
 import sys
 
@@ -19,6 +19,8 @@ max_steps = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # 0: to the end
 params = case_params(seed)
 if mode == "stack":  # several guests per host; their re-homing goes through the grouped MOVE staging
     params["allow_stacking"] = True
+if mode == "invert":  # invert_amortization=True: the multi-precision amortization (k_serial<., PLAN_INVERTED>)
+    params["sched"] = {**params["sched"], "invert_amortization": True}
 reqs, cfg = build_product(params)
 kv = None
 if mode in ("data", "stack"):
