@@ -241,6 +241,11 @@ typedef struct co_step_args {
     int64_t* counts;
     int32_t drain;  /* 0: co_step_result, 1: co_step_result_log */
     int32_t _pad;
+    /* optional: with both set, the iteration's members are also written as
+     * (ids[idx], tokens) int64 pairs (the caller's request ids by sorted
+     * position), max_members pairs at most; members may then be NULL */
+    const int64_t* ids;
+    int64_t* members_ids;
 } co_step_args;
 int co_step_packed(const co_step_args* args);
 /* Undrained append-log sizes in one call: out[0] events, out[1] iteration

@@ -81,7 +81,7 @@ class CoStepArgs(C.Structure):  # include/cacheopt.h co_step_args
                 ("n_members", C.c_void_p), ("iter_end_us", C.c_void_p), ("events", C.c_void_p),
                 ("max_events", C.c_int64), ("log_members", C.c_void_p), ("max_log_members", C.c_int64),
                 ("samples", C.c_void_p), ("max_samples", C.c_int64), ("counts", C.c_void_p), ("drain", C.c_int32),
-                ("_pad", C.c_int32)]
+                ("_pad", C.c_int32), ("ids", C.c_void_p), ("members_ids", C.c_void_p)]
 
 
 class CoEvent(C.Structure):

@@ -1015,11 +1015,22 @@ int co_step_result_log(co_engine* E, int32_t* result, int32_t* members, int64_t 
 
 int co_step_packed(const co_step_args* a) {
     if (!a) return fail(CO_EINVAL, "null argument");
-    if (!a->drain)
-        return co_step_result(a->eng, a->result, a->members, a->max_members, a->n_members, a->iter_end_us);
-    return co_step_result_log(a->eng, a->result, a->members, a->max_members, a->n_members, a->iter_end_us,
-                              a->events, a->max_events, a->log_members, a->max_log_members, a->samples,
-                              a->max_samples, a->counts);
+    // the step itself; a CO_EAGAIN from the log drain still leaves the step's result valid
+    const int r = !a->drain
+        ? co_step_result(a->eng, a->result, a->members, a->max_members, a->n_members, a->iter_end_us)
+        : co_step_result_log(a->eng, a->result, a->members, a->max_members, a->n_members, a->iter_end_us,
+                             a->events, a->max_events, a->log_members, a->max_log_members, a->samples,
+                             a->max_samples, a->counts);
+    if ((r == CO_OK || r == CO_EAGAIN) && a->ids && a->members_ids) {
+        // (req_id, tokens) pairs straight from the mapped result (valid until the next step)
+        const int32_t* res = static_cast<const int32_t*>(a->eng->result_host) + 4;
+        const int64_t n = *a->n_members;
+        for (int64_t j = 0; j < n; j++) {
+            a->members_ids[2 * j] = a->ids[res[2 * j]];
+            a->members_ids[2 * j + 1] = res[2 * j + 1];
+        }
+    }
+    return r;
 }
 
 int co_step(co_engine* E, int32_t* result) {

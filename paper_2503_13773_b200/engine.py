@@ -482,15 +482,16 @@ class Engine:
         into the host lists, so `events` then has nothing left to fetch."""
         drain = bool(drain and self.cfg.record_events)
         if self._resbuf is None:
-            self._resbuf = np.empty(2 * (3 * self._n + 64), dtype=np.int32)
+            self._resbuf = np.empty(2 * (3 * self._n + 64), dtype=np.int64)  # (req_id, tokens) pairs
             self._sr_out = (C.c_int32(), C.c_int64(), C.c_int64())
         if drain and self._evbuf is None:
             self._drain()  # sizes the host log buffers once
         sa = self._step_args.get(drain)
         if sa is None:
             r, n, end = self._sr_out
-            a = N.CoStepArgs(eng=self._h.value, result=C.addressof(r), members=self._resbuf.ctypes.data,
+            a = N.CoStepArgs(eng=self._h.value, result=C.addressof(r), members=None,
                              max_members=len(self._resbuf) // 2, n_members=C.addressof(n),
+                             ids=self._rid_np.ctypes.data, members_ids=self._resbuf.ctypes.data,
                              iter_end_us=C.addressof(end), drain=int(drain))
             if drain:
                 a.events, a.max_events = self._ev_addr, len(self._evbuf)
@@ -515,10 +516,7 @@ class Engine:
         elif rc:
             N.check(rc, "co_step_packed")
         k = n.value
-        out = self._resbuf[:2 * k].reshape(k, 2).astype(np.int64)
-        if k:
-            out[:, 0] = self._rid_np[out[:, 0]]
-        return bool(r.value), out, int(end.value)
+        return bool(r.value), self._resbuf[:2 * k].reshape(k, 2).copy(), int(end.value)
 
     def run_steps(self, max_steps: int = 0, steps_per_launch: Optional[int] = None) -> int:
         """Device loop with the run() progress guard; returns step() calls."""
