@@ -65,14 +65,16 @@ def test_config2_first_60_steps(cuda_ok):
     _compare(eng, orc, "config2")
 
 
-@pytest.mark.parametrize("seed", [4, 8])
-def test_step_result_members_match_iter_events(cuda_ok, seed):
+@pytest.mark.parametrize("seed,drain", [(4, True), (8, True), (4, False)])
+def test_step_result_members_match_iter_events(cuda_ok, seed, drain):
+    # the (req_id, tokens) pairs the library writes per step (co_step_args
+    # ids / members_ids) against the iter events, with and without the drain
     from paper_2503_13773_b200 import Engine
     reqs, cfg = build_product(case_params(seed))
     eng = Engine(reqs, cfg)
     got = []
     while True:
-        more, members, end = eng.step_result()
+        more, members, end = eng.step_result(drain=drain)
         if len(members):
             got.append((end, members.tolist()))
         if not more:
