@@ -476,7 +476,7 @@ class Engine:
 
     def step_result(self, drain: bool = True):
         """step() plus this iteration's result in one device round trip:
-        (step()'s bool, int32 array [m, 2] of (req_id, tokens) that ran, end_us).
+        (step()'s bool, int64 array [m, 2] of (req_id, tokens) that ran, end_us).
         With `drain` (default) the step's event log and utilization sample
         come back in the same library call (co_step_packed -> co_step_result_log)
         into the host lists, so `events` then has nothing left to fetch."""
